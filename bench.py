@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark of the decentralized CD hot path on B200 (BASELINE.json metric:
+"CD detect/precode throughput (Gbps) & batch latency, B=256 U=16 C=8").
+
+Workload (configs[1]): uplink CD L-MMSE detection, B=256 antennas in C=8
+clusters of B_c=32, U=16 users, 16-QAM, K=3 sweeps, fp32, uniform fusion;
+one batch = 1200 subcarriers x 14 OFDM symbols = 16,800 subcarrier-symbol
+problems per GPU-cluster-set.  Gbps = S * U * log2(Q) / t_batch (the paper's
+definition).
+
+N GPUs (torchrun, one process per GPU): the 8 clusters are partitioned over
+the ranks (C/N per rank) and every rank processes S = 16,800*N subcarriers of
+its clusters (weak scaling: per-GPU work fixed); the partial fused estimates
+are reduce-scattered over the subcarrier axis (NCCL), so each rank ends with
+the fused estimates of S/N subcarriers.
+
+  value  device-resident throughput (inputs in HBM, CUDA events, max over
+         ranks); the batch (602 MB/GPU) is larger than L2 (126 MB).
+  e2e    same metric through Engine.ul_detect with pinned HOST buffers: H2D of
+         the batch's H and y + detection + D2H of the fused estimates.
+  --impl reference   the reference's CPU implementation (oracle/_ref, built
+         from /root/reference sources) on this host's cores, same config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B, C, U, QAM, K_SWEEPS = 256, 8, 16, 16, 3
+BC = B // C
+S_PER_GPU = 1200 * 14
+SNR_DB = 10.0
+BITS = int(math.log2(QAM))
+METRIC = "CD detect/precode throughput (Gbps) & batch latency, B=256 U=16 C=8, 1-8 GPUs"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def alg_bytes_per_problem(bc, u, esz):
+    """(B_c*U + B_c + U) * bytes-per-complex per cluster-problem."""
+    return (bc * u + bc + u) * esz
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                f = [x.strip() for x in out.stdout.strip().split(",")]
+                if len(f) >= 6:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs (device-side, torch RNG; same distribution as the
+# reference's make_batch: H ~ CN(0,1), Gray 16-QAM at unit energy, AWGN N0)
+# ---------------------------------------------------------------------------
+def make_inputs(S, c_local, device, seed):
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    n0 = U * 1.0 / 10 ** (SNR_DB / 10)
+    H = torch.randn((S, c_local, U, BC), dtype=torch.complex64, device=device, generator=g)  # CN(0,1)
+    lv = torch.tensor([-3.0, -1.0, 1.0, 3.0], device=device) / math.sqrt(10.0)
+    idx = torch.randint(0, 4, (S, U, 2), device=device, generator=g)
+    x = torch.complex(lv[idx[..., 0]], lv[idx[..., 1]])
+    noise = torch.randn((S, c_local, BC), dtype=torch.complex64, device=device, generator=g) * math.sqrt(n0)
+    y = torch.einsum("scub,su->scb", H, x) + noise
+    return H.contiguous(), y.contiguous(), x.contiguous(), n0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1902_08653_b200 import Engine, kernel_name, to_fp16
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if C % world:
+        raise SystemExit(f"C={C} clusters cannot be split over {world} GPUs")
+    c_local = C // world
+    S = args.S * world  # weak scaling: per-GPU problems fixed at args.S * C
+    fmt = args.fmt
+    esz = 8 if fmt == "fp32" else 4
+    eng = Engine(local_rank)
+
+    H, y, xs, n0 = make_inputs(S, c_local, dev, 1234 + rank)
+    if fmt == "fp16":
+        H, y = to_fp16(H), to_fp16(y)
+    P = S * c_local
+    xhat = torch.empty((S, U), dtype=torch.complex64, device=dev)
+    x_local = torch.empty((S, c_local, U), dtype=torch.complex64, device=dev) if fmt == "fp32" else \
+        torch.empty((S, c_local, U, 2), dtype=torch.float16, device=dev)
+    out_rs = torch.empty((S // world, U), dtype=torch.complex64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        eng.ul_detect(H, y, n0=n0, K=K_SWEEPS, fusion=args.fusion, C_total=C, x_local=x_local, xhat=xhat)
+        if world > 1:
+            dist.reduce_scatter_tensor(torch.view_as_real(out_rs), torch.view_as_real(xhat))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    eng.sync()
+    barrier()
+    l0 = eng.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    launches = (eng.launches - l0) // max(args.steps, 1)
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = S * U * BITS / (ms * 1e-3) / 1e9  # whole-job Gbps (S subcarriers fused per step)
+
+    # dominant kernel alone (the CD kernel, on the same stream), for the roofline
+    for _ in range(3):
+        eng.ul_detect(H, y, n0=n0, K=K_SWEEPS, fusion="uniform", C_total=C, x_local=x_local, want_xhat=False)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nk = max(args.steps, 5)
+    torch.cuda.synchronize(dev)
+    k0.record(stream)
+    for _ in range(nk):
+        eng.ul_detect(H, y, n0=n0, K=K_SWEEPS, fusion="uniform", C_total=C, x_local=x_local, want_xhat=False)
+    k1.record(stream)
+    torch.cuda.synchronize(dev)
+    k_ms = k0.elapsed_time(k1) / nk
+    hbm, hbm_src = peaks()
+    achieved = P * alg_bytes_per_problem(BC, U, esz) / (k_ms * 1e-3) / 1e9
+
+    # e2e through the public API with pinned host buffers
+    e2e = None
+    if rank == 0 or world > 1:
+        Hh = H.cpu().pin_memory()
+        yh = y.cpu().pin_memory()
+        xh = torch.empty((S, U), dtype=torch.complex64).pin_memory()
+        Hd, yd = torch.empty_like(H), torch.empty_like(y)
+
+        def e2e_step():
+            Hd.copy_(Hh, non_blocking=True)
+            yd.copy_(yh, non_blocking=True)
+            eng.ul_detect(Hd, yd, n0=n0, K=K_SWEEPS, fusion=args.fusion, C_total=C, x_local=x_local, xhat=xhat)
+            if world > 1:
+                dist.reduce_scatter_tensor(torch.view_as_real(out_rs), torch.view_as_real(xhat))
+                xh[: S // world].copy_(out_rs, non_blocking=True)
+            else:
+                xh.copy_(xhat, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        n_e2e = max(2, min(args.steps, 5))
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        t1.record(stream)
+        barrier()
+        e_ms = t0.elapsed_time(t1) / n_e2e
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        h2d = H.numel() * H.element_size() + y.numel() * y.element_size()
+        d2h = (S // world) * U * 8
+        e2e = {"value": S * U * BITS / (e_ms * 1e-3) / 1e9, "unit": "Gbps", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "path": "Engine.ul_detect (C ABI dcdg_ul_detect) with pinned host H,y -> device -> host xhat"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp))
+            key = f"ul_{fmt}_{BC}_{U}"
+            if key in tj:
+                traffic = tj[key]["dram_bytes_per_problem"] * P
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC,
+        "value": round(value, 4),
+        "unit": "Gbps",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32" if fmt == "fp32" else "f16",
+        "data": "synthetic: CN(0,1) Rayleigh H, Gray 16-QAM, AWGN at 10 dB, generated on device (torch RNG)",
+        "config": {"workload": "uplink CD L-MMSE detection + uniform fusion (configs[1])" if args.fusion == "uniform"
+                   else "uplink CD L-MMSE detection + optimal fusion",
+                   "B": B, "U": U, "C": C, "B_c": BC, "K": K_SWEEPS, "qam": QAM, "fmt": fmt,
+                   "subcarrier_symbols_per_step": S, "problems_per_gpu": P, "clusters_per_gpu": c_local,
+                   "parallelism": f"clusters/{world}" if world > 1 else "single GPU, all clusters",
+                   "l2": f"inputs {P * alg_bytes_per_problem(BC, U, esz) / 1e6:.0f} MB/GPU > 126 MB L2, no flush needed",
+                   "kernel": kernel_name("ul", BC, U, fmt)},
+        "batch_latency_ms": round(ms, 5),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_source": hbm_src,
+                     "kernel_ms": round(k_ms, 5),
+                     "alg_bytes_per_launch": P * alg_bytes_per_problem(BC, U, esz)},
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (the unmodified reference library, oracle/_ref)
+# ---------------------------------------------------------------------------
+def _ref_lib():
+    from oracle.oracle import Oracle, available
+    if not available("reference"):
+        return None
+    return Oracle("reference")
+
+
+def cpu_inputs(S, seed=5):
+    rng = np.random.default_rng(seed)
+    n0 = U * 1.0 / 10 ** (SNR_DB / 10)
+    H = (rng.standard_normal((S, C, U, BC)) + 1j * rng.standard_normal((S, C, U, BC))) / math.sqrt(2)
+    lv = np.array([-3.0, -1.0, 1.0, 3.0]) / math.sqrt(10.0)
+    x = lv[rng.integers(0, 4, (S, U))] + 1j * lv[rng.integers(0, 4, (S, U))]
+    y = np.einsum("scub,su->scb", H, x) + math.sqrt(n0 / 2) * (
+        rng.standard_normal((S, C, BC)) + 1j * rng.standard_normal((S, C, BC)))
+    return np.ascontiguousarray(H), np.ascontiguousarray(y), n0
+
+
+def cpu_time_ref(S, threads, reps=1):
+    import ctypes as Ct
+    o = _ref_lib()
+    H, y, n0 = cpu_inputs(S)
+    L = o.lib
+    dp = Ct.POINTER(Ct.c_double)
+    h = L.dcdref_ul_batch_create(S, C, BC, U, H.ctypes.data_as(dp), y.ctypes.data_as(dp))
+    try:
+        ts = []
+        for _ in range(reps):
+            t = L.dcdref_ul_batch_run(h, n0, 1.0, K_SWEEPS, 1, 0, 0, threads, 0, S, None)
+            if t < 0:
+                raise RuntimeError(L.dcdref_last_error().decode())
+            ts.append(t)
+        return ts, o.backend()
+    finally:
+        L.dcdref_ul_batch_destroy(h)
+
+
+def cpu_baseline(target_s=10.0):
+    threads = os.cpu_count() or 1
+    if _ref_lib() is None:
+        return {"value": None, "unit": "Gbps", "cores": threads, "kind": "reference",
+                "sample": "oracle/_ref/libdcdref.so missing"}
+    # calibrate, then size the sample to ~target_s seconds of all-core work
+    t, _ = cpu_time_ref(240 * threads, threads)
+    per_sc = t[0] / (240 * threads)
+    S = int(min(max(target_s / per_sc, 480), 200000))
+    ts, backend = cpu_time_ref(S, threads)
+    return {"value": round(S * U * BITS / ts[0] / 1e9, 6), "unit": "Gbps", "cores": threads, "kind": "reference",
+            "sample": f"{S} subcarrier-symbols x C={C} clusters, decentralized_cd_detect (uniform fusion, K=3) "
+                      f"over {threads} std::threads, {ts[0]:.2f} s, reference kernels backend={backend}",
+            "seconds": round(ts[0], 3)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    if _ref_lib() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdcdref.so not built"}))
+        return
+    t, _ = cpu_time_ref(120 * threads, threads)
+    per_sc = t[0] / (120 * threads)
+    budget = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.5)
+    S = int(min(max(budget / per_sc, 240), 200000))
+    ts, backend = cpu_time_ref(S, threads, reps=args.warmup + args.steps)
+    timed = ts[args.warmup:]
+    sec = sum(timed) / len(timed)
+    value = S * U * BITS / sec / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 6), "unit": "Gbps", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic CN(0,1) H / 16-QAM / AWGN (numpy), host-resident",
+        "config": {"workload": "uplink CD L-MMSE detection + uniform fusion (configs[1])", "B": B, "U": U, "C": C,
+                   "B_c": BC, "K": K_SWEEPS, "qam": QAM, "subcarrier_symbols_per_step": S},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gbps", "cores": threads, "kind": "reference",
+                         "sample": f"{S} subcarrier-symbols per step, decentralized_cd_detect over {threads} threads, "
+                                   f"backend={backend}"},
+        "e2e": {"value": round(value, 6), "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--fmt", choices=["fp32", "fp16"], default="fp32")
+    ap.add_argument("--fusion", choices=["uniform", "optimal"], default="uniform")
+    ap.add_argument("--S", type=int, default=S_PER_GPU, help="subcarrier-symbols per GPU per step")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

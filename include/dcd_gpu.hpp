@@ -1,0 +1,195 @@
+/**
+ * @file dcd_gpu.hpp
+ * @brief C++ host API of the B200 decentralized CD baseband — the drop-in
+ *        surface for the reference's dcd/detect.hpp and dcd/precode.hpp.
+ *
+ * Same names, argument meaning and exception behaviour as the reference
+ * (paths relative to /root/reference/proj):
+ *   dcd::gpu::cd_detect                 <- dcd::cd_detect                include/dcd/detect.hpp:60-63
+ *   dcd::gpu::post_eq_variance          <- dcd::post_eq_variance         include/dcd/detect.hpp:67
+ *   dcd::gpu::fusion_weights            <- dcd::fusion_weights           include/dcd/detect.hpp:70
+ *   dcd::gpu::decentralized_cd_detect   <- dcd::decentralized_cd_detect  include/dcd/detect.hpp:84-86
+ *   dcd::gpu::cd_precode                <- dcd::cd_precode               include/dcd/precode.hpp:58-60
+ *   dcd::gpu::power_scale               <- dcd::power_scale              include/dcd/precode.hpp:63
+ *   dcd::gpu::decentralized_cd_precode  <- dcd::decentralized_cd_precode include/dcd/precode.hpp:72-75
+ * plus the batched device API (UplinkBatch / DownlinkBatch) the reference's
+ * per-subcarrier loops (src/cluster.cpp:138,239) become.
+ *
+ * Arithmetic: the GPU computes natively in fp32 (PrecisionFormat fp64 and
+ * fp32) or in half2 (fp16, both scopes); it does not emulate binary64.
+ * Results agree with the reference within 1e-5 (fp32) / 2e-2 (fp16) relative.
+ *
+ * Errors: std::invalid_argument / std::runtime_error with the reference's
+ * messages.  There is no CPU fallback: without a CUDA device every call
+ * throws std::runtime_error.  A non-null SweepObserver is rejected with
+ * std::invalid_argument (per-update host hooks cannot run on the GPU).
+ */
+#pragma once
+
+#include <complex>
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <vector>
+
+#include "dcdg.h"
+
+namespace dcd::gpu {
+
+using cf64 = std::complex<double>;
+using ComplexVector = std::vector<cf64>;
+
+/// Column-major complex matrix with the reference's interface
+/// (include/dcd/numerics.hpp:23-53).
+class ComplexMatrix {
+ public:
+  ComplexMatrix() = default;
+  ComplexMatrix(std::size_t rows, std::size_t cols) : rows_(rows), cols_(cols), data_(rows * cols) {}
+  static ComplexMatrix identity(std::size_t n);
+
+  std::size_t rows() const { return rows_; }
+  std::size_t cols() const { return cols_; }
+  bool empty() const { return data_.empty(); }
+  cf64& operator()(std::size_t i, std::size_t j) { return data_[j * rows_ + i]; }
+  const cf64& operator()(std::size_t i, std::size_t j) const { return data_[j * rows_ + i]; }
+  std::span<cf64> col(std::size_t j) { return {data_.data() + j * rows_, rows_}; }
+  std::span<const cf64> col(std::size_t j) const { return {data_.data() + j * rows_, rows_}; }
+  std::span<cf64> flat() { return data_; }
+  std::span<const cf64> flat() const { return data_; }
+  ComplexMatrix hermitian() const;
+  bool same_shape(const ComplexMatrix& o) const { return rows_ == o.rows_ && cols_ == o.cols_; }
+
+ private:
+  std::size_t rows_ = 0, cols_ = 0;
+  std::vector<cf64> data_;
+};
+
+enum class PrecisionFormat : std::uint8_t { fp64, fp32, fp16 };          // precision.hpp:26
+enum class PrecisionScope : std::uint8_t { messages_only, full_storage };  // precision.hpp:27
+
+struct PrecisionMode {
+  PrecisionFormat format = PrecisionFormat::fp64;
+  PrecisionScope scope = PrecisionScope::messages_only;
+  bool rounds() const { return format != PrecisionFormat::fp64; }
+  bool rounds_storage() const { return rounds() && scope == PrecisionScope::full_storage; }
+};
+
+enum class FusionMode : std::uint8_t { optimal, uniform };  // detect.hpp:24
+
+/// Declared for signature compatibility only (detect.hpp:28-36).
+class SweepObserver {
+ public:
+  virtual ~SweepObserver() = default;
+  virtual void after_update(unsigned sweep, std::size_t coord, std::span<const cf64> x,
+                            std::span<const cf64> residual) = 0;
+};
+
+struct DetectorConfig {  // detect.hpp:38-44
+  double n0 = 0.0;
+  double ex = 1.0;
+  unsigned t_max = 3;
+  FusionMode fusion = FusionMode::optimal;
+  PrecisionMode precision{};
+};
+
+struct ClusterData {  // detect.hpp:47-50
+  ComplexMatrix h;
+  ComplexVector y;
+};
+
+struct DetectionResult {  // detect.hpp:72-77
+  ComplexVector xhat;
+  std::vector<ComplexVector> local;
+  std::vector<double> sigma2;
+  std::vector<double> weights;
+};
+
+struct PrecoderConfig {  // precode.hpp:27-31
+  double rho = 1.0;
+  unsigned t_max = 3;
+  PrecisionMode precision{};
+};
+
+struct PrecodeResult {  // precode.hpp:33-37
+  ComplexVector x;
+  std::vector<ComplexVector> blocks;
+  double effective_gain = 0.0;
+};
+
+/// One CUDA device context (dcdg_ctx) plus a stream.  Reentrant per Engine;
+/// use one Engine per host thread for concurrent calls.
+class Engine {
+ public:
+  explicit Engine(int device = 0);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+  dcdg_ctx* ctx() const { return ctx_; }
+  void* stream() const { return stream_; }
+  int device() const { return device_; }
+  /// Throws the reference exception type for a non-OK dcdg status.
+  static void check(int status);
+  /// Waits for the stream and rethrows any recorded numerical error.
+  void sync();
+
+ private:
+  dcdg_ctx* ctx_ = nullptr;
+  void* stream_ = nullptr;
+  int device_ = 0;
+};
+
+/// Process-wide engine on device 0 used by the reference-signature functions.
+Engine& default_engine();
+
+// ---- reference-signature API (one subcarrier per call) --------------------
+ComplexVector cd_detect(const ComplexMatrix& h, const ComplexVector& y, double n0, double ex,
+                        unsigned t_max, const PrecisionMode& prec = {},
+                        SweepObserver* observer = nullptr);
+double post_eq_variance(const ComplexMatrix& hc, double n0, double ex);
+std::vector<double> fusion_weights(std::span<const double> sigma2);
+DetectionResult decentralized_cd_detect(std::span<const ClusterData> clusters,
+                                        const DetectorConfig& cfg, bool concurrent = false);
+ComplexVector cd_precode(const ComplexMatrix& h_dl, const ComplexVector& s, unsigned t_max,
+                         const PrecisionMode& prec = {}, SweepObserver* observer = nullptr);
+void power_scale(ComplexVector& x, double rho);
+PrecodeResult decentralized_cd_precode(std::span<const ComplexMatrix> h_dl_blocks,
+                                       const ComplexVector& s, const PrecoderConfig& cfg,
+                                       bool concurrent = false);
+
+// ---- batched device API (the hot path) --------------------------------------
+/// Device-resident batch of S subcarriers x C local clusters in the dcdg.h
+/// layout.  Owns its device buffers.
+class DeviceBatch {
+ public:
+  DeviceBatch(Engine& eng, int S, int C, int Bc, int U, int fmt);
+  ~DeviceBatch();
+  DeviceBatch(const DeviceBatch&) = delete;
+  DeviceBatch& operator=(const DeviceBatch&) = delete;
+
+  /// Host -> device upload of channel tiles [S][C][U][Bc] and receive samples
+  /// [S][C][Bc] (uplink) or symbols [S][U] (downlink), already in `fmt`.
+  void upload_h(const void* host, std::size_t bytes);
+  void upload_y(const void* host, std::size_t bytes);
+  void upload_s(const void* host, std::size_t bytes);
+
+  /// Uplink: fills x_local [S][C][U] (fmt) and xhat [S][U] (fp32 complex).
+  void detect(int C_total, int K, double n0, double ex, FusionMode fusion);
+  /// Downlink: fills x [S][C][Bc] (fmt) and gain [S] (fp32).
+  void precode(int C_total, int K, double rho, bool with_gain);
+
+  void download_xhat(void* host) const;
+  void download_x_local(void* host) const;
+  void download_x_dl(void* host) const;
+  void download_gain(float* host) const;
+  void download_sigma2(float* host) const;
+
+  int S, C, Bc, U, fmt;
+  void *H = nullptr, *y = nullptr, *s = nullptr, *x_local = nullptr, *x_dl = nullptr;
+  float *xhat = nullptr, *sigma2 = nullptr, *gain = nullptr, *gain_part = nullptr;
+
+ private:
+  Engine& eng_;
+};
+
+}  // namespace dcd::gpu

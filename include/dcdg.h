@@ -1,0 +1,170 @@
+/*
+ * dcdg.h — C ABI of the B200-native decentralized coordinate-descent (CD)
+ * baseband: per-cluster L-MMSE uplink detection (Alg. 1) with feed-forward
+ * fusion, and per-cluster ZF downlink precoding (Alg. 2) with the rho/sqrt(C)
+ * power split, batched over thousands of (subcarrier, cluster) problems.
+ *
+ * Plain pointers and sizes only — no torch, no C++ types.  This is the
+ * boundary a host binding (C++ wrapper include/dcd_gpu.hpp, ctypes, cgo, …)
+ * calls; INTEGRATION.md shows the bindings.  Reference interfaces replaced
+ * (paths relative to /root/reference/proj):
+ *
+ *   dcdg_ul_detect     <- dcd::decentralized_cd_detect  include/dcd/detect.hpp:84-86
+ *                         (per cluster dcd::cd_detect   include/dcd/detect.hpp:60-63,
+ *                          dcd::post_eq_variance        detect.hpp:67,
+ *                          dcd::fusion_weights          detect.hpp:70)
+ *   dcdg_dl_precode    <- dcd::decentralized_cd_precode include/dcd/precode.hpp:72-75
+ *                         (per cluster dcd::cd_precode  precode.hpp:58-60,
+ *                          dcd::power_scale             precode.hpp:63)
+ *   dcdg_fuse          <- the ascending-cluster fusion sum, src/detect.cpp:180-187
+ *   dcdg_post_eq_variance <- dcd::post_eq_variance      src/detect.cpp:112-130
+ *   dcdg_gain_reduce   <- assemble_blocks' effective_gain, src/precode.cpp:123-131
+ *
+ * The reference's kernels::Backend table (include/dcd/kernels.hpp:34-46) is a
+ * per-vector (n = B_c) plugin point far too fine-grained for a GPU; this ABI
+ * plugs in one level up, at the batched decentralized calls.
+ *
+ * DEVICE BATCH LAYOUT (all pointers are device pointers):
+ *   problem p = s*C + c  (subcarrier s, local cluster c; subcarrier-major)
+ *   H   [P][U][B_c]  complex; each tile is the cluster's B_c x U UPLINK block,
+ *                    column-major exactly like dcd::ComplexMatrix
+ *                    (numerics.hpp:35-40).  The downlink uses the same tiles:
+ *                    conj_rows(H_dl)[u] is uplink column u (precode.cpp:19-27).
+ *   y   [P][B_c]     uplink receive samples of each cluster
+ *   s   [S][U]       downlink symbols (one vector per subcarrier, broadcast)
+ *   x_local [P][U]   per-cluster uplink estimates (the wire payload)
+ *   xhat [S][U]      fused uplink estimate (always complex fp32)
+ *   x_dl [P][B_c]    per-cluster beamformers, already power-scaled
+ * "complex" is interleaved (re, im): float2 for DCDG_FP32, two IEEE binary16
+ * for DCDG_FP16 (the paper's half-precision path).  Buffers must be 16-byte
+ * aligned.
+ *
+ * Errors: every call returns a dcdg_status.  Argument errors are detected on
+ * the host before any launch and carry the reference's exception text
+ * (dcdg_last_error).  Numerical errors that the reference throws from inside
+ * a cluster worker (all-zero channel row, zero beamformer, singular Gram) are
+ * recorded on the device per batch; dcdg_sync_status() waits for the stream
+ * and returns them with the reference's text.  There is no CPU fallback: with
+ * no usable CUDA device every call returns DCDG_ECUDA.
+ */
+#ifndef DCDG_H
+#define DCDG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DCDG_ABI_VERSION 1
+
+typedef enum {
+  DCDG_OK = 0,
+  DCDG_EINVAL = 1,   /* std::invalid_argument in the reference */
+  DCDG_ENUMERIC = 2, /* std::runtime_error in the reference     */
+  DCDG_ECUDA = 3,
+  DCDG_ENCCL = 4
+} dcdg_status;
+
+typedef enum { DCDG_FP32 = 0, DCDG_FP16 = 1 } dcdg_format;
+typedef enum { DCDG_FUSION_OPTIMAL = 0, DCDG_FUSION_UNIFORM = 1 } dcdg_fusion; /* detect.hpp:24 */
+
+typedef struct dcdg_ctx dcdg_ctx;
+
+int dcdg_abi_version(void);
+/* Number of visible CUDA devices (0 when none). */
+int dcdg_device_count(void);
+/* Create a context bound to `device`; *out receives it. */
+int dcdg_init(int device, dcdg_ctx** out);
+int dcdg_destroy(dcdg_ctx* ctx);
+/* Text of the last error raised on this thread (reference wording). */
+const char* dcdg_last_error(void);
+/* Streams are passed as void* (cudaStream_t); NULL = legacy default stream. */
+
+/*
+ * Uplink: per-cluster CD L-MMSE (detect.cpp:67-110) over P = S*C problems,
+ * then fusion (detect.cpp:180-187).
+ *   C_total   clusters in the whole system (C_total >= C; C_total > C when the
+ *             other clusters live on other GPUs).  Uniform weights are
+ *             1/C_total.
+ *   x_local   optional [P][U] in `fmt` (NULL = not returned).
+ *   sigma2    optional [P] fp32: optimal-fusion variances (post_eq_variance);
+ *             required scratch when fusion == OPTIMAL (NULL = internal).
+ *   xhat      optional [S][U] fp32 complex.  With C == C_total it is the
+ *             reference's fused estimate (ascending-cluster order).  With
+ *             C < C_total it is this GPU's partial: uniform: sum_c x_c/C_total;
+ *             optimal: sum_c x_c/sigma2_c, with the matching partial weight
+ *             sums written to wsum [S] (fp32) for the cross-GPU reduction.
+ */
+int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, int C_total,
+                   int Bc, int U, int K, double n0, double ex, int fmt, int fusion,
+                   void* x_local, float* sigma2, float* xhat, float* wsum, void* stream);
+
+/*
+ * Downlink: per-cluster CD ZF precoding (precode.cpp:52-99) plus
+ * power_scale to rho/sqrt(C_total) (precode.cpp:101-111,155).
+ *   rho       total amplitude; rho == 0 returns the raw (unnormalised)
+ *             cd_precode beamformer, rho < 0 is an error.
+ *   s         [S][U] symbols in `fmt` (the broadcast payload).
+ *   x_dl      [P][B_c] beamformers in `fmt`.
+ *   gain_part optional [P] fp32: Re(s^H H_dl,c x_c) per cluster, the
+ *             cluster's share of assemble_blocks' effective_gain numerator.
+ *   gain      optional [S] fp32: effective_gain (requires C == C_total).
+ */
+int dcdg_dl_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, int C_total,
+                    int Bc, int U, int K, double rho, int fmt, void* x_dl, float* gain_part,
+                    float* gain, void* stream);
+
+/* sigma2[p] = (E_x/U) tr((I + (E_x/N0) H_p^H H_p)^-1)  (detect.cpp:112-130). */
+int dcdg_post_eq_variance(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, double n0,
+                          double ex, int fmt, float* sigma2, void* stream);
+
+/* xhat[s] = sum_c w_c x_local[s][c] in ascending c (detect.cpp:180-187);
+ * w from sigma2 (optimal, fusion_weights detect.cpp:132-145) or 1/C_total. */
+int dcdg_fuse(dcdg_ctx* ctx, const void* x_local, const float* sigma2, int S, int C,
+              int C_total, int U, int fmt, int fusion, float* xhat, float* wsum, void* stream);
+
+/* gain[s] = (sum_c gain_part[s][c]) / ||s_s||^2  (precode.cpp:123-131). */
+int dcdg_gain_reduce(dcdg_ctx* ctx, const float* gain_part, const void* s, int S, int C, int U,
+                     int fmt, float* gain, void* stream);
+
+/* Finalize a cross-GPU optimal-fusion reduction: xhat[s] /= wsum[s]. */
+int dcdg_fuse_finalize(dcdg_ctx* ctx, float* xhat, const float* wsum, int S, int U, void* stream);
+
+/* x[p] <- rho * x[p] / ||x[p]|| for P vectors of n complex in `fmt`
+ * (power_scale, precode.cpp:101-111; zero vectors are recorded as numerical
+ * errors, "power_scale: zero beamformer cannot be scaled"). */
+int dcdg_power_scale(dcdg_ctx* ctx, void* x, int P, int n, double rho, int fmt, void* stream);
+
+/* w[s][c] = (1/sigma2[s][c]) / sum_c' (1/sigma2[s][c'])  (fusion_weights,
+ * detect.cpp:132-145), for S independent sets of C variances. */
+int dcdg_fusion_weights(dcdg_ctx* ctx, const float* sigma2, int S, int C, float* w, void* stream);
+
+/* Waits for `stream`, then returns and clears the first numerical error the
+ * kernels recorded since the last call (DCDG_OK if none).  The message
+ * (dcdg_last_error) is the reference's exception text; the failing problem
+ * index is available from dcdg_last_error_problem(). */
+int dcdg_sync_status(dcdg_ctx* ctx, void* stream);
+long long dcdg_last_error_problem(void);
+
+/* Number of kernel launches issued through this context (for bench.py). */
+uint64_t dcdg_launch_count(dcdg_ctx* ctx);
+
+/* In-place round of n fp32 values to the nearest binary16 (RNE), widened
+ * back: the wire-format rounding of PrecisionScope::messages_only
+ * (precision.cpp:43-72, detect.cpp:170-173, precode.cpp:159-160). */
+int dcdg_round_fp16(dcdg_ctx* ctx, float* x, int64_t n, void* stream);
+
+/* Format conversion on the device: fp32 complex <-> fp16 complex (RNE). */
+int dcdg_convert(dcdg_ctx* ctx, const void* src, int src_fmt, void* dst, int dst_fmt,
+                 int64_t n_complex, void* stream);
+
+/* Which kernel variant a (direction, Bc, U, fmt) problem shape dispatches to:
+ * writes a short name ("ul_f32_reg<32,16,8>", "ul_generic_f32", …). */
+int dcdg_kernel_name(int direction /*0 UL, 1 DL*/, int Bc, int U, int fmt, char* buf, int len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DCDG_H */

@@ -1,0 +1,81 @@
+"""Build recipe for the in-tree native libraries (no JIT cache: the .so files
+travel with the repo snapshot to the GPU box).
+
+  libdcdg.so   CUDA kernels + C ABI (include/dcdg.h) + C++ host API
+               (include/dcd_gpu.hpp), sm_100a only.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIB = os.path.join(PKG, "libdcdg.so")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++20",
+    "-Xcompiler", "-fPIC,-O3",
+    "--expt-relaxed-constexpr",
+]
+
+
+def nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: the CUDA toolkit is required to build libdcdg.so")
+
+
+def sources():
+    return [os.path.join(CSRC, f) for f in ("dcdg.cu", "dcd_gpu.cpp")]
+
+
+def _stale(target, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_lib(force: bool = False, verbose: bool = False) -> str:
+    deps = sources() + [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
+        os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE)]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    objs = []
+    build_dir = os.path.join(PKG, "_build")
+    os.makedirs(build_dir, exist_ok=True)
+    for src in sources():
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
+        if src.endswith(".cpp"):
+            cmd = [nvcc(), "-x", "cu", *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        objs.append(obj)
+    cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs, "-lcudart"]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    return LIB
+
+
+def build_oracle(verbose: bool = False):
+    """The CPU checker (test infrastructure): oracle/libdcdoracle.so always,
+    oracle/_ref/libdcdref.so (the reference compiled from its sources) when
+    /root/reference is present."""
+    odir = os.path.join(ROOT, "oracle")
+    subprocess.run(["make", "-s", "-C", odir], check=True, capture_output=not verbose)
+    if os.path.isdir("/root/reference/proj/src"):
+        subprocess.run(["make", "-s", "-j8", "-C", odir, "ref"], check=True, capture_output=not verbose)
+
+
+if __name__ == "__main__":
+    build_lib(force=True, verbose=True)
+    build_oracle(verbose=True)

@@ -1,0 +1,557 @@
+// C-ABI implementation (include/dcdg.h): argument validation with the
+// reference's exception texts, kernel dispatch by problem shape, launch
+// geometry (persistent grids sized to SM count x occupancy), and the
+// numerical-status word.  No CPU fallback exists: without a CUDA device every
+// entry point fails with DCDG_ECUDA.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "dcdg.h"
+#include "dcdg_kernels.cuh"
+
+struct dcdg_ctx {
+  int device = 0;
+  int sms = 0;
+  unsigned long long* d_status = nullptr;
+  uint64_t launches = 0;
+  void* scratch = nullptr;  // x_local / sigma2 / gain_part scratch
+  size_t scratch_bytes = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local long long g_err_problem = -1;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  g_err_problem = -1;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(DCDG_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr, where)                 \
+  do {                                        \
+    cudaError_t e_ = (expr);                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int ensure_scratch(dcdg_ctx* ctx, size_t bytes) {
+  if (ctx->scratch_bytes >= bytes) return DCDG_OK;
+  if (ctx->scratch) cudaFree(ctx->scratch);
+  ctx->scratch = nullptr;
+  ctx->scratch_bytes = 0;
+  CUDA_TRY(cudaMalloc(&ctx->scratch, bytes), "scratch allocation");
+  ctx->scratch_bytes = bytes;
+  return DCDG_OK;
+}
+
+inline size_t esize(int fmt) { return fmt == DCDG_FP16 ? 4 : 8; }
+
+// ---------------------------------------------------------------------------
+// launchers for the register-resident kernels
+// ---------------------------------------------------------------------------
+constexpr int kWarps = 4;
+
+template <typename Kern>
+int occupancy_of(Kern kern, size_t smem) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kWarps, smem) != cudaSuccess || occ < 1) occ = 1;
+  return occ;
+}
+
+using UlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, float, void*, cudaStream_t);
+using DlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, int, float, void*, float*,
+                                 cudaStream_t);
+
+template <int BC, int U, int G>
+cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                          cudaStream_t st) {
+  constexpr int NPW = 32 / G;
+  constexpr size_t smem = kWarps * NPW * (BC * U * 8 + BC * 8) + kWarps * 8;
+  auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps>;
+  static const int occ = occupancy_of(kern, smem);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
+  kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K, kappa,
+                                          static_cast<float2*>(X));
+  return cudaGetLastError();
+}
+
+template <int BC, int U, int G>
+cudaError_t launch_ul_f16(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                          cudaStream_t st) {
+  constexpr int NPW = 32 / G;
+  constexpr size_t smem = kWarps * NPW * (BC * U * 4 + BC * 4) + kWarps * 8;
+  auto kern = dcdg::ul_reg_f16<BC, U, G, kWarps>;
+  static const int occ = occupancy_of(kern, smem);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
+  kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(Y), P, K, kappa,
+                                          static_cast<__half2*>(X));
+  return cudaGetLastError();
+}
+
+template <int BC, int U, int G>
+cudaError_t launch_dl_f32(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
+                          float* gp, cudaStream_t st) {
+  constexpr int NPW = 32 / G;
+  constexpr size_t smem = kWarps * NPW * (BC * U * 8 + U * 8) + kWarps * 8;
+  const int nsets = (P + NPW - 1) / NPW;
+  if (gp) {
+    auto kern = dcdg::dl_reg_f32<BC, U, G, kWarps, true>;
+    static const int occ = occupancy_of(kern, smem);
+    const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
+    kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(S), P, C, K,
+                                            rho_c, static_cast<float2*>(X), gp, ctx->d_status);
+  } else {
+    auto kern = dcdg::dl_reg_f32<BC, U, G, kWarps, false>;
+    static const int occ = occupancy_of(kern, smem);
+    const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
+    kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(S), P, C, K,
+                                            rho_c, static_cast<float2*>(X), gp, ctx->d_status);
+  }
+  return cudaGetLastError();
+}
+
+template <int BC, int U, int G>
+cudaError_t launch_dl_f16(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
+                          float* gp, cudaStream_t st) {
+  constexpr int NPW = 32 / G;
+  constexpr size_t smem = kWarps * NPW * (BC * U * 4 + U * 4) + kWarps * 8;
+  const int nsets = (P + NPW - 1) / NPW;
+  if (gp) {
+    auto kern = dcdg::dl_reg_f16<BC, U, G, kWarps, true>;
+    static const int occ = occupancy_of(kern, smem);
+    const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
+    kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(S), P, C, K,
+                                            rho_c, static_cast<__half2*>(X), gp, ctx->d_status);
+  } else {
+    auto kern = dcdg::dl_reg_f16<BC, U, G, kWarps, false>;
+    static const int occ = occupancy_of(kern, smem);
+    const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
+    kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(S), P, C, K,
+                                            rho_c, static_cast<__half2*>(X), gp, ctx->d_status);
+  }
+  return cudaGetLastError();
+}
+
+struct Spec {
+  int bc, u, fmt, g;
+  UlLaunch ul;
+  DlLaunch dl;
+};
+
+#define SPEC_F32(BC, U, G) {BC, U, DCDG_FP32, G, launch_ul_f32<BC, U, G>, launch_dl_f32<BC, U, G>}
+#define SPEC_F16(BC, U, G) {BC, U, DCDG_FP16, G, launch_ul_f16<BC, U, G>, launch_dl_f16<BC, U, G>}
+
+// Register-resident specialisations: B_c*U/G complex per lane = 128 regs of
+// channel for fp32 (64-128 for fp16).  Everything else runs the generic path.
+const Spec kSpecs[] = {
+    SPEC_F32(32, 16, 8),  // north-star target: B=256, C=8, U=16
+    SPEC_F32(32, 8, 4),   // paper / config 1: B_c=32, U=8
+    SPEC_F32(16, 16, 4),  // B=128, C=8
+    SPEC_F32(64, 16, 16), // B=256, C=4 / B=512, C=8
+    SPEC_F32(64, 8, 8),
+    SPEC_F16(32, 16, 4),
+    SPEC_F16(32, 8, 4),
+    SPEC_F16(16, 16, 4),
+    SPEC_F16(64, 16, 8),
+};
+
+const Spec* find_spec(int bc, int u, int fmt) {
+  for (const auto& s : kSpecs)
+    if (s.bc == bc && s.u == u && s.fmt == fmt) return &s;
+  return nullptr;
+}
+
+int check_ctx(dcdg_ctx* ctx) {
+  if (!ctx) return fail(DCDG_EINVAL, "dcdg: null context");
+  return DCDG_OK;
+}
+
+int check_fmt(int fmt) {
+  if (fmt != DCDG_FP32 && fmt != DCDG_FP16) return fail(DCDG_EINVAL, "dcdg: unknown storage format");
+  return DCDG_OK;
+}
+
+int launch_fuse(dcdg_ctx* ctx, const void* xl, const float* s2, int S, int C, int C_total, int U, int fmt,
+                bool optimal, float* xhat, float* wsum, cudaStream_t st) {
+  const long long n = static_cast<long long>(S) * U;
+  const int threads = 256;
+  const long long blocks = (n + threads - 1) / threads;
+  if (fmt == DCDG_FP16)
+    dcdg::fuse_kernel<__half2><<<blocks, threads, 0, st>>>(static_cast<const __half2*>(xl), s2, S, C, C_total, U,
+                                                            optimal, reinterpret_cast<float2*>(xhat), wsum,
+                                                            ctx->d_status);
+  else
+    dcdg::fuse_kernel<float2><<<blocks, threads, 0, st>>>(static_cast<const float2*>(xl), s2, S, C, C_total, U, optimal,
+                                                           reinterpret_cast<float2*>(xhat), wsum, ctx->d_status);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "fuse launch");
+  return DCDG_OK;
+}
+
+int launch_post_eq(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, double n0, double ex, int fmt, float* s2,
+                   cudaStream_t st) {
+  const size_t smem = 4 * 2 * static_cast<size_t>(U) * U * sizeof(float2);
+  const int blocks = (P + 3) / 4;
+  const float gam = static_cast<float>(ex / n0);
+  const float exu = static_cast<float>(ex / U);
+  if (fmt == DCDG_FP16) {
+    auto k = dcdg::post_eq_var<__half2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<blocks, 128, smem, st>>>(static_cast<const __half2*>(H), P, Bc, U, gam, exu, true, s2, ctx->d_status);
+  } else {
+    auto k = dcdg::post_eq_var<float2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<blocks, 128, smem, st>>>(static_cast<const float2*>(H), P, Bc, U, gam, exu, false, s2, ctx->d_status);
+  }
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "post_eq_variance launch");
+  return DCDG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dcdg_abi_version(void) { return DCDG_ABI_VERSION; }
+
+int dcdg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+const char* dcdg_last_error(void) { return g_err.c_str(); }
+
+int dcdg_init(int device, dcdg_ctx** out) {
+  if (!out) return fail(DCDG_EINVAL, "dcdg_init: null output pointer");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(DCDG_ECUDA, "dcdg_init: no CUDA device available (there is no CPU fallback)");
+  if (device < 0 || device >= n) return fail(DCDG_EINVAL, "dcdg_init: device index out of range");
+  CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+  auto* ctx = new dcdg_ctx;
+  ctx->device = device;
+  cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+  e = cudaMalloc(&ctx->d_status, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    delete ctx;
+    return cuda_fail(e, "dcdg_init status buffer");
+  }
+  cudaMemset(ctx->d_status, 0xff, sizeof(unsigned long long));
+  cudaDeviceSynchronize();
+  *out = ctx;
+  return DCDG_OK;
+}
+
+int dcdg_destroy(dcdg_ctx* ctx) {
+  if (!ctx) return DCDG_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->d_status) cudaFree(ctx->d_status);
+  if (ctx->scratch) cudaFree(ctx->scratch);
+  delete ctx;
+  return DCDG_OK;
+}
+
+uint64_t dcdg_launch_count(dcdg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int dcdg_kernel_name(int direction, int Bc, int U, int fmt, char* buf, int len) {
+  const Spec* s = find_spec(Bc, U, fmt);
+  char tmp[96];
+  const char* dir = direction ? "dl" : "ul";
+  const char* f = fmt == DCDG_FP16 ? "f16" : "f32";
+  if (s)
+    std::snprintf(tmp, sizeof tmp, "%s_reg_%s<%d,%d,%d>", dir, f, Bc, U, s->g);
+  else
+    std::snprintf(tmp, sizeof tmp, "%s_generic_%s", dir, f);
+  if (buf && len > 0) {
+    std::strncpy(buf, tmp, static_cast<size_t>(len - 1));
+    buf[len - 1] = 0;
+  }
+  return DCDG_OK;
+}
+
+int dcdg_sync_status(dcdg_ctx* ctx, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  CUDA_TRY(cudaStreamSynchronize(as_stream(stream)), "stream synchronize");
+  unsigned long long key = ~0ULL;
+  CUDA_TRY(cudaMemcpy(&key, ctx->d_status, sizeof key, cudaMemcpyDeviceToHost), "status read");
+  if (key == ~0ULL) return DCDG_OK;
+  CUDA_TRY(cudaMemset(ctx->d_status, 0xff, sizeof(unsigned long long)), "status reset");
+  const unsigned code = static_cast<unsigned>((key >> 16) & 0xff);
+  const unsigned detail = static_cast<unsigned>(key & 0xffff);
+  g_err_problem = static_cast<long long>(key >> 24);
+  switch (code) {
+    case dcdg::ST_ZERO_ROW:
+      g_err = "cd_precode: user " + std::to_string(detail) + " has an all-zero channel row";
+      return DCDG_ENUMERIC;
+    case dcdg::ST_ZERO_BEAMFORMER:
+      g_err = "power_scale: zero beamformer cannot be scaled";
+      return DCDG_ENUMERIC;
+    case dcdg::ST_SINGULAR:
+      g_err = "hermitian_solve: matrix is numerically singular";
+      return DCDG_ENUMERIC;
+    case dcdg::ST_BAD_VARIANCE:
+      g_err = "fusion_weights: variances must be positive and finite";
+      return DCDG_EINVAL;
+    default:
+      g_err = "dcdg: unknown device status";
+      return DCDG_ENUMERIC;
+  }
+}
+
+long long dcdg_last_error_problem(void) { return g_err_problem; }
+
+int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, int C_total, int Bc, int U, int K,
+                   double n0, double ex, int fmt, int fusion, void* x_local, float* sigma2, float* xhat, float* wsum,
+                   void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_fmt(fmt)) return rc;
+  // argument checks in the reference's order and words (detect.cpp:12-19,71-72,150-155)
+  if (C <= 0 || S < 0) return fail(DCDG_EINVAL, "decentralized_cd_detect: no clusters");
+  if (C_total < C) return fail(DCDG_EINVAL, "dcdg_ul_detect: C_total must be >= C");
+  if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "detector: empty channel matrix");
+  if (n0 < 0.0 || !(ex > 0.0)) return fail(DCDG_EINVAL, "detector: need N0 >= 0 and E_x > 0");
+  if (K <= 0) return fail(DCDG_EINVAL, "cd_detect: need at least one sweep");
+  const bool optimal = fusion == DCDG_FUSION_OPTIMAL;
+  if (fusion != DCDG_FUSION_OPTIMAL && fusion != DCDG_FUSION_UNIFORM)
+    return fail(DCDG_EINVAL, "dcdg_ul_detect: unknown fusion mode");
+  if (optimal && !(n0 > 0.0)) return fail(DCDG_EINVAL, "post_eq_variance: need N0 > 0 and E_x > 0");
+  if (!H || !y) return fail(DCDG_EINVAL, "dcdg_ul_detect: null input buffer");
+  const long long P = static_cast<long long>(S) * C;
+  if (P > 0x7fffffffLL) return fail(DCDG_EINVAL, "dcdg_ul_detect: batch too large (S*C must fit in int32)");
+  if (P == 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = as_stream(stream);
+  const size_t xl_bytes = static_cast<size_t>(P) * U * esize(fmt);
+  const size_t s2_bytes = optimal ? static_cast<size_t>(P) * sizeof(float) : 0;
+  size_t need = 0;
+  if (!x_local) need += (xl_bytes + 255) & ~size_t(255);
+  if (optimal && !sigma2) need += (s2_bytes + 255) & ~size_t(255);
+  if (need)
+    if (int rc = ensure_scratch(ctx, need)) return rc;
+  unsigned char* sp = static_cast<unsigned char*>(ctx->scratch);
+  if (!x_local) {
+    x_local = sp;
+    sp += (xl_bytes + 255) & ~size_t(255);
+  }
+  if (optimal && !sigma2) sigma2 = reinterpret_cast<float*>(sp);
+
+  const float kappa = static_cast<float>(n0 / ex);
+  const Spec* spec = find_spec(Bc, U, fmt);
+  if (spec) {
+    CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, x_local, st), "ul_detect launch");
+  } else {
+    const size_t smem = 4 * (static_cast<size_t>(Bc) + 2 * U) * sizeof(float2);
+    const long long blocks = (P + 3) / 4;
+    if (fmt == DCDG_FP16) {
+      auto k = dcdg::ul_generic<__half2>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k<<<blocks, 128, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(y), static_cast<int>(P),
+                                   Bc, U, K, kappa, static_cast<__half2*>(x_local));
+    } else {
+      auto k = dcdg::ul_generic<float2>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k<<<blocks, 128, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(y), static_cast<int>(P),
+                                   Bc, U, K, kappa, static_cast<float2*>(x_local));
+    }
+    CUDA_TRY(cudaGetLastError(), "ul_generic launch");
+  }
+  ++ctx->launches;
+  if (optimal)
+    if (int rc = launch_post_eq(ctx, H, static_cast<int>(P), Bc, U, n0, ex, fmt, sigma2, st)) return rc;
+  if (xhat)
+    if (int rc = launch_fuse(ctx, x_local, sigma2, S, C, C_total, U, fmt, optimal, xhat, wsum, st)) return rc;
+  return DCDG_OK;
+}
+
+int dcdg_dl_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, int C_total, int Bc, int U, int K,
+                    double rho, int fmt, void* x_dl, float* gain_part, float* gain, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_fmt(fmt)) return rc;
+  // precode.cpp:11-16,57-58,138-152,101-104
+  if (C <= 0 || S < 0) return fail(DCDG_EINVAL, "decentralized_cd_precode: no clusters");
+  if (C_total < C) return fail(DCDG_EINVAL, "dcdg_dl_precode: C_total must be >= C");
+  if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "precoder: empty channel matrix");
+  if (Bc < U)
+    return fail(DCDG_EINVAL, "decentralized_cd_precode: cluster 0 has " + std::to_string(Bc) + " antennas for " +
+                                 std::to_string(U) + " users; local zero-forcing needs B_c >= U");
+  if (K <= 0) return fail(DCDG_EINVAL, "cd_precode: need at least one sweep");
+  if (rho < 0.0 || std::isnan(rho)) return fail(DCDG_EINVAL, "power_scale: amplitude must be positive");
+  if (gain && C != C_total) return fail(DCDG_EINVAL, "dcdg_dl_precode: effective gain needs every cluster (C == C_total)");
+  if (!H || !s || !x_dl) return fail(DCDG_EINVAL, "dcdg_dl_precode: null buffer");
+  const long long P = static_cast<long long>(S) * C;
+  if (P > 0x7fffffffLL) return fail(DCDG_EINVAL, "dcdg_dl_precode: batch too large (S*C must fit in int32)");
+  if (P == 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = as_stream(stream);
+  if (gain && !gain_part) {
+    if (int rc = ensure_scratch(ctx, static_cast<size_t>(P) * sizeof(float))) return rc;
+    gain_part = static_cast<float*>(ctx->scratch);
+  }
+  // rho == 0: return the raw cd_precode beamformer (no power_scale)
+  const float rho_c = static_cast<float>(rho / std::sqrt(static_cast<double>(C_total)));
+  const Spec* spec = find_spec(Bc, U, fmt);
+  if (spec) {
+    CUDA_TRY(spec->dl(ctx, H, s, static_cast<int>(P), C, K, rho_c, x_dl, gain_part, st), "dl_precode launch");
+  } else {
+    const size_t smem = 4 * (static_cast<size_t>(Bc) + 2 * U) * sizeof(float2);
+    const long long blocks = (P + 3) / 4;
+#define DL_GENERIC(T, GAIN)                                                                                     \
+  {                                                                                                             \
+    auto k = dcdg::dl_generic<T, GAIN>;                                                                         \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));               \
+    k<<<blocks, 128, smem, st>>>(static_cast<const T*>(H), static_cast<const T*>(s), static_cast<int>(P), C, Bc, \
+                                 U, K, rho_c, static_cast<T*>(x_dl), gain_part, ctx->d_status);                \
+  }
+    if (fmt == DCDG_FP16) {
+      if (gain_part) DL_GENERIC(__half2, true) else DL_GENERIC(__half2, false)
+    } else {
+      if (gain_part) DL_GENERIC(float2, true) else DL_GENERIC(float2, false)
+    }
+#undef DL_GENERIC
+    CUDA_TRY(cudaGetLastError(), "dl_generic launch");
+  }
+  ++ctx->launches;
+  if (gain) return dcdg_gain_reduce(ctx, gain_part, s, S, C, U, fmt, gain, stream);
+  return DCDG_OK;
+}
+
+int dcdg_post_eq_variance(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, double n0, double ex, int fmt,
+                          float* sigma2, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_fmt(fmt)) return rc;
+  if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "post_eq_variance: empty channel block");
+  if (!(n0 > 0.0) || !(ex > 0.0)) return fail(DCDG_EINVAL, "post_eq_variance: need N0 > 0 and E_x > 0");
+  if (U > 32) return fail(DCDG_EINVAL, "dcdg_post_eq_variance: U > 32 not supported");
+  if (P <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  return launch_post_eq(ctx, H, P, Bc, U, n0, ex, fmt, sigma2, as_stream(stream));
+}
+
+int dcdg_fuse(dcdg_ctx* ctx, const void* x_local, const float* sigma2, int S, int C, int C_total, int U, int fmt,
+              int fusion, float* xhat, float* wsum, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_fmt(fmt)) return rc;
+  if (C <= 0) return fail(DCDG_EINVAL, "fusion_weights: no clusters");
+  if (C_total < C) return fail(DCDG_EINVAL, "dcdg_fuse: C_total must be >= C");
+  const bool optimal = fusion == DCDG_FUSION_OPTIMAL;
+  if (optimal && !sigma2) return fail(DCDG_EINVAL, "dcdg_fuse: optimal fusion needs sigma2");
+  if (S <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  return launch_fuse(ctx, x_local, sigma2, S, C, C_total, U, fmt, optimal, xhat, wsum, as_stream(stream));
+}
+
+int dcdg_fuse_finalize(dcdg_ctx* ctx, float* xhat, const float* wsum, int S, int U, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (S <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const long long n = static_cast<long long>(S) * U;
+  dcdg::fuse_finalize_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(reinterpret_cast<float2*>(xhat), wsum, S,
+                                                                              U);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "fuse_finalize launch");
+  return DCDG_OK;
+}
+
+int dcdg_gain_reduce(dcdg_ctx* ctx, const float* gain_part, const void* s, int S, int C, int U, int fmt, float* gain,
+                     void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_fmt(fmt)) return rc;
+  if (S <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int threads = 256;
+  const int blocks = (S + threads - 1) / threads;
+  if (fmt == DCDG_FP16)
+    dcdg::gain_reduce_kernel<__half2><<<blocks, threads, 0, as_stream(stream)>>>(
+        gain_part, static_cast<const __half2*>(s), S, C, U, gain);
+  else
+    dcdg::gain_reduce_kernel<float2><<<blocks, threads, 0, as_stream(stream)>>>(
+        gain_part, static_cast<const float2*>(s), S, C, U, gain);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "gain_reduce launch");
+  return DCDG_OK;
+}
+
+int dcdg_power_scale(dcdg_ctx* ctx, void* x, int P, int n, double rho, int fmt, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_fmt(fmt)) return rc;
+  if (!(rho > 0.0)) return fail(DCDG_EINVAL, "power_scale: amplitude must be positive");
+  if (n <= 0) return fail(DCDG_EINVAL, "power_scale: empty beamformer");
+  if (P <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int blocks = (P + 3) / 4;
+  if (fmt == DCDG_FP16)
+    dcdg::power_scale_kernel<__half2><<<blocks, 128, 0, as_stream(stream)>>>(static_cast<__half2*>(x), P, n,
+                                                                             static_cast<float>(rho), ctx->d_status);
+  else
+    dcdg::power_scale_kernel<float2><<<blocks, 128, 0, as_stream(stream)>>>(static_cast<float2*>(x), P, n,
+                                                                            static_cast<float>(rho), ctx->d_status);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "power_scale launch");
+  return DCDG_OK;
+}
+
+int dcdg_fusion_weights(dcdg_ctx* ctx, const float* sigma2, int S, int C, float* w, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (C <= 0) return fail(DCDG_EINVAL, "fusion_weights: no clusters");
+  if (S <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  dcdg::fusion_weights_kernel<<<(S + 127) / 128, 128, 0, as_stream(stream)>>>(sigma2, S, C, w, ctx->d_status);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "fusion_weights launch");
+  return DCDG_OK;
+}
+
+int dcdg_round_fp16(dcdg_ctx* ctx, float* x, int64_t n, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (n <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
+  dcdg::round_fp16_kernel<<<blocks, 256, 0, as_stream(stream)>>>(x, n);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "round_fp16 launch");
+  return DCDG_OK;
+}
+
+int dcdg_convert(dcdg_ctx* ctx, const void* src, int src_fmt, void* dst, int dst_fmt, int64_t n_complex,
+                 void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = check_fmt(src_fmt)) return rc;
+  if (int rc = check_fmt(dst_fmt)) return rc;
+  if (n_complex <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = as_stream(stream);
+  const long long n = 2 * n_complex;
+  const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
+  if (src_fmt == dst_fmt) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, static_cast<size_t>(n_complex) * esize(src_fmt), cudaMemcpyDeviceToDevice, st),
+             "convert copy");
+    return DCDG_OK;
+  }
+  if (src_fmt == DCDG_FP32)
+    dcdg::f32_to_f16_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(src), static_cast<__half*>(dst), n);
+  else
+    dcdg::f16_to_f32_kernel<<<blocks, 256, 0, st>>>(static_cast<const __half*>(src), static_cast<float*>(dst), n);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "convert launch");
+  return DCDG_OK;
+}
+
+}  // extern "C"

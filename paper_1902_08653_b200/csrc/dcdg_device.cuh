@@ -1,0 +1,126 @@
+// Device-side building blocks shared by the CD kernels: sm_100a PTX wrappers
+// for the bulk-copy (TMA 1-D) staging pipeline, sub-warp reductions, complex
+// load/convert helpers and the numerical-status word.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dcdg {
+
+// ---------------------------------------------------------------------------
+// shared-memory async bulk copy (cp.async.bulk, SASS UBLKCP) + mbarrier
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Orders this thread's prior generic-proxy shared-memory accesses before
+// subsequent async-proxy (bulk copy) writes to the same buffer.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Global -> shared bulk copy completing on `bar` (bytes % 16 == 0, 16-B aligned).
+// The data is streamed exactly once, so it is marked evict-first in L2.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// ---------------------------------------------------------------------------
+// reductions over a group of G consecutive lanes (xor butterfly: every lane of
+// the group ends with the bitwise-identical sum, so redundant per-lane scalar
+// updates stay consistent)
+// ---------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ float gsum(float v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int G>
+__device__ __forceinline__ __half2 gsum_h2(__half2 v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v = __hadd2(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ float warp_sum(float v) { return gsum<32>(v); }
+
+// ---------------------------------------------------------------------------
+// complex element access for the two storage formats
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 ldc(const float2* p, size_t i) { return __ldg(p + i); }
+__device__ __forceinline__ float2 ldc(const __half2* p, size_t i) { return __half22float2(__ldg(p + i)); }
+__device__ __forceinline__ void stc(float2* p, size_t i, float2 v) { p[i] = v; }
+__device__ __forceinline__ void stc(__half2* p, size_t i, float2 v) { p[i] = __floats2half2_rn(v.x, v.y); }
+
+__device__ __forceinline__ __half2 u32_as_h2(uint32_t u) {
+  __half2 h;
+  memcpy(&h, &u, 4);
+  return h;
+}
+__device__ __forceinline__ uint32_t h2_as_u32(__half2 h) {
+  uint32_t u;
+  memcpy(&u, &h, 4);
+  return u;
+}
+
+// ---------------------------------------------------------------------------
+// numerical status: the first (lowest problem index) error of a batch wins,
+// mirroring the reference's in-order cluster loop that throws at the first
+// failing cluster (src/detect.cpp:32-52, src/precode.cpp:62-78,101-111).
+// key = problem << 24 | code << 16 | detail
+// ---------------------------------------------------------------------------
+enum StatusCode : uint32_t {
+  ST_ZERO_ROW = 1,        // precode.cpp:74-76   runtime_error
+  ST_ZERO_BEAMFORMER = 2, // precode.cpp:107-108 runtime_error
+  ST_SINGULAR = 3,        // numerics.cpp:55-56  runtime_error
+  ST_BAD_VARIANCE = 4,    // detect.cpp:138-139  invalid_argument
+};
+
+__device__ __forceinline__ void record_status(unsigned long long* st, long long p, uint32_t code, uint32_t detail) {
+  if (st) atomicMin(st, (static_cast<unsigned long long>(p) << 24) | (code << 16) | (detail & 0xffffu));
+}
+
+}  // namespace dcdg

@@ -1,0 +1,230 @@
+"""Batched device API over the dcdg C ABI (torch tensors are only device
+memory and streams here).
+
+Tensor conventions (device batch layout of include/dcdg.h):
+
+  fp32:  torch.complex64   H [S, C, U, Bc], y [S, C, Bc], s [S, U]
+  fp16:  torch.float16     H [S, C, U, Bc, 2], y [S, C, Bc, 2], s [S, U, 2]
+         (interleaved (re, im) binary16 — the paper's half-precision path)
+
+Each tile H[s, c] is the cluster's B_c x U uplink block stored column by
+column (one user column of B_c antennas after the other), i.e. the memory
+order of dcd::ComplexMatrix (include/dcd/numerics.hpp:35-40).  The downlink
+uses the same tiles (reciprocity, src/precode.cpp:19-27).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import FP16, FP32, FUSION_OPTIMAL, FUSION_UNIFORM, check, lib
+
+
+def _fmt_of(t: torch.Tensor) -> int:
+    if t.dtype == torch.complex64:
+        return FP32
+    if t.dtype == torch.float16 and t.shape[-1] == 2:
+        return FP16
+    if t.dtype == torch.complex32:
+        return FP16
+    raise TypeError(f"unsupported dtype {t.dtype} (need complex64, or float16 [...,2] for fp16)")
+
+
+def _shape(t: torch.Tensor, fmt: int):
+    return tuple(t.shape[:-1]) if (fmt == FP16 and t.dtype == torch.float16) else tuple(t.shape)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _need(t: torch.Tensor, what: str):
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor (the CD path has no CPU implementation)")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    if t.data_ptr() % 16:
+        raise ValueError(f"{what} must be 16-byte aligned")
+
+
+def _fusion(f) -> int:
+    if isinstance(f, int):
+        return f
+    return {"optimal": FUSION_OPTIMAL, "uniform": FUSION_UNIFORM}[f]
+
+
+def complex_empty(shape, fmt: int, device) -> torch.Tensor:
+    if fmt == FP32:
+        return torch.empty(shape, dtype=torch.complex64, device=device)
+    return torch.empty((*shape, 2), dtype=torch.float16, device=device)
+
+
+def to_fp16(t: torch.Tensor) -> torch.Tensor:
+    """complex64 -> float16 [..., 2] (RNE), on the tensor's device."""
+    return torch.view_as_real(t).to(torch.float16).contiguous()
+
+
+def to_complex64(t: torch.Tensor) -> torch.Tensor:
+    if t.dtype == torch.complex64:
+        return t
+    if t.dtype == torch.float16:
+        return torch.view_as_complex(t.float().contiguous())
+    return t.to(torch.complex64)
+
+
+@dataclass
+class UplinkResult:
+    x_local: torch.Tensor | None
+    xhat: torch.Tensor | None
+    sigma2: torch.Tensor | None
+    wsum: torch.Tensor | None
+
+
+@dataclass
+class DownlinkResult:
+    x: torch.Tensor
+    gain_part: torch.Tensor | None
+    gain: torch.Tensor | None
+
+
+class Engine:
+    """One dcdg context bound to a CUDA device."""
+
+    def __init__(self, device: int | None = None):
+        if device is None:
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        self.device = device
+        self._ctx = C.c_void_p()
+        check(lib().dcdg_init(device, C.byref(self._ctx)))
+
+    def close(self):
+        if self._ctx:
+            lib().dcdg_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(lib().dcdg_launch_count(self._ctx))
+
+    def _stream(self, stream):
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        return C.c_void_p(stream.cuda_stream)
+
+    def sync(self, stream=None):
+        """Wait for the stream; raise the first recorded numerical error."""
+        check(lib().dcdg_sync_status(self._ctx, self._stream(stream)))
+
+    # ------------------------------------------------------------------ uplink
+    def ul_detect(self, H, y, *, n0: float, ex: float = 1.0, K: int = 3, fusion="uniform", C_total=None,
+                  want_local: bool = True, want_xhat: bool = True, x_local=None, sigma2=None, xhat=None,
+                  stream=None) -> UplinkResult:
+        fmt = _fmt_of(H)
+        S, Cn, U, Bc = _shape(H, fmt)
+        if _shape(y, fmt) != (S, Cn, Bc) or _fmt_of(y) != fmt:
+            raise ValueError("detector: observation length must match antenna count")
+        _need(H, "H")
+        _need(y, "y")
+        C_total = Cn if C_total is None else C_total
+        fu = _fusion(fusion)
+        dev = H.device
+        if x_local is None and want_local:
+            x_local = complex_empty((S, Cn, U), fmt, dev)
+        if fu == FUSION_OPTIMAL and sigma2 is None:
+            sigma2 = torch.empty((S, Cn), dtype=torch.float32, device=dev)
+        if xhat is None and want_xhat:
+            xhat = torch.empty((S, U), dtype=torch.complex64, device=dev)
+        wsum = None
+        if want_xhat and fu == FUSION_OPTIMAL and C_total > Cn:
+            wsum = torch.empty((S,), dtype=torch.float32, device=dev)
+        check(lib().dcdg_ul_detect(self._ctx, _ptr(H), _ptr(y), S, Cn, C_total, Bc, U, K, float(n0), float(ex), fmt,
+                                   fu, _ptr(x_local), _ptr(sigma2), _ptr(xhat), _ptr(wsum), self._stream(stream)))
+        return UplinkResult(x_local, xhat, sigma2, wsum)
+
+    def post_eq_variance(self, H, *, n0: float, ex: float = 1.0, out=None, stream=None):
+        fmt = _fmt_of(H)
+        S, Cn, U, Bc = _shape(H, fmt)
+        _need(H, "H")
+        if out is None:
+            out = torch.empty((S, Cn), dtype=torch.float32, device=H.device)
+        check(lib().dcdg_post_eq_variance(self._ctx, _ptr(H), S * Cn, Bc, U, float(n0), float(ex), fmt, _ptr(out),
+                                          self._stream(stream)))
+        return out
+
+    def fuse(self, x_local, sigma2=None, *, fusion="uniform", C_total=None, xhat=None, wsum=None, stream=None):
+        fmt = _fmt_of(x_local)
+        S, Cn, U = _shape(x_local, fmt)
+        C_total = Cn if C_total is None else C_total
+        if xhat is None:
+            xhat = torch.empty((S, U), dtype=torch.complex64, device=x_local.device)
+        check(lib().dcdg_fuse(self._ctx, _ptr(x_local), _ptr(sigma2), S, Cn, C_total, U, fmt, _fusion(fusion),
+                              _ptr(xhat), _ptr(wsum), self._stream(stream)))
+        return xhat
+
+    def fuse_finalize(self, xhat, wsum, stream=None):
+        S, U = xhat.shape
+        check(lib().dcdg_fuse_finalize(self._ctx, _ptr(xhat), _ptr(wsum), S, U, self._stream(stream)))
+        return xhat
+
+    def fusion_weights(self, sigma2, stream=None):
+        S, Cn = sigma2.shape
+        w = torch.empty_like(sigma2)
+        check(lib().dcdg_fusion_weights(self._ctx, _ptr(sigma2), S, Cn, _ptr(w), self._stream(stream)))
+        return w
+
+    # ---------------------------------------------------------------- downlink
+    def dl_precode(self, H, s, *, rho: float, K: int = 3, C_total=None, want_gain: bool = True, x=None,
+                   gain_part=None, gain=None, stream=None) -> DownlinkResult:
+        fmt = _fmt_of(H)
+        S, Cn, U, Bc = _shape(H, fmt)
+        if _shape(s, fmt) != (S, U) or _fmt_of(s) != fmt:
+            raise ValueError("precoder: symbol count must match user count")
+        _need(H, "H")
+        _need(s, "s")
+        C_total = Cn if C_total is None else C_total
+        dev = H.device
+        if x is None:
+            x = complex_empty((S, Cn, Bc), fmt, dev)
+        if want_gain and gain_part is None:
+            gain_part = torch.empty((S, Cn), dtype=torch.float32, device=dev)
+        if want_gain and gain is None and Cn == C_total:
+            gain = torch.empty((S,), dtype=torch.float32, device=dev)
+        check(lib().dcdg_dl_precode(self._ctx, _ptr(H), _ptr(s), S, Cn, C_total, Bc, U, K, float(rho), fmt, _ptr(x),
+                                    _ptr(gain_part), _ptr(gain), self._stream(stream)))
+        return DownlinkResult(x, gain_part, gain)
+
+    def power_scale(self, x, rho: float, stream=None):
+        fmt = _fmt_of(x)
+        shp = _shape(x, fmt)
+        n = shp[-1]
+        P = math.prod(shp[:-1]) if len(shp) > 1 else 1
+        check(lib().dcdg_power_scale(self._ctx, _ptr(x), P, n, float(rho), fmt, self._stream(stream)))
+        return x
+
+    def gain_reduce(self, gain_part, s, stream=None):
+        fmt = _fmt_of(s)
+        S, U = _shape(s, fmt)
+        Cn = gain_part.shape[1]
+        g = torch.empty((S,), dtype=torch.float32, device=s.device)
+        check(lib().dcdg_gain_reduce(self._ctx, _ptr(gain_part), _ptr(s), S, Cn, U, fmt, _ptr(g), self._stream(stream)))
+        return g
+
+    def round_fp16(self, t, stream=None):
+        """In-place binary16 rounding of an fp32/complex64 tensor (wire format)."""
+        n = t.numel() * (2 if t.is_complex() else 1)
+        check(lib().dcdg_round_fp16(self._ctx, _ptr(t), n, self._stream(stream)))
+        return t
+
+
+def kernel_name(direction: str, bc: int, u: int, fmt: str) -> str:
+    return _lib.kernel_name(0 if direction == "ul" else 1, bc, u, FP16 if fmt == "fp16" else FP32)
