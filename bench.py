@@ -126,7 +126,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1902_08653_b200 import Engine, kernel_name, to_fp16
+    from paper_1902_08653_b200 import Engine, kernel_name, to_fp16_pairs
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -145,7 +145,7 @@ def run_ours(args):
 
     H, y, xs, n0 = make_inputs(S, c_local, dev, 1234 + rank)
     if fmt == "fp16":
-        H, y = to_fp16(H), to_fp16(y)
+        H, y = to_fp16_pairs(H), to_fp16_pairs(y)
     P = S * c_local
     xhat = torch.empty((S, U), dtype=torch.complex64, device=dev)
     x_local = torch.empty((S, c_local, U), dtype=torch.complex64, device=dev) if fmt == "fp32" else \

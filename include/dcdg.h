@@ -36,8 +36,12 @@
  *   xhat [S][U]      fused uplink estimate (always complex fp32)
  *   x_dl [P][B_c]    per-cluster beamformers, already power-scaled
  * "complex" is interleaved (re, im): float2 for DCDG_FP32, two IEEE binary16
- * for DCDG_FP16 (the paper's half-precision path).  Buffers must be 16-byte
- * aligned.
+ * for DCDG_FP16 (the paper's half-precision path) — except the DCDG_FP16
+ * channel tiles H and receive vectors y, which are stored ROW-PAIR PLANAR:
+ * rows (2i, 2i+1) of a column/vector occupy 8 bytes as
+ * {re_2i, re_2i+1, im_2i, im_2i+1}, so the half2 kernels load planar half2
+ * pairs directly (B_c must be even; dcdg_convert(..., DCDG_FP16_PAIRS, ...)
+ * produces this layout from complex fp32).  Buffers must be 16-byte aligned.
  *
  * Errors: every call returns a dcdg_status.  Argument errors are detected on
  * the host before any launch and carry the reference's exception text
@@ -66,7 +70,7 @@ typedef enum {
   DCDG_ENCCL = 4
 } dcdg_status;
 
-typedef enum { DCDG_FP32 = 0, DCDG_FP16 = 1 } dcdg_format;
+typedef enum { DCDG_FP32 = 0, DCDG_FP16 = 1, DCDG_FP16_PAIRS = 2 /* conversion only */ } dcdg_format;
 typedef enum { DCDG_FUSION_OPTIMAL = 0, DCDG_FUSION_UNIFORM = 1 } dcdg_fusion; /* detect.hpp:24 */
 
 typedef struct dcdg_ctx dcdg_ctx;
@@ -155,7 +159,9 @@ uint64_t dcdg_launch_count(dcdg_ctx* ctx);
  * (precision.cpp:43-72, detect.cpp:170-173, precode.cpp:159-160). */
 int dcdg_round_fp16(dcdg_ctx* ctx, float* x, int64_t n, void* stream);
 
-/* Format conversion on the device: fp32 complex <-> fp16 complex (RNE). */
+/* Format conversion on the device: fp32 complex <-> fp16 complex (RNE),
+ * interleaved (DCDG_FP16) or row-pair planar (DCDG_FP16_PAIRS, n_complex
+ * even) — the latter is the DCDG_FP16 layout of H and y. */
 int dcdg_convert(dcdg_ctx* ctx, const void* src, int src_fmt, void* dst, int dst_fmt,
                  int64_t n_complex, void* stream);
 

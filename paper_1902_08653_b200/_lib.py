@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdcdg.so")
+LIB_PATH = os.environ.get("DCDG_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdcdg.so")
 
 DCDG_OK, DCDG_EINVAL, DCDG_ENUMERIC, DCDG_ECUDA, DCDG_ENCCL = 0, 1, 2, 3, 4
 FP32, FP16 = 0, 1

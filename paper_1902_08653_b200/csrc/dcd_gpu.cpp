@@ -59,6 +59,32 @@ void pack(const cf64* v, std::size_t n, int fmt, unsigned char* out) {
   }
 }
 
+// Rows of a tile / receive vector on the device: fp16 tiles are row-pair
+// planar (include/dcdg.h), so an odd antenna count is padded with one zero
+// row (a zero row leaves every CD iterate unchanged).
+std::size_t dev_rows(std::size_t b, int fmt) { return fmt == DCDG_FP16 ? (b + 1) & ~std::size_t(1) : b; }
+
+// Column-major b x u block (or a b-vector when u == 1) into the device tile
+// layout: fp32 interleaved; fp16 row-pair planar {re_2i, re_2i+1, im_2i, im_2i+1}.
+void pack_tile(const cf64* v, std::size_t b, std::size_t u, int fmt, unsigned char* out) {
+  if (fmt != DCDG_FP16) {
+    pack(v, b * u, fmt, out);
+    return;
+  }
+  const std::size_t bp = dev_rows(b, fmt);
+  auto* h = reinterpret_cast<__half*>(out);
+  for (std::size_t j = 0; j < u; ++j)
+    for (std::size_t i = 0; i < bp; i += 2) {
+      const cf64 a = v[j * b + i];
+      const cf64 c = i + 1 < b ? v[j * b + i + 1] : cf64{0.0, 0.0};
+      __half* o = h + 2 * (j * bp + i);
+      o[0] = __double2half(a.real());
+      o[1] = __double2half(c.real());
+      o[2] = __double2half(a.imag());
+      o[3] = __double2half(c.imag());
+    }
+}
+
 void unpack(const unsigned char* in, std::size_t n, int fmt, cf64* out) {
   if (fmt == DCDG_FP16) {
     const auto* h = reinterpret_cast<const __half*>(in);
@@ -187,14 +213,14 @@ ComplexVector cd_detect(const ComplexMatrix& h, const ComplexVector& y, double n
   std::lock_guard<std::mutex> lk(g_default_mu);
   Engine& eng = default_engine();
   const DevPrecision dp = map_precision(prec);
-  const std::size_t b = h.rows(), u = h.cols(), es = esize(dp.fmt);
-  std::vector<unsigned char> hb(b * u * es), yb(b * es), xb(u * es);
-  pack(h.flat().data(), b * u, dp.fmt, hb.data());
-  pack(y.data(), b, dp.fmt, yb.data());
+  const std::size_t b = h.rows(), u = h.cols(), es = esize(dp.fmt), bd = dev_rows(b, dp.fmt);
+  std::vector<unsigned char> hb(bd * u * es), yb(bd * es), xb(u * es);
+  pack_tile(h.flat().data(), b, u, dp.fmt, hb.data());
+  pack_tile(y.data(), b, 1, dp.fmt, yb.data());
   DevMem dh(hb.size()), dy(yb.size()), dx(xb.size());
   h2d(dh.p, hb.data(), hb.size(), eng.stream());
   h2d(dy.p, yb.data(), yb.size(), eng.stream());
-  Engine::check(dcdg_ul_detect(eng.ctx(), dh.p, dy.p, 1, 1, 1, static_cast<int>(b), static_cast<int>(u),
+  Engine::check(dcdg_ul_detect(eng.ctx(), dh.p, dy.p, 1, 1, 1, static_cast<int>(bd), static_cast<int>(u),
                                static_cast<int>(t_max), n0, ex, dp.fmt, DCDG_FUSION_UNIFORM, dx.p, nullptr, nullptr,
                                nullptr, eng.stream()));
   d2h(xb.data(), dx.p, xb.size(), eng.stream());
@@ -266,14 +292,14 @@ DetectionResult decentralized_cd_detect(std::span<const ClusterData> clusters, c
   for (std::size_t c = 0; c < nc; ++c) {
     hoff[c] = hbytes;
     yoff[c] = ybytes;
-    const std::size_t b = clusters[c].h.rows();
+    const std::size_t b = dev_rows(clusters[c].h.rows(), dp.fmt);
     hbytes += uniform_bc ? b * u * es : align_up(b * u * es);
     ybytes += uniform_bc ? b * es : align_up(b * es);
   }
   std::vector<unsigned char> hb(hbytes), yb(ybytes);
   for (std::size_t c = 0; c < nc; ++c) {
-    pack(clusters[c].h.flat().data(), clusters[c].h.rows() * u, dp.fmt, hb.data() + hoff[c]);
-    pack(clusters[c].y.data(), clusters[c].y.size(), dp.fmt, yb.data() + yoff[c]);
+    pack_tile(clusters[c].h.flat().data(), clusters[c].h.rows(), u, dp.fmt, hb.data() + hoff[c]);
+    pack_tile(clusters[c].y.data(), clusters[c].y.size(), 1, dp.fmt, yb.data() + yoff[c]);
   }
   const std::size_t xl_bytes = nc * u * es;
   DevMem dh(hbytes), dy(ybytes), dxl(xl_bytes), ds2(nc * sizeof(float)), dxh(u * 8), dw(nc * sizeof(float));
@@ -283,13 +309,13 @@ DetectionResult decentralized_cd_detect(std::span<const ClusterData> clusters, c
   const int ui = static_cast<int>(u), K = static_cast<int>(cfg.t_max);
   if (uniform_bc) {
     Engine::check(dcdg_ul_detect(eng.ctx(), dh.p, dy.p, 1, static_cast<int>(nc), static_cast<int>(nc),
-                                 static_cast<int>(clusters[0].h.rows()), ui, K, cfg.n0, cfg.ex, dp.fmt, fusion, dxl.p,
+                                 static_cast<int>(dev_rows(clusters[0].h.rows(), dp.fmt)), ui, K, cfg.n0, cfg.ex, dp.fmt, fusion, dxl.p,
                                  optimal ? ds2.as<float>() : nullptr, nullptr, nullptr, eng.stream()));
   } else {
     for (std::size_t c = 0; c < nc; ++c)
       Engine::check(dcdg_ul_detect(eng.ctx(), static_cast<unsigned char*>(dh.p) + hoff[c],
                                    static_cast<unsigned char*>(dy.p) + yoff[c], 1, 1, 1,
-                                   static_cast<int>(clusters[c].h.rows()), ui, K, cfg.n0, cfg.ex, dp.fmt, fusion,
+                                   static_cast<int>(dev_rows(clusters[c].h.rows(), dp.fmt)), ui, K, cfg.n0, cfg.ex, dp.fmt, fusion,
                                    static_cast<unsigned char*>(dxl.p) + c * u * es,
                                    optimal ? ds2.as<float>() + c : nullptr, nullptr, nullptr, eng.stream()));
   }
@@ -340,17 +366,17 @@ ComplexVector cd_precode(const ComplexMatrix& h_dl, const ComplexVector& s, unsi
   std::lock_guard<std::mutex> lk(g_default_mu);
   Engine& eng = default_engine();
   const DevPrecision dp = map_precision(prec);
-  const std::size_t u = h_dl.rows(), b = h_dl.cols(), es = esize(dp.fmt);
+  const std::size_t u = h_dl.rows(), b = h_dl.cols(), es = esize(dp.fmt), bd = dev_rows(b, dp.fmt);
   std::vector<cf64> tile(b * u);
   uplink_tile_of(h_dl, tile.data());
-  std::vector<unsigned char> hb(b * u * es), sb(u * es), xb(b * es);
-  pack(tile.data(), b * u, dp.fmt, hb.data());
+  std::vector<unsigned char> hb(bd * u * es), sb(u * es), xb(bd * es);
+  pack_tile(tile.data(), b, u, dp.fmt, hb.data());
   pack(s.data(), u, dp.fmt, sb.data());
   DevMem dh(hb.size()), ds(sb.size()), dx(xb.size());
   h2d(dh.p, hb.data(), hb.size(), eng.stream());
   h2d(ds.p, sb.data(), sb.size(), eng.stream());
   // rho == 0: unnormalised beamformer, exactly what cd_precode returns
-  Engine::check(dcdg_dl_precode(eng.ctx(), dh.p, ds.p, 1, 1, 1, static_cast<int>(b), static_cast<int>(u),
+  Engine::check(dcdg_dl_precode(eng.ctx(), dh.p, ds.p, 1, 1, 1, static_cast<int>(bd), static_cast<int>(u),
                                 static_cast<int>(t_max), 0.0, dp.fmt, dx.p, nullptr, nullptr, eng.stream()));
   d2h(xb.data(), dx.p, xb.size(), eng.stream());
   eng.sync();
@@ -399,18 +425,18 @@ PrecodeResult decentralized_cd_precode(std::span<const ComplexMatrix> h_dl_block
   std::vector<std::size_t> hoff(nc), xoff(nc);
   std::size_t hbytes = 0, xbytes = 0, btot = 0;
   for (std::size_t c = 0; c < nc; ++c) {
-    const std::size_t b = h_dl_blocks[c].cols();
+    const std::size_t b = dev_rows(h_dl_blocks[c].cols(), dp.fmt);
     hoff[c] = hbytes;
     xoff[c] = xbytes;
     hbytes += uniform_bc ? b * u * es : align_up(b * u * es);
     xbytes += uniform_bc ? b * es : align_up(b * es);
-    btot += b;
+    btot += h_dl_blocks[c].cols();
   }
   std::vector<unsigned char> hb(hbytes), sb(u * es), xb(xbytes);
   for (std::size_t c = 0; c < nc; ++c) {
     std::vector<cf64> tile(h_dl_blocks[c].cols() * u);
     uplink_tile_of(h_dl_blocks[c], tile.data());
-    pack(tile.data(), tile.size(), dp.fmt, hb.data() + hoff[c]);
+    pack_tile(tile.data(), h_dl_blocks[c].cols(), u, dp.fmt, hb.data() + hoff[c]);
   }
   pack(s.data(), u, dp.fmt, sb.data());
   DevMem dh(hbytes), ds(sb.size()), dx(xbytes), dgp(nc * sizeof(float)), dg(sizeof(float));
@@ -421,14 +447,15 @@ PrecodeResult decentralized_cd_precode(std::span<const ComplexMatrix> h_dl_block
     Engine::check(dcdg_round_fp16(eng.ctx(), ds.as<float>(), static_cast<int64_t>(2 * u), eng.stream()));
   const int ui = static_cast<int>(u), K = static_cast<int>(cfg.t_max), nci = static_cast<int>(nc);
   if (uniform_bc) {
-    Engine::check(dcdg_dl_precode(eng.ctx(), dh.p, ds.p, 1, nci, nci, static_cast<int>(h_dl_blocks[0].cols()), ui, K,
+    Engine::check(dcdg_dl_precode(eng.ctx(), dh.p, ds.p, 1, nci, nci,
+                                  static_cast<int>(dev_rows(h_dl_blocks[0].cols(), dp.fmt)), ui, K,
                                   cfg.rho, dp.fmt, dx.p, dgp.as<float>(), nullptr, eng.stream()));
   } else {
     // each cluster is its own launch; rho/sqrt(C) is applied with C = nc
     const double rho_1 = cfg.rho / std::sqrt(static_cast<double>(nc));
     for (std::size_t c = 0; c < nc; ++c)
       Engine::check(dcdg_dl_precode(eng.ctx(), static_cast<unsigned char*>(dh.p) + hoff[c], ds.p, 1, 1, 1,
-                                    static_cast<int>(h_dl_blocks[c].cols()), ui, K, rho_1, dp.fmt,
+                                    static_cast<int>(dev_rows(h_dl_blocks[c].cols(), dp.fmt)), ui, K, rho_1, dp.fmt,
                                     static_cast<unsigned char*>(dx.p) + xoff[c], dgp.as<float>() + c, nullptr,
                                     eng.stream()));
   }

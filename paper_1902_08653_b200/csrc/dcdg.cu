@@ -12,7 +12,8 @@
 #include <string>
 
 #include "dcdg.h"
-#include "dcdg_kernels.cuh"
+#include "dcdg_aux_kernels.cuh"
+#include "dcdg_reg_kernels.cuh"
 
 struct dcdg_ctx {
   int device = 0;
@@ -61,7 +62,13 @@ inline size_t esize(int fmt) { return fmt == DCDG_FP16 ? 4 : 8; }
 // ---------------------------------------------------------------------------
 // launchers for the register-resident kernels
 // ---------------------------------------------------------------------------
-constexpr int kWarps = 4;
+#ifndef DCDG_CTA_WARPS
+#define DCDG_CTA_WARPS 1
+#endif
+// Warps per CTA of the register-resident kernels.  Each warp owns its own
+// staging slot and mbarrier, so CTAs need no block-level synchronisation;
+// one-warp CTAs let occupancy follow the register budget exactly.
+constexpr int kWarps = DCDG_CTA_WARPS;
 
 template <typename Kern>
 int occupancy_of(Kern kern, size_t smem) {
@@ -75,12 +82,13 @@ using UlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, 
 using DlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, int, float, void*, float*,
                                  cudaStream_t);
 
-template <int BC, int U, int G>
+template <int BC, int U, int G, int MINB>
 cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
                           cudaStream_t st) {
   constexpr int NPW = 32 / G;
-  constexpr size_t smem = kWarps * NPW * (BC * U * 8 + BC * 8) + kWarps * 8;
-  auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps>;
+  constexpr size_t smem =
+      dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U), NPW, kWarps>::kBytes;
+  auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps, MINB>;
   static const int occ = occupancy_of(kern, smem);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
@@ -89,12 +97,13 @@ cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, in
   return cudaGetLastError();
 }
 
-template <int BC, int U, int G>
+template <int BC, int U, int G, int MINB>
 cudaError_t launch_ul_f16(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
                           cudaStream_t st) {
   constexpr int NPW = 32 / G;
-  constexpr size_t smem = kWarps * NPW * (BC * U * 4 + BC * 4) + kWarps * 8;
-  auto kern = dcdg::ul_reg_f16<BC, U, G, kWarps>;
+  constexpr size_t smem =
+      dcdg::CtaSmem<NPW*(BC * U * 4 + BC * 4), dcdg::ul_scal_bytes(U), NPW, kWarps>::kBytes;
+  auto kern = dcdg::ul_reg_f16<BC, U, G, kWarps, MINB>;
   static const int occ = occupancy_of(kern, smem);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
@@ -103,48 +112,48 @@ cudaError_t launch_ul_f16(dcdg_ctx* ctx, const void* H, const void* Y, int P, in
   return cudaGetLastError();
 }
 
-template <int BC, int U, int G>
-cudaError_t launch_dl_f32(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
-                          float* gp, cudaStream_t st) {
+template <int BC, int U, int G, int MINB, bool GAIN>
+cudaError_t launch_dl_f32_k(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
+                            float* gp, cudaStream_t st) {
   constexpr int NPW = 32 / G;
-  constexpr size_t smem = kWarps * NPW * (BC * U * 8 + U * 8) + kWarps * 8;
+  constexpr size_t smem =
+      dcdg::CtaSmem<NPW*(BC * U * 8 + U * 8), dcdg::dl_scal_bytes(U), NPW, kWarps>::kBytes;
+  auto kern = dcdg::dl_reg_f32<BC, U, G, kWarps, MINB, GAIN>;
+  static const int occ = occupancy_of(kern, smem);
   const int nsets = (P + NPW - 1) / NPW;
-  if (gp) {
-    auto kern = dcdg::dl_reg_f32<BC, U, G, kWarps, true>;
-    static const int occ = occupancy_of(kern, smem);
-    const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
-    kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(S), P, C, K,
-                                            rho_c, static_cast<float2*>(X), gp, ctx->d_status);
-  } else {
-    auto kern = dcdg::dl_reg_f32<BC, U, G, kWarps, false>;
-    static const int occ = occupancy_of(kern, smem);
-    const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
-    kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(S), P, C, K,
-                                            rho_c, static_cast<float2*>(X), gp, ctx->d_status);
-  }
+  const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
+  kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(S), P, C, K, rho_c,
+                                          static_cast<float2*>(X), gp, ctx->d_status);
   return cudaGetLastError();
 }
 
-template <int BC, int U, int G>
+template <int BC, int U, int G, int MINB>
+cudaError_t launch_dl_f32(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
+                          float* gp, cudaStream_t st) {
+  return gp ? launch_dl_f32_k<BC, U, G, MINB, true>(ctx, H, S, P, C, K, rho_c, X, gp, st)
+            : launch_dl_f32_k<BC, U, G, MINB, false>(ctx, H, S, P, C, K, rho_c, X, gp, st);
+}
+
+template <int BC, int U, int G, int MINB, bool GAIN>
+cudaError_t launch_dl_f16_k(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
+                            float* gp, cudaStream_t st) {
+  constexpr int NPW = 32 / G;
+  constexpr size_t smem =
+      dcdg::CtaSmem<NPW*(BC * U * 4 + U * 4), dcdg::dl_scal_bytes(U), NPW, kWarps>::kBytes;
+  auto kern = dcdg::dl_reg_f16<BC, U, G, kWarps, MINB, GAIN>;
+  static const int occ = occupancy_of(kern, smem);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
+  kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(S), P, C, K,
+                                          rho_c, static_cast<__half2*>(X), gp, ctx->d_status);
+  return cudaGetLastError();
+}
+
+template <int BC, int U, int G, int MINB>
 cudaError_t launch_dl_f16(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
                           float* gp, cudaStream_t st) {
-  constexpr int NPW = 32 / G;
-  constexpr size_t smem = kWarps * NPW * (BC * U * 4 + U * 4) + kWarps * 8;
-  const int nsets = (P + NPW - 1) / NPW;
-  if (gp) {
-    auto kern = dcdg::dl_reg_f16<BC, U, G, kWarps, true>;
-    static const int occ = occupancy_of(kern, smem);
-    const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
-    kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(S), P, C, K,
-                                            rho_c, static_cast<__half2*>(X), gp, ctx->d_status);
-  } else {
-    auto kern = dcdg::dl_reg_f16<BC, U, G, kWarps, false>;
-    static const int occ = occupancy_of(kern, smem);
-    const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
-    kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(S), P, C, K,
-                                            rho_c, static_cast<__half2*>(X), gp, ctx->d_status);
-  }
-  return cudaGetLastError();
+  return gp ? launch_dl_f16_k<BC, U, G, MINB, true>(ctx, H, S, P, C, K, rho_c, X, gp, st)
+            : launch_dl_f16_k<BC, U, G, MINB, false>(ctx, H, S, P, C, K, rho_c, X, gp, st);
 }
 
 struct Spec {
@@ -153,16 +162,36 @@ struct Spec {
   DlLaunch dl;
 };
 
-#define SPEC_F32(BC, U, G) {BC, U, DCDG_FP32, G, launch_ul_f32<BC, U, G>, launch_dl_f32<BC, U, G>}
-#define SPEC_F16(BC, U, G) {BC, U, DCDG_FP16, G, launch_ul_f16<BC, U, G>, launch_dl_f16<BC, U, G>}
+#define SPEC_F32(BC, U, G)                                                           \
+  {BC, U, DCDG_FP32, G, launch_ul_f32<BC, U, G, minb(DCDG_MIN_WARPS_UL_F32)>, \
+   launch_dl_f32<BC, U, G, minb(DCDG_MIN_WARPS_DL_F32)>}
+#define SPEC_F16(BC, U, G)                                                           \
+  {BC, U, DCDG_FP16, G, launch_ul_f16<BC, U, G, minb(DCDG_MIN_WARPS_UL_F16)>, \
+   launch_dl_f16<BC, U, G, minb(DCDG_MIN_WARPS_DL_F16)>}
 
 // Register-resident specialisations: B_c*U/G complex per lane = 128 regs of
 // channel for fp32 (64-128 for fp16).  Everything else runs the generic path.
+// Minimum resident warps per SM requested from ptxas per kernel family
+// (register cap = 65536 / (32 * warps)); tuned on B200 with scripts/kbench.py.
+#ifndef DCDG_MIN_WARPS_UL_F32
+#define DCDG_MIN_WARPS_UL_F32 8
+#endif
+#ifndef DCDG_MIN_WARPS_DL_F32
+#define DCDG_MIN_WARPS_DL_F32 10
+#endif
+#ifndef DCDG_MIN_WARPS_UL_F16
+#define DCDG_MIN_WARPS_UL_F16 8
+#endif
+#ifndef DCDG_MIN_WARPS_DL_F16
+#define DCDG_MIN_WARPS_DL_F16 8
+#endif
+constexpr int minb(int warps) { return warps / kWarps > 0 ? warps / kWarps : 1; }
+
 const Spec kSpecs[] = {
-    SPEC_F32(32, 16, 8),  // north-star target: B=256, C=8, U=16
-    SPEC_F32(32, 8, 4),   // paper / config 1: B_c=32, U=8
-    SPEC_F32(16, 16, 4),  // B=128, C=8
-    SPEC_F32(64, 16, 16), // B=256, C=4 / B=512, C=8
+    SPEC_F32(32, 16, 8),   // north-star target: B=256, C=8, U=16
+    SPEC_F32(32, 8, 4),    // paper / config 1: B_c=32, U=8
+    SPEC_F32(16, 16, 4),   // B=128, C=8
+    SPEC_F32(64, 16, 16),  // B=256, C=4 / B=512, C=8
     SPEC_F32(64, 8, 8),
     SPEC_F16(32, 16, 4),
     SPEC_F16(32, 8, 4),
@@ -329,6 +358,8 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
   if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "detector: empty channel matrix");
   if (n0 < 0.0 || !(ex > 0.0)) return fail(DCDG_EINVAL, "detector: need N0 >= 0 and E_x > 0");
   if (K <= 0) return fail(DCDG_EINVAL, "cd_detect: need at least one sweep");
+  if (fmt == DCDG_FP16 && (Bc & 1))
+    return fail(DCDG_EINVAL, "dcdg: fp16 row-pair planar tiles need an even antenna count B_c");
   const bool optimal = fusion == DCDG_FUSION_OPTIMAL;
   if (fusion != DCDG_FUSION_OPTIMAL && fusion != DCDG_FUSION_UNIFORM)
     return fail(DCDG_EINVAL, "dcdg_ul_detect: unknown fusion mode");
@@ -393,6 +424,8 @@ int dcdg_dl_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, i
     return fail(DCDG_EINVAL, "decentralized_cd_precode: cluster 0 has " + std::to_string(Bc) + " antennas for " +
                                  std::to_string(U) + " users; local zero-forcing needs B_c >= U");
   if (K <= 0) return fail(DCDG_EINVAL, "cd_precode: need at least one sweep");
+  if (fmt == DCDG_FP16 && (Bc & 1))
+    return fail(DCDG_EINVAL, "dcdg: fp16 row-pair planar tiles need an even antenna count B_c");
   if (rho < 0.0 || std::isnan(rho)) return fail(DCDG_EINVAL, "power_scale: amplitude must be positive");
   if (gain && C != C_total) return fail(DCDG_EINVAL, "dcdg_dl_precode: effective gain needs every cluster (C == C_total)");
   if (!H || !s || !x_dl) return fail(DCDG_EINVAL, "dcdg_dl_precode: null buffer");
@@ -440,6 +473,8 @@ int dcdg_post_eq_variance(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, do
   if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "post_eq_variance: empty channel block");
   if (!(n0 > 0.0) || !(ex > 0.0)) return fail(DCDG_EINVAL, "post_eq_variance: need N0 > 0 and E_x > 0");
   if (U > 32) return fail(DCDG_EINVAL, "dcdg_post_eq_variance: U > 32 not supported");
+  if (fmt == DCDG_FP16 && (Bc & 1))
+    return fail(DCDG_EINVAL, "dcdg: fp16 row-pair planar tiles need an even antenna count B_c");
   if (P <= 0) return DCDG_OK;
   CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
   return launch_post_eq(ctx, H, P, Bc, U, n0, ex, fmt, sigma2, as_stream(stream));
@@ -533,22 +568,33 @@ int dcdg_round_fp16(dcdg_ctx* ctx, float* x, int64_t n, void* stream) {
 int dcdg_convert(dcdg_ctx* ctx, const void* src, int src_fmt, void* dst, int dst_fmt, int64_t n_complex,
                  void* stream) {
   if (int rc = check_ctx(ctx)) return rc;
-  if (int rc = check_fmt(src_fmt)) return rc;
-  if (int rc = check_fmt(dst_fmt)) return rc;
+  auto ok = [](int f) { return f == DCDG_FP32 || f == DCDG_FP16 || f == DCDG_FP16_PAIRS; };
+  if (!ok(src_fmt) || !ok(dst_fmt)) return fail(DCDG_EINVAL, "dcdg: unknown storage format");
   if (n_complex <= 0) return DCDG_OK;
+  if ((src_fmt == DCDG_FP16_PAIRS || dst_fmt == DCDG_FP16_PAIRS) && (n_complex & 1))
+    return fail(DCDG_EINVAL, "dcdg_convert: row-pair planar fp16 needs an even element count");
   CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
   cudaStream_t st = as_stream(stream);
   const long long n = 2 * n_complex;
   const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
   if (src_fmt == dst_fmt) {
-    CUDA_TRY(cudaMemcpyAsync(dst, src, static_cast<size_t>(n_complex) * esize(src_fmt), cudaMemcpyDeviceToDevice, st),
+    CUDA_TRY(cudaMemcpyAsync(dst, src, static_cast<size_t>(n_complex) * esize(src_fmt == DCDG_FP32 ? DCDG_FP32 : DCDG_FP16),
+                             cudaMemcpyDeviceToDevice, st),
              "convert copy");
     return DCDG_OK;
   }
-  if (src_fmt == DCDG_FP32)
+  if (src_fmt == DCDG_FP32 && dst_fmt == DCDG_FP16)
     dcdg::f32_to_f16_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(src), static_cast<__half*>(dst), n);
-  else
+  else if (src_fmt == DCDG_FP16 && dst_fmt == DCDG_FP32)
     dcdg::f16_to_f32_kernel<<<blocks, 256, 0, st>>>(static_cast<const __half*>(src), static_cast<float*>(dst), n);
+  else if (src_fmt == DCDG_FP32 && dst_fmt == DCDG_FP16_PAIRS)
+    dcdg::f32_to_f16_pairs_kernel<<<blocks, 256, 0, st>>>(static_cast<const float4*>(src), static_cast<uint2*>(dst),
+                                                          n_complex / 2);
+  else if (src_fmt == DCDG_FP16_PAIRS && dst_fmt == DCDG_FP32)
+    dcdg::f16_pairs_to_f32_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint2*>(src), static_cast<float4*>(dst),
+                                                          n_complex / 2);
+  else
+    return fail(DCDG_EINVAL, "dcdg_convert: unsupported conversion (go through DCDG_FP32)");
   ++ctx->launches;
   CUDA_TRY(cudaGetLastError(), "convert launch");
   return DCDG_OK;

@@ -1,0 +1,384 @@
+// Generic (any-shape) CD kernels, the post-equalization variance, fusion,
+// gain reduction, power scaling and format conversion kernels.
+#pragma once
+
+#include "dcdg_device.cuh"
+
+namespace dcdg {
+
+// ===========================================================================
+// Generic kernels: any B_c, U (one warp per problem, fp32 math).  Used for
+// shapes without a register-resident specialisation and for fp16 shapes
+// whose B_c is not a multiple of 4G.  Residual / beamformer and scalars live
+// in shared memory; lane l owns rows l, l+32, ...
+// ===========================================================================
+template <typename T>
+__global__ void __launch_bounds__(128) ul_generic(const T* __restrict__ H, const T* __restrict__ Y, int P, int BC,
+                                                  int U, int K, float kappa, T* __restrict__ X) {
+  extern __shared__ float2 gsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long p = static_cast<long long>(blockIdx.x) * 4 + warp;
+  if (p >= P) return;
+  float2* r = gsm + warp * (BC + 2 * U);
+  float2* x = r + BC;
+  float2* mn = x + U;
+  const T* h = H + static_cast<size_t>(p) * BC * U;
+  for (int i = lane; i < BC; i += 32) r[i] = ldv(Y + static_cast<size_t>(p) * BC, i);
+  for (int j = 0; j < U; ++j) {
+    float e = 0.f;
+    for (int i = lane; i < BC; i += 32) {
+      const float2 v = ldv(h + static_cast<size_t>(j) * BC, i);
+      e = fmaf(v.y, v.y, fmaf(v.x, v.x, e));
+    }
+    e = warp_sum(e);
+    if (lane == 0) {
+      const float m = __frcp_rn(e + kappa);
+      mn[j] = make_float2(m, m * e);
+      x[j] = make_float2(0.f, 0.f);
+    }
+  }
+  __syncwarp();
+  for (int t = 0; t < K; ++t)
+    for (int j = 0; j < U; ++j) {
+      float dr = 0.f, di = 0.f;
+      for (int i = lane; i < BC; i += 32) {
+        const float2 hv = ldv(h + static_cast<size_t>(j) * BC, i);
+        const float2 rv = r[i];
+        dr = fmaf(hv.x, rv.x, fmaf(hv.y, rv.y, dr));
+        di = fmaf(hv.x, rv.y, fmaf(-hv.y, rv.x, di));
+      }
+      dr = warp_sum(dr);
+      di = warp_sum(di);
+      const float2 mnj = mn[j], xo = x[j];
+      const float nxr = fmaf(mnj.x, dr, mnj.y * xo.x), nxi = fmaf(mnj.x, di, mnj.y * xo.y);
+      const float dxr = nxr - xo.x, dxi = nxi - xo.y;
+      __syncwarp();
+      if (lane == 0) x[j] = make_float2(nxr, nxi);
+      for (int i = lane; i < BC; i += 32) {
+        const float2 hv = ldv(h + static_cast<size_t>(j) * BC, i);
+        float2 rv = r[i];
+        rv.x = fmaf(-dxr, hv.x, fmaf(dxi, hv.y, rv.x));
+        rv.y = fmaf(-dxr, hv.y, fmaf(-dxi, hv.x, rv.y));
+        r[i] = rv;
+      }
+      __syncwarp();
+    }
+  for (int j = lane; j < U; j += 32) stc(X, static_cast<size_t>(p) * U + j, x[j]);
+}
+
+template <typename T, bool GAIN>
+__global__ void __launch_bounds__(128)
+    dl_generic(const T* __restrict__ H, const T* __restrict__ Sy, int P, int C, int BC, int U, int K, float rho_c,
+               T* __restrict__ X, float* __restrict__ gain_part, unsigned long long* __restrict__ status) {
+  extern __shared__ float2 gsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long p = static_cast<long long>(blockIdx.x) * 4 + warp;
+  if (p >= P) return;
+  float2* x = gsm + warp * (BC + 2 * U);
+  float2* sb = x + BC;  // normalised targets
+  float* pn = reinterpret_cast<float*>(sb + U);  // row normalisers
+  const T* h = H + static_cast<size_t>(p) * BC * U;
+  const T* s = Sy + static_cast<size_t>(p / C) * U;
+  int zero_user = -1;
+  for (int j = 0; j < U; ++j) {
+    float e = 0.f;
+    for (int i = lane; i < BC; i += 32) {
+      const float2 v = ldv(h + static_cast<size_t>(j) * BC, i);
+      e = fmaf(v.y, v.y, fmaf(v.x, v.x, e));
+    }
+    e = warp_sum(e);
+    if (e == 0.f && zero_user < 0) zero_user = j;
+    const float pj = __frcp_rn(__fsqrt_rn(e));
+    if (lane == 0) {
+      const float2 sv = ldc(s, j);
+      sb[j] = make_float2(sv.x * pj, sv.y * pj);
+      pn[j] = pj;
+    }
+  }
+  for (int i = lane; i < BC; i += 32) x[i] = make_float2(0.f, 0.f);
+  __syncwarp();
+  for (int t = 0; t < K; ++t)
+    for (int j = 0; j < U; ++j) {
+      const float pj = pn[j];
+      float dr = 0.f, di = 0.f;
+      for (int i = lane; i < BC; i += 32) {
+        float2 hv = ldv(h + static_cast<size_t>(j) * BC, i);
+        hv.x *= pj;
+        hv.y *= pj;
+        const float2 xv = x[i];
+        dr = fmaf(hv.x, xv.x, fmaf(hv.y, xv.y, dr));
+        di = fmaf(hv.x, xv.y, fmaf(-hv.y, xv.x, di));
+      }
+      dr = warp_sum(dr) - sb[j].x;
+      di = warp_sum(di) - sb[j].y;
+      for (int i = lane; i < BC; i += 32) {
+        float2 hv = ldv(h + static_cast<size_t>(j) * BC, i);
+        hv.x *= pj;
+        hv.y *= pj;
+        float2 xv = x[i];
+        xv.x = fmaf(-dr, hv.x, fmaf(di, hv.y, xv.x));
+        xv.y = fmaf(-dr, hv.y, fmaf(-di, hv.x, xv.y));
+        x[i] = xv;
+      }
+    }
+  float e = 0.f;
+  for (int i = lane; i < BC; i += 32) e = fmaf(x[i].y, x[i].y, fmaf(x[i].x, x[i].x, e));
+  e = warp_sum(e);
+  const float gsc = rho_c > 0.f ? rho_c / __fsqrt_rn(e) : 1.f;
+  float gq = 0.f;
+  for (int i = lane; i < BC; i += 32) {
+    const float2 xv = make_float2(x[i].x * gsc, x[i].y * gsc);
+    stc(X, static_cast<size_t>(p) * BC + i, xv);
+    if (GAIN) {
+      // v_i = sum_u s_u h_iu (unnormalised)
+      float vr = 0.f, vi = 0.f;
+      for (int j = 0; j < U; ++j) {
+        const float2 hv = ldv(h + static_cast<size_t>(j) * BC, i);
+        const float2 sv = ldc(s, j);
+        vr = fmaf(sv.x, hv.x, fmaf(-sv.y, hv.y, vr));
+        vi = fmaf(sv.x, hv.y, fmaf(sv.y, hv.x, vi));
+      }
+      gq = fmaf(vr, xv.x, fmaf(vi, xv.y, gq));
+    }
+  }
+  if (GAIN) gq = warp_sum(gq);
+  if (lane == 0) {
+    if (zero_user >= 0) record_status(status, p, ST_ZERO_ROW, zero_user);
+    else if (e == 0.f && rho_c > 0.f) record_status(status, p, ST_ZERO_BEAMFORMER, 0);
+    if (GAIN) gain_part[p] = gq;
+  }
+}
+
+// ===========================================================================
+// Post-equalization variance (optimal fusion), one warp per problem:
+// A = I + (Ex/N0) H^H H (Gram, detect.cpp:21-28,118-121); Cholesky A = L L^H
+// (numerics.cpp:45-58); sigma^2 = (Ex/U) tr(A^-1) = (Ex/U) ||L^-1||_F^2
+// (the reference sums U Cholesky solves, detect.cpp:122-129).
+// Shared memory per warp: A/L [U][U] + Z [U][U] complex fp32 (U <= 32).
+// ===========================================================================
+template <typename T>
+__global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int P, int BC, int U, float gam,
+                                                   float ex_over_u, bool round_fp16, float* __restrict__ sigma2,
+                                                   unsigned long long* __restrict__ status) {
+  extern __shared__ float2 vsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long p = static_cast<long long>(blockIdx.x) * 4 + warp;
+  if (p >= P) return;
+  float2* A = vsm + warp * (2 * U * U);  // column-major, lower triangle used
+  float2* Z = A + U * U;
+  const T* h = H + static_cast<size_t>(p) * BC * U;
+  const int ntri = U * (U + 1) / 2;
+  for (int e = lane; e < ntri; e += 32) {
+    // e -> (i >= j): column j, row i
+    int j = 0, rem = e;
+    while (rem >= U - j) {
+      rem -= U - j;
+      ++j;
+    }
+    const int i = j + rem;
+    float gr = 0.f, gi = 0.f;  // conj(h_i)^T h_j
+    for (int b = 0; b < BC; ++b) {
+      const float2 a = ldv(h + static_cast<size_t>(i) * BC, b);
+      const float2 c = ldv(h + static_cast<size_t>(j) * BC, b);
+      gr = fmaf(a.x, c.x, fmaf(a.y, c.y, gr));
+      gi = fmaf(a.x, c.y, fmaf(-a.y, c.x, gi));
+    }
+    A[j * U + i] = make_float2((i == j ? 1.f : 0.f) + gam * gr, gam * gi);
+  }
+  __syncwarp();
+  float maxdiag = 0.f;  // numerics.cpp:38-41 (pivot floor 1e-14 * max |A_jj|)
+  for (int j = lane; j < U; j += 32) maxdiag = fmaxf(maxdiag, fabsf(A[j * U + j].x));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) maxdiag = fmaxf(maxdiag, __shfl_xor_sync(0xffffffffu, maxdiag, o));
+  const float floor_ = 1e-14f * maxdiag;
+  bool singular = false;
+  // left-looking Cholesky, lanes parallel over rows i >= j
+  for (int j = 0; j < U; ++j) {
+    float d = A[j * U + j].x;
+    for (int kk = 0; kk < j; ++kk) {
+      const float2 l = A[kk * U + j];
+      d -= l.x * l.x + l.y * l.y;
+    }
+    if (!(d > floor_)) singular = true;
+    const float ljj = __fsqrt_rn(fmaxf(d, 1e-30f));
+    for (int i = j + 1 + lane; i < U; i += 32) {
+      float2 s = A[j * U + i];
+      for (int kk = 0; kk < j; ++kk) {
+        const float2 a = A[kk * U + i], b = A[kk * U + j];  // s -= L_ik conj(L_jk)
+        s.x -= a.x * b.x + a.y * b.y;
+        s.y -= a.y * b.x - a.x * b.y;
+      }
+      A[j * U + i] = make_float2(s.x / ljj, s.y / ljj);
+    }
+    __syncwarp();
+    if (lane == 0) A[j * U + j] = make_float2(ljj, 0.f);
+    __syncwarp();
+  }
+  // columns of L^-1: lane c solves L z = e_c (rows i >= c)
+  float tr = 0.f;
+  for (int c = lane; c < U; c += 32) {
+    for (int i = c; i < U; ++i) {
+      float sr = (i == c) ? 1.f : 0.f, si = 0.f;
+      for (int kk = c; kk < i; ++kk) {
+        const float2 l = A[kk * U + i], z = Z[c * U + kk];
+        sr -= l.x * z.x - l.y * z.y;
+        si -= l.x * z.y + l.y * z.x;
+      }
+      const float li = A[i * U + i].x;
+      const float2 z = make_float2(sr / li, si / li);
+      Z[c * U + i] = z;
+      tr = fmaf(z.x, z.x, fmaf(z.y, z.y, tr));
+    }
+  }
+  tr = warp_sum(tr);
+  if (lane == 0) {
+    float s2 = ex_over_u * tr;
+    if (round_fp16) s2 = __half2float(__float2half_rn(s2));
+    sigma2[p] = s2;
+    if (singular) record_status(status, p, ST_SINGULAR, 0);
+  }
+}
+
+// ===========================================================================
+// Fusion (detect.cpp:132-145,180-187): one thread per (subcarrier, user),
+// ascending cluster order.  Full fusion (C == C_total) reproduces the
+// reference's weights; partial fusion (C < C_total, multi-GPU) emits
+// sum_c w_c x_c with uniform w = 1/C_total, or sum_c x_c / sigma_c^2 plus the
+// weight sum for the optimal cross-GPU normalisation.
+// ===========================================================================
+template <typename T>
+__global__ void fuse_kernel(const T* __restrict__ XL, const float* __restrict__ sigma2, int S, int C, int C_total, int U,
+                            bool optimal, float2* __restrict__ xhat, float* __restrict__ wsum,
+                            unsigned long long* __restrict__ status) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long long>(S) * U) return;
+  const long long s = idx / U;
+  const int u = static_cast<int>(idx - s * U);
+  const bool full = C == C_total;
+  float2 acc = make_float2(0.f, 0.f);
+  if (!optimal) {
+    const float w = 1.f / static_cast<float>(C_total);
+    for (int c = 0; c < C; ++c) {
+      const float2 v = ldc(XL, (static_cast<size_t>(s) * C + c) * U + u);
+      acc.x = fmaf(w, v.x, acc.x);
+      acc.y = fmaf(w, v.y, acc.y);
+    }
+  } else {
+    float total = 0.f;
+    bool bad = false;
+    for (int c = 0; c < C; ++c) {
+      const float v = sigma2[s * C + c];
+      if (!(v > 0.f) || !isfinite(v)) bad = true;
+      total += 1.f / v;
+    }
+    if (bad && u == 0) record_status(status, s * C, ST_BAD_VARIANCE, 0);
+    for (int c = 0; c < C; ++c) {
+      const float w = full ? (1.f / sigma2[s * C + c]) / total : 1.f / sigma2[s * C + c];
+      const float2 v = ldc(XL, (static_cast<size_t>(s) * C + c) * U + u);
+      acc.x = fmaf(w, v.x, acc.x);
+      acc.y = fmaf(w, v.y, acc.y);
+    }
+    if (!full && wsum && u == 0) wsum[s] = total;
+  }
+  xhat[idx] = acc;
+}
+
+__global__ void fuse_finalize_kernel(float2* __restrict__ xhat, const float* __restrict__ wsum, int S, int U) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long long>(S) * U) return;
+  const float w = wsum[idx / U];
+  xhat[idx] = make_float2(xhat[idx].x / w, xhat[idx].y / w);
+}
+
+template <typename T>
+__global__ void gain_reduce_kernel(const float* __restrict__ part, const T* __restrict__ Sy, int S, int C, int U,
+                                   float* __restrict__ gain) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  float se = 0.f;
+  for (int u = 0; u < U; ++u) {
+    const float2 v = ldc(Sy, static_cast<size_t>(s) * U + u);
+    se = fmaf(v.y, v.y, fmaf(v.x, v.x, se));
+  }
+  float num = 0.f;
+  for (int c = 0; c < C; ++c) num += part[s * C + c];
+  gain[s] = se > 0.f ? num / se : 0.f;
+}
+
+template <typename T>
+__global__ void power_scale_kernel(T* __restrict__ X, int P, int n, float rho, unsigned long long* __restrict__ status) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long p = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + warp;
+  if (p >= P) return;
+  T* x = X + static_cast<size_t>(p) * n;
+  float e = 0.f;
+  for (int i = lane; i < n; i += 32) {
+    const float2 v = ldc(x, i);
+    e = fmaf(v.y, v.y, fmaf(v.x, v.x, e));
+  }
+  e = warp_sum(e);
+  if (e == 0.f) {
+    if (lane == 0) record_status(status, p, ST_ZERO_BEAMFORMER, 0);
+    return;
+  }
+  const float g = rho / __fsqrt_rn(e);
+  for (int i = lane; i < n; i += 32) {
+    const float2 v = ldc(x, i);
+    stc(x, i, make_float2(v.x * g, v.y * g));
+  }
+}
+
+__global__ void fusion_weights_kernel(const float* __restrict__ s2, int S, int C, float* __restrict__ w,
+                                      unsigned long long* __restrict__ status) {
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  float total = 0.f;
+  bool bad = false;
+  for (int c = 0; c < C; ++c) {
+    const float v = s2[s * C + c];
+    if (!(v > 0.f) || !isfinite(v)) bad = true;
+    total += 1.f / v;
+  }
+  if (bad) record_status(status, s * C, ST_BAD_VARIANCE, 0);
+  for (int c = 0; c < C; ++c) w[s * C + c] = (1.f / s2[s * C + c]) / total;
+}
+
+__global__ void round_fp16_kernel(float* __restrict__ x, long long n) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    x[i] = __half2float(__float2half_rn(x[i]));
+}
+
+// complex fp32 -> row-pair planar fp16 {re_a, re_b, im_a, im_b} and back
+__global__ void f32_to_f16_pairs_kernel(const float4* __restrict__ src, uint2* __restrict__ dst, long long npairs) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < npairs;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const float4 v = src[i];  // re_a, im_a, re_b, im_b
+    uint2 o;
+    o.x = h2_as_u32(__floats2half2_rn(v.x, v.z));
+    o.y = h2_as_u32(__floats2half2_rn(v.y, v.w));
+    dst[i] = o;
+  }
+}
+
+__global__ void f16_pairs_to_f32_kernel(const uint2* __restrict__ src, float4* __restrict__ dst, long long npairs) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < npairs;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const float2 re = __half22float2(u32_as_h2(src[i].x)), im = __half22float2(u32_as_h2(src[i].y));
+    dst[i] = make_float4(re.x, im.x, re.y, im.y);
+  }
+}
+
+__global__ void f32_to_f16_kernel(const float* __restrict__ src, __half* __restrict__ dst, long long n) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = __float2half_rn(src[i]);
+}
+
+__global__ void f16_to_f32_kernel(const __half* __restrict__ src, float* __restrict__ dst, long long n) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = __half2float(src[i]);
+}
+
+}  // namespace dcdg

@@ -60,6 +60,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// 32-bit shared loads that ptxas may not merge into a vector load: used to
+// place interleaved (re, im) data directly into planar register pairs.
+__device__ __forceinline__ float lds_f32(const void* p) {
+  float v;
+  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(const void* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)));
+  return v;
+}
+
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -88,12 +101,39 @@ __device__ __forceinline__ __half2 gsum_h2(__half2 v) {
 __device__ __forceinline__ float warp_sum(float v) { return gsum<32>(v); }
 
 // ---------------------------------------------------------------------------
+// packed fp32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2: one instruction for
+// two lanes of fp32, scalar operands broadcast, negation folded)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 ffma2(float s, float2 b, float2 c) { return __ffma2_rn(make_float2(s, s), b, c); }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fmul2(float s, float2 b) { return __fmul2_rn(make_float2(s, s), b); }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+// Build the planar register pair (a, b) once: x + (+0.0) is not an identity
+// under IEEE (it maps -0 to +0), so ptxas keeps the FADD2 result instead of
+// re-pairing the source registers with MOVs before every later use.
+__device__ __forceinline__ float2 pair(float a, float b) { return __fadd2_rn(make_float2(a, b), make_float2(0.f, 0.f)); }
+__device__ __forceinline__ float hsum(float2 a) { return a.x + a.y; }
+__device__ __forceinline__ float2 shfl_xor2(float2 v, int o) {
+  return make_float2(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
+}
+
+// ---------------------------------------------------------------------------
 // complex element access for the two storage formats
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float2 ldc(const float2* p, size_t i) { return __ldg(p + i); }
 __device__ __forceinline__ float2 ldc(const __half2* p, size_t i) { return __half22float2(__ldg(p + i)); }
 __device__ __forceinline__ void stc(float2* p, size_t i, float2 v) { p[i] = v; }
 __device__ __forceinline__ void stc(__half2* p, size_t i, float2 v) { p[i] = __floats2half2_rn(v.x, v.y); }
+
+// Element i of a B_c-vector stored in the fp16 row-pair planar layout
+// ({re_2i, re_2i+1, im_2i, im_2i+1}); fp32 vectors are plain interleaved.
+__device__ __forceinline__ float2 ldv(const float2* v, int i) { return __ldg(v + i); }
+__device__ __forceinline__ float2 ldv(const __half2* v, int i) {
+  const __half* h = reinterpret_cast<const __half*>(v) + (i >> 1) * 4 + (i & 1);
+  return make_float2(__half2float(h[0]), __half2float(h[2]));
+}
 
 __device__ __forceinline__ __half2 u32_as_h2(uint32_t u) {
   __half2 h;

@@ -1,0 +1,904 @@
+// Register-resident sub-warp CD kernels for sm_100a — the hot path.
+//
+// Mapping
+//   * G consecutive lanes own one (subcarrier, cluster) problem; a warp holds
+//     NPW = 32/G problems.  Lane k of a group owns R = B_c/G antenna rows, as
+//     16-byte row chunks q*G + k, so each 16-B load of a group is contiguous
+//     (coalesced HBM bursts, conflict-free 128-B shared-memory phases).
+//   * The B_c x U channel tile stays in registers for all K sweeps (128 regs
+//     per lane at the target shape); the residual r (uplink) / beamformer x
+//     (downlink) rows stay in registers too.  Per-coordinate scalars
+//     (m_j, n_j, x_j, s_j, pair Gram) live in a small shared-memory block per
+//     problem, read with group-broadcast loads off the critical path.
+//   * Tiles are staged HBM -> shared memory by cp.async.bulk (TMA 1-D, SASS
+//     UBLKCP) per warp and set of NPW problems, completing on a per-warp
+//     mbarrier.  The next set's copy is issued as soon as the current set is
+//     in registers, so the HBM stream overlaps the whole sweep computation.
+//     Warps are persistent (grid = SMs x occupancy).
+//
+// Coordinate pairs (latency)
+//   Alg. 1 / Alg. 2 update one coordinate at a time, and every update needs a
+//   group-wide reduction of a B_c-long dot product (log2(G) shuffle rounds) —
+//   the latency that bounds a naive mapping.  Here coordinates are processed
+//   in the reference's order but two at a time: both dot products of the
+//   pair (j, j+1) are taken against the same residual and reduced in ONE
+//   shuffle round; the second is then corrected exactly with the pair Gram
+//   entry computed once per problem:
+//       h_{j+1}^H (r - dx_j h_j) = h_{j+1}^H r - dx_j (h_{j+1}^H h_j).
+//   The iterates are those of the reference (same sweep order, same updates
+//   in exact arithmetic); only fp rounding differs.
+//
+// Reference algorithms (paths relative to /root/reference/proj):
+//   uplink   Alg. 1 = cd_detect               src/detect.cpp:67-110
+//   downlink Alg. 2 = cd_precode + power_scale src/precode.cpp:52-111
+//            + the cluster's effective-gain share, assemble_blocks src/precode.cpp:115-132
+#pragma once
+
+#include "dcdg_device.cuh"
+
+namespace dcdg {
+
+template <int TILE_B, int VEC_B, int NPW>
+struct Slot {
+  static constexpr int kBytes = NPW * (TILE_B + VEC_B);
+};
+
+// Issue the bulk copies of set `set` (problems [set*NPW, set*NPW + n)).
+// Uplink: per-problem vectors y.  Downlink: the symbol vectors of the
+// subcarriers the set touches (problem p belongs to subcarrier p / C).
+__device__ __forceinline__ void issue_set(unsigned char* slot, uint64_t* bar, const void* H, const void* V, int set,
+                                          int P, int npw, int tile_b, int vec_b, bool vec_per_problem, int C,
+                                          uint64_t pol) {
+  const int p0 = set * npw;
+  const int n = min(npw, P - p0);
+  int v0, nv;
+  if (vec_per_problem) {
+    v0 = p0;
+    nv = n;
+  } else {
+    v0 = p0 / C;
+    nv = (p0 + n - 1) / C - v0 + 1;
+  }
+  mbar_arrive_expect_tx(bar, static_cast<uint32_t>(n * tile_b + nv * vec_b));
+  bulk_g2s(slot, static_cast<const unsigned char*>(H) + static_cast<size_t>(p0) * tile_b, n * tile_b, bar, pol);
+  bulk_g2s(slot + npw * tile_b, static_cast<const unsigned char*>(V) + static_cast<size_t>(v0) * vec_b, nv * vec_b,
+           bar, pol);
+}
+
+// Reduce-scatter NV per-lane partials over the G lanes of a group with xor
+// butterflies: afterwards lane k holds the full sums of values
+// [k*NV/G, (k+1)*NV/G) in v[0 .. NV/G).  log2(G) rounds, NV-NV/G shuffles.
+template <int O, int N, int NV>
+struct ReduceScatter {
+  static __device__ __forceinline__ void run(float (&v)[NV], int k) {
+    const bool hi = (k & O) != 0;
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      const float a = v[i], b = v[i + N / 2];
+      const float send = hi ? a : b;
+      const float keep = hi ? b : a;
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+    }
+    ReduceScatter<O / 2, N / 2, NV>::run(v, k);
+  }
+};
+template <int N, int NV>
+struct ReduceScatter<0, N, NV> {
+  static __device__ __forceinline__ void run(float (&)[NV], int) {}
+};
+
+template <int G, int NV>
+__device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int k) {
+  static_assert(NV % G == 0, "values must split evenly over the group");
+  ReduceScatter<G / 2, NV, NV>::run(v, k);
+}
+
+// Per-problem scalar blocks (bytes); +16 skews consecutive groups' blocks
+// across shared-memory banks.  Used by the kernels and their launchers.
+__host__ __device__ constexpr int ul_scal_bytes(int U) { return U * 24 + 16; }
+__host__ __device__ constexpr int dl_scal_bytes(int U) { return U * 32 + 16; }
+
+// Shared-memory layout of one CTA: [W staging slots][W*NPW scalar blocks][W mbarriers]
+template <int SLOT_B, int SCAL_B, int NPW, int W>
+struct CtaSmem {
+  static constexpr int kScalOff = W * SLOT_B;
+  static constexpr int kBarOff = kScalOff + W * NPW * SCAL_B;
+  static constexpr int kBytes = kBarOff + W * 8;
+};
+
+// ===========================================================================
+// Uplink, fp32 storage and arithmetic, on packed row PAIRS: every lane keeps
+// its rows as float2 (row 2c, row 2c+1) planes of re and im, so each complex
+// MAC over two rows is 2 FFMA2 (sm_100 packed fp32x2) and the rank-1
+// coefficient dx is a broadcast operand.
+// Scalar block per problem: float4 mnx[U] = (m_j, n_j, Re x_j, Im x_j) and
+// float4 gp[U/2] = (Re G, Im G, -Im G, Re G) with G = h_{2i+1}^H h_{2i}.
+// ===========================================================================
+template <int BC, int U, int G, int W, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB)
+    ul_reg_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
+               float2* __restrict__ X) {
+  static_assert(32 % G == 0 && BC % (2 * G) == 0 && U % 2 == 0 && (2 * U) % G == 0, "shape");
+  constexpr int NPW = 32 / G, R = BC / G, NP = R / 2;
+  constexpr int TILE_B = BC * U * 8, Y_B = BC * 8, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
+  constexpr int SCAL_B = ul_scal_bytes(U);
+  using L = CtaSmem<SLOT_B, SCAL_B, NPW, W>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / G, k = lane % G;
+  unsigned char* slot = smem + warp * SLOT_B;
+  float4* mnx = reinterpret_cast<float4*>(smem + L::kScalOff + (warp * NPW + g) * SCAL_B);
+  float4* gp = mnx + U;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff) + warp;
+  const int nsets = (P + NPW - 1) / NPW;
+  const int nw = gridDim.x * W;
+  int set = blockIdx.x * W + warp;
+  const uint64_t pol = l2_evict_first_policy();
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (lane == 0 && set < nsets) issue_set(slot, bar, H, Y, set, P, NPW, TILE_B, Y_B, true, 1, pol);
+  uint32_t phase = 0;
+  const float2 z2 = make_float2(0.f, 0.f);
+  for (; set < nsets; set += nw) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    float2 hr[U][NP], hi[U][NP], rr[NP], ri[NP];
+    {
+      // one 16-B load per row pair, re-paired once into planar registers
+      const float4* t4 = reinterpret_cast<const float4*>(slot + g * TILE_B);
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          const float4 v = t4[j * (BC / 2) + c * G + k];
+          hr[j][c] = pair(v.x, v.z);
+          hi[j][c] = pair(v.y, v.w);
+        }
+      const float4* y4 = reinterpret_cast<const float4*>(slot + NPW * TILE_B + g * Y_B);
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        const float4 v = y4[c * G + k];
+        rr[c] = pair(v.x, v.z);
+        ri[c] = pair(v.y, v.w);
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
+
+    // ---- per-problem scalars: ||h_j||^2 (detect.cpp:86-90) and pair Grams
+    {
+      float v[2 * U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        float2 e = fmul2(hr[j][0], hr[j][0]);
+        e = ffma2(hi[j][0], hi[j][0], e);
+#pragma unroll
+        for (int c = 1; c < NP; ++c) e = ffma2(hi[j][c], hi[j][c], ffma2(hr[j][c], hr[j][c], e));
+        v[j] = hsum(e);
+      }
+#pragma unroll
+      for (int i = 0; i < U / 2; ++i) {  // G = h_{2i+1}^H h_{2i}
+        float2 gr = z2, gi = z2;
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          gr = ffma2(hi[2 * i + 1][c], hi[2 * i][c], ffma2(hr[2 * i + 1][c], hr[2 * i][c], gr));
+          gi = ffma2(neg2(hi[2 * i + 1][c]), hr[2 * i][c], ffma2(hr[2 * i + 1][c], hi[2 * i][c], gi));
+        }
+        v[U + 2 * i] = hsum(gr);
+        v[U + 2 * i + 1] = hsum(gi);
+      }
+      group_reduce_scatter<G>(v, k);
+      constexpr int PER = 2 * U / G;
+      float* gf = reinterpret_cast<float*>(gp);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int idx = k * PER + i;
+        if (idx < U) {
+          const float m = __fdividef(1.f, v[i] + kappa);  // m_j = 1/(||h_j||^2 + N0/Ex)
+          mnx[idx] = make_float4(m, m * v[i], 0.f, 0.f);  // n_j = m_j ||h_j||^2, x_j = 0
+        } else {
+          const int gi = idx - U, pr = gi >> 1;
+          if (gi & 1) {
+            gf[pr * 4 + 1] = v[i];
+            gf[pr * 4 + 2] = -v[i];
+          } else {
+            gf[pr * 4 + 0] = v[i];
+            gf[pr * 4 + 3] = v[i];
+          }
+        }
+      }
+    }
+    __syncwarp();
+
+    // ---- K sweeps over the users in ascending order, two coordinates per round
+    for (int t = 0; t < K; ++t) {
+#pragma unroll
+      for (int jp = 0; jp < U / 2; ++jp) {
+        const int j0 = 2 * jp, j1 = 2 * jp + 1;
+        const float4 A0 = mnx[j0], A1 = mnx[j1], GG = gp[jp];
+        // h_j^H r for both coordinates (cdotc, detect.cpp:100), on row pairs
+        float2 a0 = z2, c0 = z2, a1 = z2, c1 = z2;
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          a0 = ffma2(hi[j0][c], ri[c], ffma2(hr[j0][c], rr[c], a0));
+          c0 = ffma2(neg2(hi[j0][c]), rr[c], ffma2(hr[j0][c], ri[c], c0));
+          a1 = ffma2(hi[j1][c], ri[c], ffma2(hr[j1][c], rr[c], a1));
+          c1 = ffma2(neg2(hi[j1][c]), rr[c], ffma2(hr[j1][c], ri[c], c1));
+        }
+        float2 d0 = make_float2(hsum(a0), hsum(c0));
+        float2 d1 = make_float2(hsum(a1), hsum(c1));
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+          d0 = fadd2(d0, shfl_xor2(d0, o));
+          d1 = fadd2(d1, shfl_xor2(d1, o));
+        }
+        // x_j' = m_j h_j^H r + n_j x_j ; dx = x_j' - x_j   (detect.cpp:100-103)
+        const float2 x0 = make_float2(A0.z, A0.w), x1 = make_float2(A1.z, A1.w);
+        const float2 n0 = ffma2(A0.x, d0, fmul2(A0.y, x0));
+        const float2 dx0 = fadd2(n0, neg2(x0));
+        // h_{j+1}^H (r - dx_j h_j) = h_{j+1}^H r - dx_j G
+        d1 = ffma2(-dx0.x, make_float2(GG.x, GG.y), d1);
+        d1 = ffma2(-dx0.y, make_float2(GG.z, GG.w), d1);
+        const float2 n1 = ffma2(A1.x, d1, fmul2(A1.y, x1));
+        const float2 dx1 = fadd2(n1, neg2(x1));
+        // every lane of the group stores the same value
+        *reinterpret_cast<float2*>(&mnx[j0].z) = n0;
+        *reinterpret_cast<float2*>(&mnx[j1].z) = n1;
+        // r -= dx_j h_j ; r -= dx_{j+1} h_{j+1}   (caxpy, detect.cpp:104)
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          rr[c] = ffma2(dx0.y, hi[j0][c], ffma2(-dx0.x, hr[j0][c], rr[c]));
+          ri[c] = ffma2(-dx0.y, hr[j0][c], ffma2(-dx0.x, hi[j0][c], ri[c]));
+          rr[c] = ffma2(dx1.y, hi[j1][c], ffma2(-dx1.x, hr[j1][c], rr[c]));
+          ri[c] = ffma2(-dx1.y, hr[j1][c], ffma2(-dx1.x, hi[j1][c], ri[c]));
+        }
+      }
+    }
+    __syncwarp();
+    const int p = set * NPW + g;
+    if (p < P) {
+      float4* xo = reinterpret_cast<float4*>(X + static_cast<size_t>(p) * U);
+#pragma unroll
+      for (int i = k; i < U / 2; i += G) {
+        const float4 u0 = mnx[2 * i], u1 = mnx[2 * i + 1];
+        xo[i] = make_float4(u0.z, u0.w, u1.z, u1.w);
+      }
+    }
+    __syncwarp();
+  }
+}
+// ===========================================================================
+// Uplink, fp16 storage + half2 arithmetic (the paper's half-precision path).
+// The fp16 channel tile and receive vector are stored row-pair planar
+// ({re_2i, re_2i+1, im_2i, im_2i+1} per 8 bytes, see include/dcdg.h), so each
+// lane loads its rows directly as planar half2 PAIRS (re_i, re_i+1), (im_i, im_i+1),
+// so a complex MAC over two rows is 2 HFMA2 (4 FFMA per row in fp32).  Dot
+// products accumulate in half2 and are reduced as one packed (re, im) half2
+// per shuffle; the per-coordinate scalar update runs in fp32.
+// ===========================================================================
+template <int BC, int U, int G, int W, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB)
+    ul_reg_f16(const __half2* __restrict__ H, const __half2* __restrict__ Y, int P, int K, float kappa,
+               __half2* __restrict__ X) {
+  static_assert(32 % G == 0 && BC % (4 * G) == 0 && U % 4 == 0 && (2 * U) % G == 0, "shape");
+  constexpr int NPW = 32 / G, R = BC / G, CH = R / 4, NP = R / 2;
+  constexpr int TILE_B = BC * U * 4, Y_B = BC * 4, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
+  constexpr int SCAL_B = ul_scal_bytes(U);
+  using L = CtaSmem<SLOT_B, SCAL_B, NPW, W>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / G, k = lane % G;
+  unsigned char* slot = smem + warp * SLOT_B;
+  float4* mng = reinterpret_cast<float4*>(smem + L::kScalOff + (warp * NPW + g) * SCAL_B);
+  float2* xs = reinterpret_cast<float2*>(mng + U);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff) + warp;
+  const int nsets = (P + NPW - 1) / NPW;
+  const int nw = gridDim.x * W;
+  int set = blockIdx.x * W + warp;
+  const uint64_t pol = l2_evict_first_policy();
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (lane == 0 && set < nsets) issue_set(slot, bar, H, Y, set, P, NPW, TILE_B, Y_B, true, 1, pol);
+  uint32_t phase = 0;
+  const __half2 z2 = __float2half2_rn(0.f);
+  for (; set < nsets; set += nw) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    __half2 hre[U][NP], him[U][NP], rre[NP], rim[NP];
+    {
+      // fp16 tiles are row-pair planar: {re_2i, re_2i+1, im_2i, im_2i+1}
+      const uint4* t4 = reinterpret_cast<const uint4*>(slot + g * TILE_B);
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const uint4 v = t4[j * (BC / 4) + c * G + k];
+          hre[j][2 * c] = u32_as_h2(v.x);
+          him[j][2 * c] = u32_as_h2(v.y);
+          hre[j][2 * c + 1] = u32_as_h2(v.z);
+          him[j][2 * c + 1] = u32_as_h2(v.w);
+        }
+      const uint4* y4 = reinterpret_cast<const uint4*>(slot + NPW * TILE_B + g * Y_B);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const uint4 v = y4[c * G + k];
+        rre[2 * c] = u32_as_h2(v.x);
+        rim[2 * c] = u32_as_h2(v.y);
+        rre[2 * c + 1] = u32_as_h2(v.z);
+        rim[2 * c + 1] = u32_as_h2(v.w);
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
+
+    {
+      float v[2 * U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        __half2 acc = __hmul2(hre[j][0], hre[j][0]);
+        acc = __hfma2(him[j][0], him[j][0], acc);
+#pragma unroll
+        for (int q = 1; q < NP; ++q) {
+          acc = __hfma2(hre[j][q], hre[j][q], acc);
+          acc = __hfma2(him[j][q], him[j][q], acc);
+        }
+        const float2 f = __half22float2(acc);
+        v[j] = f.x + f.y;
+      }
+#pragma unroll
+      for (int i = 0; i < U / 2; ++i) {
+        __half2 gr = z2, gi = z2;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          gr = __hfma2(hre[2 * i + 1][q], hre[2 * i][q], __hfma2(him[2 * i + 1][q], him[2 * i][q], gr));
+          gi = __hfma2(hre[2 * i + 1][q], him[2 * i][q], __hfma2(__hneg2(him[2 * i + 1][q]), hre[2 * i][q], gi));
+        }
+        const float2 fr = __half22float2(gr), fi = __half22float2(gi);
+        v[U + 2 * i] = fr.x + fr.y;
+        v[U + 2 * i + 1] = fi.x + fi.y;
+      }
+      group_reduce_scatter<G>(v, k);
+      constexpr int PER = 2 * U / G;
+      float* mf = reinterpret_cast<float*>(mng);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int idx = k * PER + i;
+        if (idx < U) {
+          const float m = __fdividef(1.f, v[i] + kappa);
+          mf[idx * 4] = m;
+          mf[idx * 4 + 1] = m * v[i];
+          xs[idx] = make_float2(0.f, 0.f);
+        } else {
+          const int gi = idx - U;
+          mf[((gi >> 1) * 2 + 1) * 4 + 2 + (gi & 1)] = v[i];
+        }
+      }
+    }
+    __syncwarp();
+
+    for (int t = 0; t < K; ++t) {
+#pragma unroll
+      for (int jp = 0; jp < U / 2; ++jp) {
+        const int j0 = 2 * jp, j1 = 2 * jp + 1;
+        const float4 s0 = mng[j0], s1 = mng[j1];
+        const float2 x0 = xs[j0], x1 = xs[j1];
+        __half2 a0 = z2, a1 = z2, b0 = z2, b1 = z2, c0 = z2, c1 = z2, e0 = z2, e1 = z2;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          a0 = __hfma2(hre[j0][q], rre[q], a0);
+          a1 = __hfma2(him[j0][q], rim[q], a1);
+          b0 = __hfma2(hre[j0][q], rim[q], b0);
+          b1 = __hfma2(him[j0][q], rre[q], b1);
+          c0 = __hfma2(hre[j1][q], rre[q], c0);
+          c1 = __hfma2(him[j1][q], rim[q], c1);
+          e0 = __hfma2(hre[j1][q], rim[q], e0);
+          e1 = __hfma2(him[j1][q], rre[q], e1);
+        }
+        const __half2 re0 = __hadd2(a0, a1), im0 = __hsub2(b0, b1);
+        const __half2 re1 = __hadd2(c0, c1), im1 = __hsub2(e0, e1);
+        __half2 d0 = __hadd2(__lows2half2(re0, im0), __highs2half2(re0, im0));
+        __half2 d1 = __hadd2(__lows2half2(re1, im1), __highs2half2(re1, im1));
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+          d0 = __hadd2(d0, __shfl_xor_sync(0xffffffffu, d0, o));
+          d1 = __hadd2(d1, __shfl_xor_sync(0xffffffffu, d1, o));
+        }
+        const float2 f0 = __half22float2(d0);
+        float2 f1 = __half22float2(d1);
+        const float n0r = fmaf(s0.x, f0.x, s0.y * x0.x), n0i = fmaf(s0.x, f0.y, s0.y * x0.y);
+        const float dx0r = n0r - x0.x, dx0i = n0i - x0.y;
+        f1.x = fmaf(-dx0r, s1.z, fmaf(dx0i, s1.w, f1.x));
+        f1.y = fmaf(-dx0r, s1.w, fmaf(-dx0i, s1.z, f1.y));
+        const float n1r = fmaf(s1.x, f1.x, s1.y * x1.x), n1i = fmaf(s1.x, f1.y, s1.y * x1.y);
+        const float dx1r = n1r - x1.x, dx1i = n1i - x1.y;
+        xs[j0] = make_float2(n0r, n0i);
+        xs[j1] = make_float2(n1r, n1i);
+        const __half2 ndr0 = __float2half2_rn(-dx0r), pdi0 = __float2half2_rn(dx0i), ndi0 = __float2half2_rn(-dx0i);
+        const __half2 ndr1 = __float2half2_rn(-dx1r), pdi1 = __float2half2_rn(dx1i), ndi1 = __float2half2_rn(-dx1i);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          rre[q] = __hfma2(ndr0, hre[j0][q], __hfma2(pdi0, him[j0][q], rre[q]));
+          rim[q] = __hfma2(ndr0, him[j0][q], __hfma2(ndi0, hre[j0][q], rim[q]));
+          rre[q] = __hfma2(ndr1, hre[j1][q], __hfma2(pdi1, him[j1][q], rre[q]));
+          rim[q] = __hfma2(ndr1, him[j1][q], __hfma2(ndi1, hre[j1][q], rim[q]));
+        }
+      }
+    }
+    __syncwarp();
+    const int p = set * NPW + g;
+    if (p < P) {
+      uint4* xo = reinterpret_cast<uint4*>(X + static_cast<size_t>(p) * U);
+#pragma unroll
+      for (int i = k; i < U / 4; i += G) {
+        uint4 w;
+        w.x = h2_as_u32(__floats2half2_rn(xs[4 * i].x, xs[4 * i].y));
+        w.y = h2_as_u32(__floats2half2_rn(xs[4 * i + 1].x, xs[4 * i + 1].y));
+        w.z = h2_as_u32(__floats2half2_rn(xs[4 * i + 2].x, xs[4 * i + 2].y));
+        w.w = h2_as_u32(__floats2half2_rn(xs[4 * i + 3].x, xs[4 * i + 3].y));
+        xo[i] = w;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ===========================================================================
+// Downlink, fp32, packed row pairs (see ul_reg_f32).  The dual rows h_u are
+// the uplink columns (conj_rows, precode.cpp:19-27), normalised in registers
+// (p_u = 1/||h_u||, precode.cpp:69-87).  Scalar block per problem:
+// float4 ss[U] = (Re s~_u, Im s~_u, p_u, -), s~_u = p_u s_u;
+// float4 gp[U/2] = (Re G~, Im G~, -Im G~, Re G~), G~ = h~_{2i+1}^H h~_{2i};
+// float2 sraw[U] (the received symbols).
+// ===========================================================================
+template <int BC, int U, int G, int W, int MINB, bool GAIN>
+__global__ void __launch_bounds__(32 * W, MINB)
+    dl_reg_f32(const float2* __restrict__ H, const float2* __restrict__ Sy, int P, int C, int K, float rho_c,
+               float2* __restrict__ X, float* __restrict__ gain_part, unsigned long long* __restrict__ status) {
+  static_assert(32 % G == 0 && BC % (2 * G) == 0 && U % 2 == 0 && (2 * U) % G == 0, "shape");
+  constexpr int NPW = 32 / G, R = BC / G, NP = R / 2;
+  constexpr int TILE_B = BC * U * 8, S_B = U * 8, SLOT_B = Slot<TILE_B, S_B, NPW>::kBytes;
+  constexpr int SCAL_B = dl_scal_bytes(U);
+  using L = CtaSmem<SLOT_B, SCAL_B, NPW, W>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / G, k = lane % G;
+  unsigned char* slot = smem + warp * SLOT_B;
+  float4* ss = reinterpret_cast<float4*>(smem + L::kScalOff + (warp * NPW + g) * SCAL_B);
+  float4* gp = ss + U;
+  float2* sraw = reinterpret_cast<float2*>(gp + U / 2);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff) + warp;
+  const int nsets = (P + NPW - 1) / NPW;
+  const int nw = gridDim.x * W;
+  int set = blockIdx.x * W + warp;
+  const uint64_t pol = l2_evict_first_policy();
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (lane == 0 && set < nsets) issue_set(slot, bar, H, Sy, set, P, NPW, TILE_B, S_B, false, C, pol);
+  uint32_t phase = 0;
+  const float2 z2 = make_float2(0.f, 0.f);
+  for (; set < nsets; set += nw) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    const int p = set * NPW + g;
+    float2 hr[U][NP], hi[U][NP];
+    {
+      const float4* t4 = reinterpret_cast<const float4*>(slot + g * TILE_B);
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          const float4 v = t4[j * (BC / 2) + c * G + k];
+          hr[j][c] = pair(v.x, v.z);
+          hi[j][c] = pair(v.y, v.w);
+        }
+      const int sidx = min(p, P - 1) / C - (set * NPW) / C;
+      const float4* s4 = reinterpret_cast<const float4*>(slot + NPW * TILE_B + sidx * S_B);
+      float4* d4 = reinterpret_cast<float4*>(sraw);
+#pragma unroll
+      for (int i = k; i < U / 2; i += G) d4[i] = s4[i];
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Sy, set + nw, P, NPW, TILE_B, S_B, false, C, pol);
+
+    // ---- row norms and raw pair Grams, reduce-scattered over the group
+    constexpr int PER = 2 * U / G;
+    float vv[2 * U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      float2 e = fmul2(hr[j][0], hr[j][0]);
+      e = ffma2(hi[j][0], hi[j][0], e);
+#pragma unroll
+      for (int c = 1; c < NP; ++c) e = ffma2(hi[j][c], hi[j][c], ffma2(hr[j][c], hr[j][c], e));
+      vv[j] = hsum(e);
+    }
+#pragma unroll
+    for (int i = 0; i < U / 2; ++i) {
+      float2 gr = z2, gi = z2;
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        gr = ffma2(hi[2 * i + 1][c], hi[2 * i][c], ffma2(hr[2 * i + 1][c], hr[2 * i][c], gr));
+        gi = ffma2(neg2(hi[2 * i + 1][c]), hr[2 * i][c], ffma2(hr[2 * i + 1][c], hi[2 * i][c], gi));
+      }
+      vv[U + 2 * i] = hsum(gr);
+      vv[U + 2 * i + 1] = hsum(gi);
+    }
+    group_reduce_scatter<G>(vv, k);
+    int zero_user = -1;
+    float* sf = reinterpret_cast<float*>(ss);
+    float* gf = reinterpret_cast<float*>(gp);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int idx = k * PER + i;
+      if (idx < U) {
+        if (vv[i] == 0.f && zero_user < 0) zero_user = idx;
+        const float pinv = rsqrtf(vv[i]);
+        sf[idx * 4 + 2] = pinv;  // p_u = 1/||h_u||
+        sf[idx * 4 + 3] = vv[i] * pinv;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int idx = k * PER + i;
+      if (idx < U) {
+        const float2 s = sraw[idx];
+        const float pj = sf[idx * 4 + 2];
+        sf[idx * 4] = s.x * pj;  // s~_u = p_u s_u
+        sf[idx * 4 + 1] = s.y * pj;
+      } else {
+        const int gi = idx - U, pr = gi >> 1;
+        const float val = vv[i] * (sf[(2 * pr + 1) * 4 + 2] * sf[(2 * pr) * 4 + 2]);  // G~ = p_a p_b G
+        if (gi & 1) {
+          gf[pr * 4 + 1] = val;
+          gf[pr * 4 + 2] = -val;
+        } else {
+          gf[pr * 4 + 0] = val;
+          gf[pr * 4 + 3] = val;
+        }
+      }
+    }
+    // normalise the rows held in registers
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const float pj = sf[j * 4 + 2];
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        hr[j][c] = fmul2(pj, hr[j][c]);
+        hi[j][c] = fmul2(pj, hi[j][c]);
+      }
+    }
+    __syncwarp();
+
+    float2 xr[NP], xi[NP];
+#pragma unroll
+    for (int c = 0; c < NP; ++c) xr[c] = xi[c] = z2;
+    for (int t = 0; t < K; ++t) {
+#pragma unroll
+      for (int jp = 0; jp < U / 2; ++jp) {
+        const int j0 = 2 * jp, j1 = 2 * jp + 1;
+        const float4 S0 = ss[j0], S1 = ss[j1], GG = gp[jp];
+        float2 a0 = z2, c0 = z2, a1 = z2, c1 = z2;
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          a0 = ffma2(hi[j0][c], xi[c], ffma2(hr[j0][c], xr[c], a0));
+          c0 = ffma2(neg2(hi[j0][c]), xr[c], ffma2(hr[j0][c], xi[c], c0));
+          a1 = ffma2(hi[j1][c], xi[c], ffma2(hr[j1][c], xr[c], a1));
+          c1 = ffma2(neg2(hi[j1][c]), xr[c], ffma2(hr[j1][c], xi[c], c1));
+        }
+        float2 d0 = make_float2(hsum(a0), hsum(c0));
+        float2 d1 = make_float2(hsum(a1), hsum(c1));
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+          d0 = fadd2(d0, shfl_xor2(d0, o));
+          d1 = fadd2(d1, shfl_xor2(d1, o));
+        }
+        // resid_u = h~_u^H x - s~_u ; x -= resid_u h~_u   (precode.cpp:89-94)
+        const float2 r0 = fadd2(d0, make_float2(-S0.x, -S0.y));
+        d1 = ffma2(-r0.x, make_float2(GG.x, GG.y), d1);
+        d1 = ffma2(-r0.y, make_float2(GG.z, GG.w), d1);
+        const float2 r1 = fadd2(d1, make_float2(-S1.x, -S1.y));
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          xr[c] = ffma2(r0.y, hi[j0][c], ffma2(-r0.x, hr[j0][c], xr[c]));
+          xi[c] = ffma2(-r0.y, hr[j0][c], ffma2(-r0.x, hi[j0][c], xi[c]));
+          xr[c] = ffma2(r1.y, hi[j1][c], ffma2(-r1.x, hr[j1][c], xr[c]));
+          xi[c] = ffma2(-r1.y, hr[j1][c], ffma2(-r1.x, hi[j1][c], xi[c]));
+        }
+      }
+    }
+    // power_scale to rho_c = rho / sqrt(C)   (precode.cpp:101-111,155); rho_c == 0: raw beamformer
+    float2 e2 = fmul2(xr[0], xr[0]);
+    e2 = ffma2(xi[0], xi[0], e2);
+#pragma unroll
+    for (int c = 1; c < NP; ++c) e2 = ffma2(xi[c], xi[c], ffma2(xr[c], xr[c], e2));
+    const float e = gsum<G>(hsum(e2));
+    const float gsc = rho_c > 0.f ? rho_c / __fsqrt_rn(e) : 1.f;
+#pragma unroll
+    for (int c = 0; c < NP; ++c) {
+      xr[c] = fmul2(gsc, xr[c]);
+      xi[c] = fmul2(gsc, xi[c]);
+    }
+    // gain share Re(s^H H_dl,c x_c) = Re(v^H x_c), v = H_c s = sum_u (s_u ||h_u||) h~_u
+    float gq = 0.f;
+    if (GAIN) {
+      float2 vr[NP], vi[NP];
+#pragma unroll
+      for (int c = 0; c < NP; ++c) vr[c] = vi[c] = z2;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const float2 sj = sraw[j];
+        const float nj = ss[j].w;
+        const float cr = sj.x * nj, ci = sj.y * nj;
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          vr[c] = ffma2(-ci, hi[j][c], ffma2(cr, hr[j][c], vr[c]));
+          vi[c] = ffma2(ci, hr[j][c], ffma2(cr, hi[j][c], vi[c]));
+        }
+      }
+      float2 q2 = fmul2(vr[0], xr[0]);
+      q2 = ffma2(vi[0], xi[0], q2);
+#pragma unroll
+      for (int c = 1; c < NP; ++c) q2 = ffma2(vi[c], xi[c], ffma2(vr[c], xr[c], q2));
+      gq = gsum<G>(hsum(q2));
+    }
+    if (p < P) {
+      if (zero_user >= 0) record_status(status, p, ST_ZERO_ROW, zero_user);
+      if (k == 0) {
+        if (e == 0.f && rho_c > 0.f) record_status(status, p, ST_ZERO_BEAMFORMER, 0);
+        if (GAIN) gain_part[p] = gq;
+      }
+      float4* x4 = reinterpret_cast<float4*>(X + static_cast<size_t>(p) * BC);
+#pragma unroll
+      for (int c = 0; c < NP; ++c) x4[c * G + k] = make_float4(xr[c].x, xi[c].x, xr[c].y, xi[c].y);
+    }
+    __syncwarp();
+  }
+}
+// ===========================================================================
+// Downlink, fp16 storage + half2 arithmetic.
+// ===========================================================================
+template <int BC, int U, int G, int W, int MINB, bool GAIN>
+__global__ void __launch_bounds__(32 * W, MINB)
+    dl_reg_f16(const __half2* __restrict__ H, const __half2* __restrict__ Sy, int P, int C, int K, float rho_c,
+               __half2* __restrict__ X, float* __restrict__ gain_part, unsigned long long* __restrict__ status) {
+  static_assert(32 % G == 0 && BC % (4 * G) == 0 && U % 4 == 0 && (2 * U) % G == 0, "shape");
+  constexpr int NPW = 32 / G, R = BC / G, CH = R / 4, NP = R / 2;
+  constexpr int TILE_B = BC * U * 4, S_B = U * 4, SLOT_B = Slot<TILE_B, S_B, NPW>::kBytes;
+  constexpr int SCAL_B = dl_scal_bytes(U);
+  using L = CtaSmem<SLOT_B, SCAL_B, NPW, W>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / G, k = lane % G;
+  unsigned char* slot = smem + warp * SLOT_B;
+  float4* sg = reinterpret_cast<float4*>(smem + L::kScalOff + (warp * NPW + g) * SCAL_B);
+  float2* sraw = reinterpret_cast<float2*>(sg + U);
+  float* pn = reinterpret_cast<float*>(sraw + U);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff) + warp;
+  const int nsets = (P + NPW - 1) / NPW;
+  const int nw = gridDim.x * W;
+  int set = blockIdx.x * W + warp;
+  const uint64_t pol = l2_evict_first_policy();
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (lane == 0 && set < nsets) issue_set(slot, bar, H, Sy, set, P, NPW, TILE_B, S_B, false, C, pol);
+  uint32_t phase = 0;
+  const __half2 z2 = __float2half2_rn(0.f);
+  for (; set < nsets; set += nw) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    const int p = set * NPW + g;
+    __half2 hre[U][NP], him[U][NP];
+    {
+      // fp16 tiles are row-pair planar: {re_2i, re_2i+1, im_2i, im_2i+1}
+      const uint4* t4 = reinterpret_cast<const uint4*>(slot + g * TILE_B);
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const uint4 v = t4[j * (BC / 4) + c * G + k];
+          hre[j][2 * c] = u32_as_h2(v.x);
+          him[j][2 * c] = u32_as_h2(v.y);
+          hre[j][2 * c + 1] = u32_as_h2(v.z);
+          him[j][2 * c + 1] = u32_as_h2(v.w);
+        }
+      const int sidx = min(p, P - 1) / C - (set * NPW) / C;
+      const __half2* s2 = reinterpret_cast<const __half2*>(slot + NPW * TILE_B + sidx * S_B);
+#pragma unroll
+      for (int i = k; i < U; i += G) sraw[i] = __half22float2(s2[i]);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Sy, set + nw, P, NPW, TILE_B, S_B, false, C, pol);
+
+    __half2 vre[NP], vim[NP];
+    if (GAIN) {
+#pragma unroll
+      for (int q = 0; q < NP; ++q) vre[q] = vim[q] = z2;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const float2 sj = sraw[j];
+        const __half2 s_r = __float2half2_rn(sj.x), s_i = __float2half2_rn(sj.y), n_i = __float2half2_rn(-sj.y);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          vre[q] = __hfma2(s_r, hre[j][q], __hfma2(n_i, him[j][q], vre[q]));
+          vim[q] = __hfma2(s_r, him[j][q], __hfma2(s_i, hre[j][q], vim[q]));
+        }
+      }
+    }
+    constexpr int PER = 2 * U / G;
+    float vv[2 * U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      __half2 acc = __hmul2(hre[j][0], hre[j][0]);
+      acc = __hfma2(him[j][0], him[j][0], acc);
+#pragma unroll
+      for (int q = 1; q < NP; ++q) {
+        acc = __hfma2(hre[j][q], hre[j][q], acc);
+        acc = __hfma2(him[j][q], him[j][q], acc);
+      }
+      const float2 f = __half22float2(acc);
+      vv[j] = f.x + f.y;
+    }
+#pragma unroll
+    for (int i = 0; i < U / 2; ++i) {
+      __half2 gr = z2, gi = z2;
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        gr = __hfma2(hre[2 * i + 1][q], hre[2 * i][q], __hfma2(him[2 * i + 1][q], him[2 * i][q], gr));
+        gi = __hfma2(hre[2 * i + 1][q], him[2 * i][q], __hfma2(__hneg2(him[2 * i + 1][q]), hre[2 * i][q], gi));
+      }
+      const float2 fr = __half22float2(gr), fi = __half22float2(gi);
+      vv[U + 2 * i] = fr.x + fr.y;
+      vv[U + 2 * i + 1] = fi.x + fi.y;
+    }
+    group_reduce_scatter<G>(vv, k);
+    int zero_user = -1;
+    float* sgf = reinterpret_cast<float*>(sg);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int idx = k * PER + i;
+      if (idx < U) {
+        if (vv[i] == 0.f && zero_user < 0) zero_user = idx;
+        pn[idx] = rsqrtf(vv[i]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int idx = k * PER + i;
+      if (idx < U) {
+        const float2 s = sraw[idx];
+        const float pj = pn[idx];
+        sgf[idx * 4] = s.x * pj;
+        sgf[idx * 4 + 1] = s.y * pj;
+      } else {
+        const int gi = idx - U;
+        const int a = (gi >> 1) * 2 + 1;
+        sgf[a * 4 + 2 + (gi & 1)] = vv[i] * (pn[a] * pn[a - 1]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const __half2 p2 = __float2half2_rn(pn[j]);
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        hre[j][q] = __hmul2(p2, hre[j][q]);
+        him[j][q] = __hmul2(p2, him[j][q]);
+      }
+    }
+    __syncwarp();
+
+    __half2 xre[NP], xim[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) xre[q] = xim[q] = z2;
+    for (int t = 0; t < K; ++t) {
+#pragma unroll
+      for (int jp = 0; jp < U / 2; ++jp) {
+        const int j0 = 2 * jp, j1 = 2 * jp + 1;
+        const float4 s0 = sg[j0], s1 = sg[j1];
+        __half2 a0 = z2, a1 = z2, b0 = z2, b1 = z2, c0 = z2, c1 = z2, e0 = z2, e1 = z2;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          a0 = __hfma2(hre[j0][q], xre[q], a0);
+          a1 = __hfma2(him[j0][q], xim[q], a1);
+          b0 = __hfma2(hre[j0][q], xim[q], b0);
+          b1 = __hfma2(him[j0][q], xre[q], b1);
+          c0 = __hfma2(hre[j1][q], xre[q], c0);
+          c1 = __hfma2(him[j1][q], xim[q], c1);
+          e0 = __hfma2(hre[j1][q], xim[q], e0);
+          e1 = __hfma2(him[j1][q], xre[q], e1);
+        }
+        const __half2 re0 = __hadd2(a0, a1), im0 = __hsub2(b0, b1);
+        const __half2 re1 = __hadd2(c0, c1), im1 = __hsub2(e0, e1);
+        __half2 d0 = __hadd2(__lows2half2(re0, im0), __highs2half2(re0, im0));
+        __half2 d1 = __hadd2(__lows2half2(re1, im1), __highs2half2(re1, im1));
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+          d0 = __hadd2(d0, __shfl_xor_sync(0xffffffffu, d0, o));
+          d1 = __hadd2(d1, __shfl_xor_sync(0xffffffffu, d1, o));
+        }
+        const float2 f0 = __half22float2(d0);
+        float2 f1 = __half22float2(d1);
+        const float r0r = f0.x - s0.x, r0i = f0.y - s0.y;
+        f1.x = fmaf(-r0r, s1.z, fmaf(r0i, s1.w, f1.x));
+        f1.y = fmaf(-r0r, s1.w, fmaf(-r0i, s1.z, f1.y));
+        const float r1r = f1.x - s1.x, r1i = f1.y - s1.y;
+        const __half2 ndr0 = __float2half2_rn(-r0r), pdi0 = __float2half2_rn(r0i), ndi0 = __float2half2_rn(-r0i);
+        const __half2 ndr1 = __float2half2_rn(-r1r), pdi1 = __float2half2_rn(r1i), ndi1 = __float2half2_rn(-r1i);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          xre[q] = __hfma2(ndr0, hre[j0][q], __hfma2(pdi0, him[j0][q], xre[q]));
+          xim[q] = __hfma2(ndr0, him[j0][q], __hfma2(ndi0, hre[j0][q], xim[q]));
+          xre[q] = __hfma2(ndr1, hre[j1][q], __hfma2(pdi1, him[j1][q], xre[q]));
+          xim[q] = __hfma2(ndr1, him[j1][q], __hfma2(ndi1, hre[j1][q], xim[q]));
+        }
+      }
+    }
+    float e;
+    {
+      __half2 acc = __hmul2(xre[0], xre[0]);
+      acc = __hfma2(xim[0], xim[0], acc);
+#pragma unroll
+      for (int q = 1; q < NP; ++q) {
+        acc = __hfma2(xre[q], xre[q], acc);
+        acc = __hfma2(xim[q], xim[q], acc);
+      }
+      const float2 f = __half22float2(acc);
+      e = gsum<G>(f.x + f.y);
+    }
+    const float gsc = rho_c > 0.f ? rho_c / __fsqrt_rn(e) : 1.f;
+    const __half2 g2 = __float2half2_rn(gsc);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      xre[q] = __hmul2(g2, xre[q]);
+      xim[q] = __hmul2(g2, xim[q]);
+    }
+    float gq = 0.f;
+    if (GAIN) {
+      __half2 acc = __hmul2(vre[0], xre[0]);
+      acc = __hfma2(vim[0], xim[0], acc);
+#pragma unroll
+      for (int q = 1; q < NP; ++q) {
+        acc = __hfma2(vre[q], xre[q], acc);
+        acc = __hfma2(vim[q], xim[q], acc);
+      }
+      const float2 f = __half22float2(acc);
+      gq = gsum<G>(f.x + f.y);
+    }
+    if (p < P) {
+      if (zero_user >= 0) record_status(status, p, ST_ZERO_ROW, zero_user);
+      if (k == 0) {
+        if (e == 0.f && rho_c > 0.f) record_status(status, p, ST_ZERO_BEAMFORMER, 0);
+        if (GAIN) gain_part[p] = gq;
+      }
+      uint4* x4 = reinterpret_cast<uint4*>(X + static_cast<size_t>(p) * BC);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        uint4 v;
+        v.x = h2_as_u32(__lows2half2(xre[2 * c], xim[2 * c]));
+        v.y = h2_as_u32(__highs2half2(xre[2 * c], xim[2 * c]));
+        v.z = h2_as_u32(__lows2half2(xre[2 * c + 1], xim[2 * c + 1]));
+        v.w = h2_as_u32(__highs2half2(xre[2 * c + 1], xim[2 * c + 1]));
+        x4[c * G + k] = v;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace dcdg

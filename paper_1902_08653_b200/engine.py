@@ -5,7 +5,10 @@ Tensor conventions (device batch layout of include/dcdg.h):
 
   fp32:  torch.complex64   H [S, C, U, Bc], y [S, C, Bc], s [S, U]
   fp16:  torch.float16     H [S, C, U, Bc, 2], y [S, C, Bc, 2], s [S, U, 2]
-         (interleaved (re, im) binary16 — the paper's half-precision path)
+         binary16 — the paper's half-precision path.  s, x_local and x are
+         interleaved (re, im); the channel tiles H and receive vectors y are
+         ROW-PAIR PLANAR along the antenna axis ({re_2i, re_2i+1, im_2i,
+         im_2i+1}, include/dcdg.h): build them with ``to_fp16_pairs``.
 
 Each tile H[s, c] is the cluster's B_c x U uplink block stored column by
 column (one user column of B_c antennas after the other), i.e. the memory
@@ -66,6 +69,24 @@ def complex_empty(shape, fmt: int, device) -> torch.Tensor:
 def to_fp16(t: torch.Tensor) -> torch.Tensor:
     """complex64 -> float16 [..., 2] (RNE), on the tensor's device."""
     return torch.view_as_real(t).to(torch.float16).contiguous()
+
+
+def to_fp16_pairs(t: torch.Tensor) -> torch.Tensor:
+    """complex64 [..., B] -> float16 [..., B, 2] in the row-pair planar layout
+    of fp16 channel tiles / receive vectors (B even)."""
+    r = torch.view_as_real(t)
+    shp = r.shape
+    if shp[-2] % 2:
+        raise ValueError("fp16 row-pair planar layout needs an even antenna count")
+    r = r.reshape(*shp[:-2], shp[-2] // 2, 2, 2).transpose(-1, -2)
+    return r.reshape(shp).to(torch.float16).contiguous()
+
+
+def from_fp16_pairs(t: torch.Tensor) -> torch.Tensor:
+    """Inverse of ``to_fp16_pairs`` (returns complex64)."""
+    shp = t.shape
+    r = t.float().reshape(*shp[:-2], shp[-2] // 2, 2, 2).transpose(-1, -2).reshape(shp)
+    return torch.view_as_complex(r.contiguous())
 
 
 def to_complex64(t: torch.Tensor) -> torch.Tensor:

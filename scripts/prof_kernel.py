@@ -1,0 +1,30 @@
+"""Launch the CD kernels a few times at the north-star shape for ncu capture.
+usage: python scripts/prof_kernel.py [ul|dl] [fp32|fp16] [reps] [S]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import math  # noqa: E402
+
+import torch  # noqa: E402
+
+from bench import make_inputs  # noqa: E402
+from paper_1902_08653_b200 import Engine, to_fp16, to_fp16_pairs  # noqa: E402
+
+direction = sys.argv[1] if len(sys.argv) > 1 else "ul"
+fmt = sys.argv[2] if len(sys.argv) > 2 else "fp32"
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 4
+S = int(sys.argv[4]) if len(sys.argv) > 4 else 16800
+dev = torch.device("cuda", 0)
+eng = Engine(0)
+H, y, x, n0 = make_inputs(S, 8, dev, 1)
+if fmt == "fp16":
+    H, y, x = to_fp16_pairs(H), to_fp16_pairs(y), to_fp16(x)
+for _ in range(reps):
+    if direction == "ul":
+        eng.ul_detect(H, y, n0=n0, K=3, fusion="uniform", want_xhat=False)
+    else:
+        eng.dl_precode(H, x, rho=math.sqrt(16), K=3, want_gain=False)
+eng.sync()
+torch.cuda.synchronize()
+print("done", direction, fmt, eng.launches)

@@ -28,10 +28,16 @@ def rel_err(got, want, axis=-1):
     return float(np.max(num / den)) if num.size else 0.0
 
 
-def to_dev(a, fmt="fp32"):
+def to_dev(a, fmt="fp32", pairs=False):
+    """numpy complex -> device tensor; fp16 channel tiles / receive vectors use
+    the row-pair planar layout (pairs=True), symbol vectors stay interleaved."""
     import torch
+
+    from paper_1902_08653_b200 import to_fp16_pairs
     t = torch.from_numpy(np.ascontiguousarray(a, np.complex128)).to(torch.complex64).cuda()
     if fmt == "fp16":
+        if pairs:
+            return to_fp16_pairs(t)
         return torch.view_as_real(t).to(torch.float16).contiguous()
     return t.contiguous()
 

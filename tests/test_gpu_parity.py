@@ -50,7 +50,8 @@ def test_uplink_fp16(engine, port, shape):
     b = batch(C, Bc, U, S=48)
     xhat, local, _ = port.ul_detect_batch(b["h_tiles"], b["y"], b["n0"], 1.0, 3, UNIFORM)
     xhat16, local16, _ = port.ul_detect_batch(b["h_tiles"], b["y"], b["n0"], 1.0, 3, UNIFORM, FP16, FULL_STORAGE)
-    r = engine.ul_detect(to_dev(b["h_tiles"], "fp16"), to_dev(b["y"], "fp16"), n0=b["n0"], K=3, fusion="uniform")
+    r = engine.ul_detect(to_dev(b["h_tiles"], "fp16", True), to_dev(b["y"], "fp16", True), n0=b["n0"], K=3,
+                         fusion="uniform")
     engine.sync()
     assert rel_err(to_host(r.x_local), local) <= TOL_FP16
     assert rel_err(to_host(r.x_local), local16) <= TOL_FP16
@@ -67,7 +68,7 @@ def test_downlink(engine, port, shape, fmt):
     sym = qam_symbols(48, U)
     rho = float(np.sqrt(U))  # harness.cpp:159, rho = sqrt(U * Ex)
     x, g = port.dl_precode_batch(b["h_tiles"], sym, rho, 3)
-    r = engine.dl_precode(to_dev(b["h_tiles"], fmt), to_dev(sym, fmt), rho=rho, K=3)
+    r = engine.dl_precode(to_dev(b["h_tiles"], fmt, True), to_dev(sym, fmt), rho=rho, K=3)
     engine.sync()
     tol = TOL_FP32 if fmt == "fp32" else TOL_FP16
     assert rel_err(to_host(r.x), x) <= tol
