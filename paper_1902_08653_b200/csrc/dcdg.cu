@@ -82,13 +82,17 @@ using UlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, 
 using DlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, int, float, void*, float*,
                                  cudaStream_t);
 
+#ifndef DCDG_LB_UL
+#define DCDG_LB_UL 2
+#endif
 template <int BC, int U, int G, int MINB>
 cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
                           cudaStream_t st) {
   constexpr int NPW = 32 / G;
+  constexpr int LB = (U % DCDG_LB_UL == 0 && (U * DCDG_LB_UL) % G == 0) ? DCDG_LB_UL : 2;
   constexpr size_t smem =
-      dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U), NPW, kWarps>::kBytes;
-  auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps, MINB>;
+      dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U, LB), NPW, kWarps>::kBytes;
+  auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps, MINB, LB>;
   static const int occ = occupancy_of(kern, smem);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);

@@ -16,14 +16,14 @@
 //     in registers, so the HBM stream overlaps the whole sweep computation.
 //     Warps are persistent (grid = SMs x occupancy).
 //
-// Coordinate pairs (latency)
+// Coordinate blocks (latency)
 //   Alg. 1 / Alg. 2 update one coordinate at a time, and every update needs a
 //   group-wide reduction of a B_c-long dot product (log2(G) shuffle rounds) —
 //   the latency that bounds a naive mapping.  Here coordinates are processed
-//   in the reference's order but two at a time: both dot products of the
-//   pair (j, j+1) are taken against the same residual and reduced in ONE
-//   shuffle round; the second is then corrected exactly with the pair Gram
-//   entry computed once per problem:
+//   in the reference's order but a block of LB at a time: all LB dot products
+//   are taken against the same residual and reduced in ONE shuffle round; each
+//   is then corrected exactly for the updates made earlier in the block with
+//   the block's Gram entries, computed once per problem:
 //       h_{j+1}^H (r - dx_j h_j) = h_{j+1}^H r - dx_j (h_{j+1}^H h_j).
 //   The iterates are those of the reference (same sweep order, same updates
 //   in exact arithmetic); only fp rounding differs.
@@ -95,7 +95,9 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int k) {
 
 // Per-problem scalar blocks (bytes); +16 skews consecutive groups' blocks
 // across shared-memory banks.  Used by the kernels and their launchers.
-__host__ __device__ constexpr int ul_scal_bytes(int U) { return U * 24 + 16; }
+__host__ __device__ constexpr int ul_scal_bytes(int U, int LB = 2) {
+  return U * 16 + (U / LB) * (LB * (LB - 1) / 2) * 16 + 16;
+}
 __host__ __device__ constexpr int dl_scal_bytes(int U) { return U * 32 + 16; }
 
 // Shared-memory layout of one CTA: [W staging slots][W*NPW scalar blocks][W mbarriers]
@@ -111,24 +113,28 @@ struct CtaSmem {
 // its rows as float2 (row 2c, row 2c+1) planes of re and im, so each complex
 // MAC over two rows is 2 FFMA2 (sm_100 packed fp32x2) and the rank-1
 // coefficient dx is a broadcast operand.
+// Coordinates are processed in blocks of LB (see "Coordinate blocks" above):
+// one shuffle round reduces all LB dot products, then the block's
+// lower-triangular Gram entries G_ab = h_a^H h_b (a > b) correct them exactly.
 // Scalar block per problem: float4 mnx[U] = (m_j, n_j, Re x_j, Im x_j) and
-// float4 gp[U/2] = (Re G, Im G, -Im G, Re G) with G = h_{2i+1}^H h_{2i}.
+// float4 gb[U/LB][LB(LB-1)/2] = (Re G, Im G, -Im G, Re G).
 // ===========================================================================
-template <int BC, int U, int G, int W, int MINB>
+template <int BC, int U, int G, int W, int MINB, int LB>
 __global__ void __launch_bounds__(32 * W, MINB)
     ul_reg_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
                float2* __restrict__ X) {
-  static_assert(32 % G == 0 && BC % (2 * G) == 0 && U % 2 == 0 && (2 * U) % G == 0, "shape");
+  static_assert(32 % G == 0 && BC % (2 * G) == 0 && U % LB == 0 && (U * LB) % G == 0, "shape");
   constexpr int NPW = 32 / G, R = BC / G, NP = R / 2;
+  constexpr int T = LB * (LB - 1) / 2;  // Gram entries per block
   constexpr int TILE_B = BC * U * 8, Y_B = BC * 8, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
-  constexpr int SCAL_B = ul_scal_bytes(U);
+  constexpr int SCAL_B = ul_scal_bytes(U, LB);
   using L = CtaSmem<SLOT_B, SCAL_B, NPW, W>;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane / G, k = lane % G;
   unsigned char* slot = smem + warp * SLOT_B;
   float4* mnx = reinterpret_cast<float4*>(smem + L::kScalOff + (warp * NPW + g) * SCAL_B);
-  float4* gp = mnx + U;
+  float4* gb = mnx + U;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff) + warp;
   const int nsets = (P + NPW - 1) / NPW;
   const int nw = gridDim.x * W;
@@ -169,9 +175,9 @@ __global__ void __launch_bounds__(32 * W, MINB)
     __syncwarp();
     if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
 
-    // ---- per-problem scalars: ||h_j||^2 (detect.cpp:86-90) and pair Grams
+    // ---- per-problem scalars: ||h_j||^2 (detect.cpp:86-90) and block Grams
     {
-      float v[2 * U];
+      float v[U * LB];
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         float2 e = fmul2(hr[j][0], hr[j][0]);
@@ -181,19 +187,24 @@ __global__ void __launch_bounds__(32 * W, MINB)
         v[j] = hsum(e);
       }
 #pragma unroll
-      for (int i = 0; i < U / 2; ++i) {  // G = h_{2i+1}^H h_{2i}
-        float2 gr = z2, gi = z2;
+      for (int q = 0; q < U / LB; ++q)
 #pragma unroll
-        for (int c = 0; c < NP; ++c) {
-          gr = ffma2(hi[2 * i + 1][c], hi[2 * i][c], ffma2(hr[2 * i + 1][c], hr[2 * i][c], gr));
-          gi = ffma2(neg2(hi[2 * i + 1][c]), hr[2 * i][c], ffma2(hr[2 * i + 1][c], hi[2 * i][c], gi));
-        }
-        v[U + 2 * i] = hsum(gr);
-        v[U + 2 * i + 1] = hsum(gi);
-      }
+        for (int a = 1; a < LB; ++a)
+#pragma unroll
+          for (int b = 0; b < a; ++b) {  // G_ab = h_{qLB+a}^H h_{qLB+b}
+            const int ja = q * LB + a, jb = q * LB + b, e = q * T + a * (a - 1) / 2 + b;
+            float2 gr = z2, gi = z2;
+#pragma unroll
+            for (int c = 0; c < NP; ++c) {
+              gr = ffma2(hi[ja][c], hi[jb][c], ffma2(hr[ja][c], hr[jb][c], gr));
+              gi = ffma2(neg2(hi[ja][c]), hr[jb][c], ffma2(hr[ja][c], hi[jb][c], gi));
+            }
+            v[U + 2 * e] = hsum(gr);
+            v[U + 2 * e + 1] = hsum(gi);
+          }
       group_reduce_scatter<G>(v, k);
-      constexpr int PER = 2 * U / G;
-      float* gf = reinterpret_cast<float*>(gp);
+      constexpr int PER = U * LB / G;
+      float* gf = reinterpret_cast<float*>(gb);
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const int idx = k * PER + i;
@@ -201,60 +212,66 @@ __global__ void __launch_bounds__(32 * W, MINB)
           const float m = __fdividef(1.f, v[i] + kappa);  // m_j = 1/(||h_j||^2 + N0/Ex)
           mnx[idx] = make_float4(m, m * v[i], 0.f, 0.f);  // n_j = m_j ||h_j||^2, x_j = 0
         } else {
-          const int gi = idx - U, pr = gi >> 1;
+          const int gi = idx - U, e = gi >> 1;
           if (gi & 1) {
-            gf[pr * 4 + 1] = v[i];
-            gf[pr * 4 + 2] = -v[i];
+            gf[e * 4 + 1] = v[i];
+            gf[e * 4 + 2] = -v[i];
           } else {
-            gf[pr * 4 + 0] = v[i];
-            gf[pr * 4 + 3] = v[i];
+            gf[e * 4 + 0] = v[i];
+            gf[e * 4 + 3] = v[i];
           }
         }
       }
     }
     __syncwarp();
 
-    // ---- K sweeps over the users in ascending order, two coordinates per round
+    // ---- K sweeps over the users in ascending order, LB coordinates per round
     for (int t = 0; t < K; ++t) {
 #pragma unroll
-      for (int jp = 0; jp < U / 2; ++jp) {
-        const int j0 = 2 * jp, j1 = 2 * jp + 1;
-        const float4 A0 = mnx[j0], A1 = mnx[j1], GG = gp[jp];
-        // h_j^H r for both coordinates (cdotc, detect.cpp:100), on row pairs
-        float2 a0 = z2, c0 = z2, a1 = z2, c1 = z2;
+      for (int q = 0; q < U / LB; ++q) {
+        float2 d[LB];
 #pragma unroll
-        for (int c = 0; c < NP; ++c) {
-          a0 = ffma2(hi[j0][c], ri[c], ffma2(hr[j0][c], rr[c], a0));
-          c0 = ffma2(neg2(hi[j0][c]), rr[c], ffma2(hr[j0][c], ri[c], c0));
-          a1 = ffma2(hi[j1][c], ri[c], ffma2(hr[j1][c], rr[c], a1));
-          c1 = ffma2(neg2(hi[j1][c]), rr[c], ffma2(hr[j1][c], ri[c], c1));
+        for (int a = 0; a < LB; ++a) {  // h_j^H r (cdotc, detect.cpp:100), all against the same r
+          const int j = q * LB + a;
+          float2 ar = z2, ai = z2;
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            ar = ffma2(hi[j][c], ri[c], ffma2(hr[j][c], rr[c], ar));
+            ai = ffma2(neg2(hi[j][c]), rr[c], ffma2(hr[j][c], ri[c], ai));
+          }
+          d[a] = make_float2(hsum(ar), hsum(ai));
         }
-        float2 d0 = make_float2(hsum(a0), hsum(c0));
-        float2 d1 = make_float2(hsum(a1), hsum(c1));
 #pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) {
-          d0 = fadd2(d0, shfl_xor2(d0, o));
-          d1 = fadd2(d1, shfl_xor2(d1, o));
+        for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+          for (int a = 0; a < LB; ++a) d[a] = fadd2(d[a], shfl_xor2(d[a], o));
+        float2 dx[LB];
+#pragma unroll
+        for (int a = 0; a < LB; ++a) {
+          const int j = q * LB + a;
+          const float4 A = mnx[j];
+          // h_j^H (r - sum_{b<a} dx_b h_b) = h_j^H r - sum_b dx_b G_ab
+#pragma unroll
+          for (int b = 0; b < a; ++b) {
+            const float4 Gab = gb[q * T + a * (a - 1) / 2 + b];
+            d[a] = ffma2(-dx[b].x, make_float2(Gab.x, Gab.y), d[a]);
+            d[a] = ffma2(-dx[b].y, make_float2(Gab.z, Gab.w), d[a]);
+          }
+          // x_j' = m_j h_j^H r + n_j x_j ; dx = x_j' - x_j   (detect.cpp:100-103)
+          const float2 xo = make_float2(A.z, A.w);
+          const float2 xn = ffma2(A.x, d[a], fmul2(A.y, xo));
+          dx[a] = fadd2(xn, neg2(xo));
+          *reinterpret_cast<float2*>(&mnx[j].z) = xn;  // every lane of the group stores the same value
         }
-        // x_j' = m_j h_j^H r + n_j x_j ; dx = x_j' - x_j   (detect.cpp:100-103)
-        const float2 x0 = make_float2(A0.z, A0.w), x1 = make_float2(A1.z, A1.w);
-        const float2 n0 = ffma2(A0.x, d0, fmul2(A0.y, x0));
-        const float2 dx0 = fadd2(n0, neg2(x0));
-        // h_{j+1}^H (r - dx_j h_j) = h_{j+1}^H r - dx_j G
-        d1 = ffma2(-dx0.x, make_float2(GG.x, GG.y), d1);
-        d1 = ffma2(-dx0.y, make_float2(GG.z, GG.w), d1);
-        const float2 n1 = ffma2(A1.x, d1, fmul2(A1.y, x1));
-        const float2 dx1 = fadd2(n1, neg2(x1));
-        // every lane of the group stores the same value
-        *reinterpret_cast<float2*>(&mnx[j0].z) = n0;
-        *reinterpret_cast<float2*>(&mnx[j1].z) = n1;
-        // r -= dx_j h_j ; r -= dx_{j+1} h_{j+1}   (caxpy, detect.cpp:104)
+        // r -= dx_j h_j for the block   (caxpy, detect.cpp:104)
 #pragma unroll
-        for (int c = 0; c < NP; ++c) {
-          rr[c] = ffma2(dx0.y, hi[j0][c], ffma2(-dx0.x, hr[j0][c], rr[c]));
-          ri[c] = ffma2(-dx0.y, hr[j0][c], ffma2(-dx0.x, hi[j0][c], ri[c]));
-          rr[c] = ffma2(dx1.y, hi[j1][c], ffma2(-dx1.x, hr[j1][c], rr[c]));
-          ri[c] = ffma2(-dx1.y, hr[j1][c], ffma2(-dx1.x, hi[j1][c], ri[c]));
+        for (int a = 0; a < LB; ++a) {
+          const int j = q * LB + a;
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            rr[c] = ffma2(dx[a].y, hi[j][c], ffma2(-dx[a].x, hr[j][c], rr[c]));
+            ri[c] = ffma2(-dx[a].y, hr[j][c], ffma2(-dx[a].x, hi[j][c], ri[c]));
+          }
         }
       }
     }
@@ -271,6 +288,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
     __syncwarp();
   }
 }
+
 // ===========================================================================
 // Uplink, fp16 storage + half2 arithmetic (the paper's half-precision path).
 // The fp16 channel tile and receive vector are stored row-pair planar
