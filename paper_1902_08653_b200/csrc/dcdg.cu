@@ -354,7 +354,6 @@ long long dcdg_last_error_problem(void) { return g_err_problem; }
 int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, int C_total, int Bc, int U, int K,
                    double n0, double ex, int fmt, int fusion, void* x_local, float* sigma2, float* xhat, float* wsum,
                    void* stream) {
-  if (int rc = check_ctx(ctx)) return rc;
   if (int rc = check_fmt(fmt)) return rc;
   // argument checks in the reference's order and words (detect.cpp:12-19,71-72,150-155)
   if (C <= 0 || S < 0) return fail(DCDG_EINVAL, "decentralized_cd_detect: no clusters");
@@ -371,6 +370,7 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
   if (!H || !y) return fail(DCDG_EINVAL, "dcdg_ul_detect: null input buffer");
   const long long P = static_cast<long long>(S) * C;
   if (P > 0x7fffffffLL) return fail(DCDG_EINVAL, "dcdg_ul_detect: batch too large (S*C must fit in int32)");
+  if (int rc = check_ctx(ctx)) return rc;  // after the device-independent argument checks
   if (P == 0) return DCDG_OK;
   CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
   cudaStream_t st = as_stream(stream);
@@ -418,7 +418,6 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
 
 int dcdg_dl_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, int C_total, int Bc, int U, int K,
                     double rho, int fmt, void* x_dl, float* gain_part, float* gain, void* stream) {
-  if (int rc = check_ctx(ctx)) return rc;
   if (int rc = check_fmt(fmt)) return rc;
   // precode.cpp:11-16,57-58,138-152,101-104
   if (C <= 0 || S < 0) return fail(DCDG_EINVAL, "decentralized_cd_precode: no clusters");
@@ -435,6 +434,7 @@ int dcdg_dl_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, i
   if (!H || !s || !x_dl) return fail(DCDG_EINVAL, "dcdg_dl_precode: null buffer");
   const long long P = static_cast<long long>(S) * C;
   if (P > 0x7fffffffLL) return fail(DCDG_EINVAL, "dcdg_dl_precode: batch too large (S*C must fit in int32)");
+  if (int rc = check_ctx(ctx)) return rc;  // after the device-independent argument checks
   if (P == 0) return DCDG_OK;
   CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
   cudaStream_t st = as_stream(stream);
@@ -472,13 +472,13 @@ int dcdg_dl_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, i
 
 int dcdg_post_eq_variance(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, double n0, double ex, int fmt,
                           float* sigma2, void* stream) {
-  if (int rc = check_ctx(ctx)) return rc;
   if (int rc = check_fmt(fmt)) return rc;
   if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "post_eq_variance: empty channel block");
   if (!(n0 > 0.0) || !(ex > 0.0)) return fail(DCDG_EINVAL, "post_eq_variance: need N0 > 0 and E_x > 0");
   if (U > 32) return fail(DCDG_EINVAL, "dcdg_post_eq_variance: U > 32 not supported");
   if (fmt == DCDG_FP16 && (Bc & 1))
     return fail(DCDG_EINVAL, "dcdg: fp16 row-pair planar tiles need an even antenna count B_c");
+  if (int rc = check_ctx(ctx)) return rc;  // after the device-independent argument checks
   if (P <= 0) return DCDG_OK;
   CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
   return launch_post_eq(ctx, H, P, Bc, U, n0, ex, fmt, sigma2, as_stream(stream));
@@ -486,12 +486,12 @@ int dcdg_post_eq_variance(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, do
 
 int dcdg_fuse(dcdg_ctx* ctx, const void* x_local, const float* sigma2, int S, int C, int C_total, int U, int fmt,
               int fusion, float* xhat, float* wsum, void* stream) {
-  if (int rc = check_ctx(ctx)) return rc;
   if (int rc = check_fmt(fmt)) return rc;
   if (C <= 0) return fail(DCDG_EINVAL, "fusion_weights: no clusters");
   if (C_total < C) return fail(DCDG_EINVAL, "dcdg_fuse: C_total must be >= C");
   const bool optimal = fusion == DCDG_FUSION_OPTIMAL;
   if (optimal && !sigma2) return fail(DCDG_EINVAL, "dcdg_fuse: optimal fusion needs sigma2");
+  if (int rc = check_ctx(ctx)) return rc;  // after the device-independent argument checks
   if (S <= 0) return DCDG_OK;
   CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
   return launch_fuse(ctx, x_local, sigma2, S, C, C_total, U, fmt, optimal, xhat, wsum, as_stream(stream));
@@ -529,10 +529,10 @@ int dcdg_gain_reduce(dcdg_ctx* ctx, const float* gain_part, const void* s, int S
 }
 
 int dcdg_power_scale(dcdg_ctx* ctx, void* x, int P, int n, double rho, int fmt, void* stream) {
-  if (int rc = check_ctx(ctx)) return rc;
   if (int rc = check_fmt(fmt)) return rc;
   if (!(rho > 0.0)) return fail(DCDG_EINVAL, "power_scale: amplitude must be positive");
   if (n <= 0) return fail(DCDG_EINVAL, "power_scale: empty beamformer");
+  if (int rc = check_ctx(ctx)) return rc;  // after the device-independent argument checks
   if (P <= 0) return DCDG_OK;
   CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
   const int blocks = (P + 3) / 4;
@@ -548,8 +548,8 @@ int dcdg_power_scale(dcdg_ctx* ctx, void* x, int P, int n, double rho, int fmt, 
 }
 
 int dcdg_fusion_weights(dcdg_ctx* ctx, const float* sigma2, int S, int C, float* w, void* stream) {
-  if (int rc = check_ctx(ctx)) return rc;
   if (C <= 0) return fail(DCDG_EINVAL, "fusion_weights: no clusters");
+  if (int rc = check_ctx(ctx)) return rc;  // after the device-independent argument checks
   if (S <= 0) return DCDG_OK;
   CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
   dcdg::fusion_weights_kernel<<<(S + 127) / 128, 128, 0, as_stream(stream)>>>(sigma2, S, C, w, ctx->d_status);
