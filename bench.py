@@ -122,11 +122,69 @@ def make_inputs(S, c_local, device, seed):
     return H.contiguous(), y.contiguous(), x.contiguous(), n0
 
 
+def _ev():
+    import torch
+    return torch.cuda.Event(enable_timing=True)
+
+
+def _time_stream(fn, stream, reps):
+    """Average ms of `fn` over `reps` calls, CUDA events on `stream`."""
+    import torch
+    torch.cuda.synchronize()
+    a, b = _ev(), _ev()
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def secondary_lines(eng, dev, S, reps, hbm):
+    """Kernel-level numbers for the other north-star workloads (configs[2],
+    configs[3] and optimal fusion) at the same batch size, N=1."""
+    import torch
+
+    from paper_1902_08653_b200 import to_fp16, to_fp16_pairs
+    out = {}
+    H, y, x, n0 = make_inputs(S, C, dev, 4321)
+    st = torch.cuda.current_stream(dev)
+    P = S * C
+    rho = math.sqrt(U)
+    for fmt in ("fp32", "fp16"):
+        esz = 8 if fmt == "fp32" else 4
+        Hh, yh, xh = (H, y, x) if fmt == "fp32" else (to_fp16_pairs(H), to_fp16_pairs(y), to_fp16(x))
+        for d in ("ul", "dl"):
+            if d == "ul":
+                fn = lambda: eng.ul_detect(Hh, yh, n0=n0, K=K_SWEEPS, fusion="uniform")  # noqa: E731
+                kfn = lambda: eng.ul_detect(Hh, yh, n0=n0, K=K_SWEEPS, want_xhat=False)  # noqa: E731
+            else:
+                fn = lambda: eng.dl_precode(Hh, xh, rho=rho, K=K_SWEEPS, want_gain=True)  # noqa: E731
+                kfn = lambda: eng.dl_precode(Hh, xh, rho=rho, K=K_SWEEPS, want_gain=False)  # noqa: E731
+            for _ in range(3):
+                fn()
+            ms = _time_stream(fn, st, reps)
+            kms = _time_stream(kfn, st, reps)
+            ach = P * alg_bytes_per_problem(BC, U, esz) / (kms * 1e-3) / 1e9
+            out[f"{d}_{fmt}"] = {"value": round(S * U * BITS / (ms * 1e-3) / 1e9, 4), "unit": "Gbps",
+                                 "ms_per_batch": round(ms, 5), "kernel_ms": round(kms, 5),
+                                 "roofline_frac": round(ach / hbm, 4), "achieved_GBps": round(ach, 1)}
+    fn = lambda: eng.ul_detect(H, y, n0=n0, K=K_SWEEPS, fusion="optimal")  # noqa: E731
+    fn()
+    ms = _time_stream(fn, st, reps)
+    out["ul_fp32_optimal_fusion"] = {"value": round(S * U * BITS / (ms * 1e-3) / 1e9, 4), "unit": "Gbps",
+                                     "ms_per_batch": round(ms, 5),
+                                     "note": "CD kernel + post-equalization variance (Gram+Cholesky) + fusion"}
+    eng.sync()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_1902_08653_b200 import Engine, kernel_name, to_fp16_pairs
+    from paper_1902_08653_b200.distributed import CudaCompute, DistributedCD, partition
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -135,28 +193,21 @@ def run_ours(args):
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    if C % world:
-        raise SystemExit(f"C={C} clusters cannot be split over {world} GPUs")
-    c_local = C // world
-    S = args.S * world  # weak scaling: per-GPU problems fixed at args.S * C
+    S_total = args.S * world  # weak scaling: per-GPU work fixed at args.S * C problems
+    part = partition(C, world, rank, S_total)
     fmt = args.fmt
     esz = 8 if fmt == "fp32" else 4
     eng = Engine(local_rank)
+    dcd = DistributedCD(part, CudaCompute(eng), mode=args.mode)
 
-    H, y, xs, n0 = make_inputs(S, c_local, dev, 1234 + rank)
+    H, y, _, n0 = make_inputs(part.S_local, part.C_local, dev, 1234 + rank)
     if fmt == "fp16":
         H, y = to_fp16_pairs(H), to_fp16_pairs(y)
-    P = S * c_local
-    xhat = torch.empty((S, U), dtype=torch.complex64, device=dev)
-    x_local = torch.empty((S, c_local, U), dtype=torch.complex64, device=dev) if fmt == "fp32" else \
-        torch.empty((S, c_local, U, 2), dtype=torch.float16, device=dev)
-    out_rs = torch.empty((S // world, U), dtype=torch.complex64, device=dev)
+    P = part.S_local * part.C_local
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        eng.ul_detect(H, y, n0=n0, K=K_SWEEPS, fusion=args.fusion, C_total=C, x_local=x_local, xhat=xhat)
-        if world > 1:
-            dist.reduce_scatter_tensor(torch.view_as_real(out_rs), torch.view_as_real(xhat))
+        return dcd.uplink(H, y, n0=n0, K=K_SWEEPS, fusion=args.fusion)
 
     def barrier():
         if world > 1:
@@ -168,7 +219,7 @@ def run_ours(args):
     eng.sync()
     barrier()
     l0 = eng.launches
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0, e1 = _ev(), _ev()
     with ClockSampler(local_rank) as clk:
         barrier()
         e0.record(stream)
@@ -182,61 +233,74 @@ def run_ours(args):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = S * U * BITS / (ms * 1e-3) / 1e9  # whole-job Gbps (S subcarriers fused per step)
+    value = S_total * U * BITS / (ms * 1e-3) / 1e9  # whole-job Gbps: S_total subcarrier-symbols detected per step
 
-    # dominant kernel alone (the CD kernel, on the same stream), for the roofline
+    # dominant kernel alone (the CD kernel, same stream) for the roofline
+    kfn = lambda: eng.ul_detect(H, y, n0=n0, K=K_SWEEPS, want_xhat=False)  # noqa: E731
     for _ in range(3):
-        eng.ul_detect(H, y, n0=n0, K=K_SWEEPS, fusion="uniform", C_total=C, x_local=x_local, want_xhat=False)
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    nk = max(args.steps, 5)
-    torch.cuda.synchronize(dev)
-    k0.record(stream)
-    for _ in range(nk):
-        eng.ul_detect(H, y, n0=n0, K=K_SWEEPS, fusion="uniform", C_total=C, x_local=x_local, want_xhat=False)
-    k1.record(stream)
-    torch.cuda.synchronize(dev)
-    k_ms = k0.elapsed_time(k1) / nk
+        kfn()
+    k_ms = _time_stream(kfn, stream, max(args.steps, 5))
     hbm, hbm_src = peaks()
-    achieved = P * alg_bytes_per_problem(BC, U, esz) / (k_ms * 1e-3) / 1e9
+    alg = P * alg_bytes_per_problem(BC, U, esz)
+    achieved = alg / (k_ms * 1e-3) / 1e9
 
-    # e2e through the public API with pinned host buffers
-    e2e = None
-    if rank == 0 or world > 1:
-        Hh = H.cpu().pin_memory()
-        yh = y.cpu().pin_memory()
-        xh = torch.empty((S, U), dtype=torch.complex64).pin_memory()
-        Hd, yd = torch.empty_like(H), torch.empty_like(y)
+    # e2e through the public API: pinned host H, y -> device (copy stream,
+    # chunked) overlapped with detection (compute stream) -> host estimates
+    Hh = H.cpu().pin_memory()
+    yh = y.cpu().pin_memory()
+    Hd, yd = torch.empty_like(H), torch.empty_like(y)
+    n_chunks = 8 if (world == 1 and part.S_local % 8 == 0) else 1
+    cs = part.S_local // n_chunks
+    copy_st, comp_st = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    own = part.own_hi - part.own_lo
+    xh_host = torch.empty((own, U), dtype=torch.complex64).pin_memory()
 
-        def e2e_step():
-            Hd.copy_(Hh, non_blocking=True)
-            yd.copy_(yh, non_blocking=True)
-            eng.ul_detect(Hd, yd, n0=n0, K=K_SWEEPS, fusion=args.fusion, C_total=C, x_local=x_local, xhat=xhat)
-            if world > 1:
-                dist.reduce_scatter_tensor(torch.view_as_real(out_rs), torch.view_as_real(xhat))
-                xh[: S // world].copy_(out_rs, non_blocking=True)
+    def e2e_step():
+        evs = []
+        for i in range(n_chunks):
+            with torch.cuda.stream(copy_st):
+                Hd[i * cs:(i + 1) * cs].copy_(Hh[i * cs:(i + 1) * cs], non_blocking=True)
+                yd[i * cs:(i + 1) * cs].copy_(yh[i * cs:(i + 1) * cs], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_st)
+                evs.append(ev)
+        with torch.cuda.stream(comp_st):
+            if world == 1:
+                for i in range(n_chunks):
+                    comp_st.wait_event(evs[i])
+                    r = eng.ul_detect(Hd[i * cs:(i + 1) * cs], yd[i * cs:(i + 1) * cs], n0=n0, K=K_SWEEPS,
+                                      fusion=args.fusion, want_local=False, stream=comp_st)
+                    xh_host[i * cs:(i + 1) * cs].copy_(r.xhat, non_blocking=True)
             else:
-                xh.copy_(xhat, non_blocking=True)
+                comp_st.wait_event(evs[-1])
+                out = dcd.uplink(Hd, yd, n0=n0, K=K_SWEEPS, fusion=args.fusion)
+                xh_host.copy_(out, non_blocking=True)
 
+    e2e_step()
+    barrier()
+    n_e2e = max(2, min(args.steps, 5))
+    t0, t1 = _ev(), _ev()
+    torch.cuda.synchronize(dev)
+    t0.record(copy_st)
+    for _ in range(n_e2e):
         e2e_step()
-        barrier()
-        n_e2e = max(2, min(args.steps, 5))
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        for _ in range(n_e2e):
-            e2e_step()
-        t1.record(stream)
-        barrier()
-        e_ms = t0.elapsed_time(t1) / n_e2e
-        if world > 1:
-            t = torch.tensor([e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        h2d = H.numel() * H.element_size() + y.numel() * y.element_size()
-        d2h = (S // world) * U * 8
-        e2e = {"value": S * U * BITS / (e_ms * 1e-3) / 1e9, "unit": "Gbps", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "path": "Engine.ul_detect (C ABI dcdg_ul_detect) with pinned host H,y -> device -> host xhat"}
+        comp_st.synchronize()  # the host consumes this step's estimates
+    t1.record(comp_st)
+    barrier()
+    e_ms = t0.elapsed_time(t1) / n_e2e
+    if world > 1:
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    h2d = H.numel() * H.element_size() + y.numel() * y.element_size()
+    e2e = {"value": round(S_total * U * BITS / (e_ms * 1e-3) / 1e9, 5), "unit": "Gbps", "ms_per_step": round(e_ms, 4),
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(own * U * 8),
+           "path": "Engine.ul_detect (C ABI dcdg_ul_detect): pinned host H,y -> device in %d chunks on a copy "
+                   "stream overlapped with detection -> host fused estimates" % n_chunks}
 
+    extra = None
+    if rank == 0 and world == 1 and not args.fast:
+        extra = secondary_lines(eng, dev, args.S, max(5, args.steps // 2), hbm)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -248,7 +312,7 @@ def run_ours(args):
             tj = json.load(open(tp))
             key = f"ul_{fmt}_{BC}_{U}"
             if key in tj:
-                traffic = tj[key]["dram_bytes_per_problem"] * P
+                traffic = int(tj[key]["dram_bytes_per_problem"] * P)
         except Exception:
             traffic = None
     line = {
@@ -264,22 +328,23 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f32" if fmt == "fp32" else "f16",
         "data": "synthetic: CN(0,1) Rayleigh H, Gray 16-QAM, AWGN at 10 dB, generated on device (torch RNG)",
-        "config": {"workload": "uplink CD L-MMSE detection + uniform fusion (configs[1])" if args.fusion == "uniform"
-                   else "uplink CD L-MMSE detection + optimal fusion",
+        "config": {"workload": f"uplink CD L-MMSE detection + {args.fusion} fusion (configs[1])",
                    "B": B, "U": U, "C": C, "B_c": BC, "K": K_SWEEPS, "qam": QAM, "fmt": fmt,
-                   "subcarrier_symbols_per_step": S, "problems_per_gpu": P, "clusters_per_gpu": c_local,
-                   "parallelism": f"clusters/{world}" if world > 1 else "single GPU, all clusters",
-                   "l2": f"inputs {P * alg_bytes_per_problem(BC, U, esz) / 1e6:.0f} MB/GPU > 126 MB L2, no flush needed",
+                   "subcarrier_symbols_per_step": S_total, "problems_per_gpu": P, "clusters_per_gpu": part.C_local,
+                   "parallelism": (f"clusters/{world}, fusion {args.mode}" if world > 1 else "single GPU, all clusters"),
+                   "l2": f"inputs {alg / 1e6:.0f} MB/GPU > 126 MB L2, no flush needed",
                    "kernel": kernel_name("ul", BC, U, fmt)},
         "batch_latency_ms": round(ms, 5),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_source": hbm_src,
-                     "kernel_ms": round(k_ms, 5),
-                     "alg_bytes_per_launch": P * alg_bytes_per_problem(BC, U, esz)},
+                     "kernel_ms": round(k_ms, 5), "alg_bytes_per_launch": alg,
+                     "alg_bytes_per_problem": alg_bytes_per_problem(BC, U, esz)},
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if extra:
+        line["extra"] = extra
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
     print(json.dumps(line))
@@ -327,20 +392,24 @@ def cpu_time_ref(S, threads, reps=1):
         L.dcdref_ul_batch_destroy(h)
 
 
+CPU_SAMPLE_S = 2400  # subcarrier-symbols per timed CPU run (x C = 19,200 cluster-problems, ~150 MB fp64)
+
+
 def cpu_baseline(target_s=10.0):
     threads = os.cpu_count() or 1
     if _ref_lib() is None:
         return {"value": None, "unit": "Gbps", "cores": threads, "kind": "reference",
                 "sample": "oracle/_ref/libdcdref.so missing"}
-    # calibrate, then size the sample to ~target_s seconds of all-core work
-    t, _ = cpu_time_ref(240 * threads, threads)
-    per_sc = t[0] / (240 * threads)
-    S = int(min(max(target_s / per_sc, 480), 200000))
-    ts, backend = cpu_time_ref(S, threads)
-    return {"value": round(S * U * BITS / ts[0] / 1e9, 6), "unit": "Gbps", "cores": threads, "kind": "reference",
-            "sample": f"{S} subcarrier-symbols x C={C} clusters, decentralized_cd_detect (uniform fusion, K=3) "
-                      f"over {threads} std::threads, {ts[0]:.2f} s, reference kernels backend={backend}",
-            "seconds": round(ts[0], 3)}
+    t, _ = cpu_time_ref(CPU_SAMPLE_S, threads)
+    reps = int(min(max(target_s / max(t[0], 1e-3), 1), 5000))
+    ts, backend = cpu_time_ref(CPU_SAMPLE_S, threads, reps=reps)
+    sec = sum(ts)
+    return {"value": round(CPU_SAMPLE_S * reps * U * BITS / sec / 1e9, 6), "unit": "Gbps", "cores": threads,
+            "kind": "reference",
+            "sample": f"{reps} x {CPU_SAMPLE_S} subcarrier-symbols (C={C} clusters each) through the reference's "
+                      f"decentralized_cd_detect (uniform fusion, K=3) on {threads} std::threads, {sec:.2f} s, "
+                      f"reference kernels backend={backend}",
+            "seconds": round(sec, 3)}
 
 
 def run_reference(args):
@@ -352,10 +421,12 @@ def run_reference(args):
     if _ref_lib() is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdcdref.so not built"}))
         return
-    t, _ = cpu_time_ref(120 * threads, threads)
-    per_sc = t[0] / (120 * threads)
-    budget = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.5)
-    S = int(min(max(budget / per_sc, 240), 200000))
+    # each step: a bounded sample of the workload through the reference's own
+    # decentralized_cd_detect, all host threads, sized to fit the time budget
+    t, _ = cpu_time_ref(CPU_SAMPLE_S, threads)
+    per_sc = t[0] / CPU_SAMPLE_S
+    budget = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.2)
+    S = int(min(max(budget / per_sc, 240), 4 * CPU_SAMPLE_S))
     ts, backend = cpu_time_ref(S, threads, reps=args.warmup + args.steps)
     timed = ts[args.warmup:]
     sec = sum(timed) / len(timed)
@@ -368,8 +439,8 @@ def run_reference(args):
                    "B_c": BC, "K": K_SWEEPS, "qam": QAM, "subcarrier_symbols_per_step": S},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 6), "unit": "Gbps", "cores": threads, "kind": "reference",
-                         "sample": f"{S} subcarrier-symbols per step, decentralized_cd_detect over {threads} threads, "
-                                   f"backend={backend}"},
+                         "sample": f"{S} subcarrier-symbols per step through decentralized_cd_detect on {threads} "
+                                   f"std::threads, backend={backend}"},
         "e2e": {"value": round(value, 6), "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -386,6 +457,8 @@ def main():
     ap.add_argument("--S", type=int, default=S_PER_GPU, help="subcarrier-symbols per GPU per step")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--fast", action="store_true", help="skip the secondary (DL, fp16, optimal) lines")
+    ap.add_argument("--mode", choices=["reduce", "gather"], default="reduce", help="multi-GPU fusion exchange")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
