@@ -89,7 +89,7 @@ template <int BC, int U, int G, int MINB>
 cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
                           cudaStream_t st) {
   constexpr int NPW = 32 / G;
-  constexpr int LB = (U % DCDG_LB_UL == 0 && (U * DCDG_LB_UL) % G == 0) ? DCDG_LB_UL : 2;
+  constexpr int LB = (U % DCDG_LB_UL == 0 && (2 * (U / DCDG_LB_UL) * (DCDG_LB_UL * (DCDG_LB_UL - 1) / 2)) % G == 0) ? DCDG_LB_UL : 2;
   constexpr size_t smem =
       dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U, LB), NPW, kWarps>::kBytes;
   auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps, MINB, LB>;
@@ -238,19 +238,31 @@ int launch_fuse(dcdg_ctx* ctx, const void* xl, const float* s2, int S, int C, in
 
 int launch_post_eq(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, double n0, double ex, int fmt, float* s2,
                    cudaStream_t st) {
-  const size_t smem = 4 * 2 * static_cast<size_t>(U) * U * sizeof(float2);
+  const size_t smem = 4 * static_cast<size_t>(dcdg::pev_smem_per_warp(U));
   const int blocks = (P + 3) / 4;
   const float gam = static_cast<float>(ex / n0);
   const float exu = static_cast<float>(ex / U);
-  if (fmt == DCDG_FP16) {
-    auto k = dcdg::post_eq_var<__half2>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k<<<blocks, 128, smem, st>>>(static_cast<const __half2*>(H), P, Bc, U, gam, exu, true, s2, ctx->d_status);
-  } else {
-    auto k = dcdg::post_eq_var<float2>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k<<<blocks, 128, smem, st>>>(static_cast<const float2*>(H), P, Bc, U, gam, exu, false, s2, ctx->d_status);
+#define PEV_LAUNCH(T, UT, BT)                                                                                \
+  {                                                                                                         \
+    auto k = dcdg::post_eq_var<T, UT, BT>;                                                                  \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));           \
+    k<<<blocks, 128, smem, st>>>(static_cast<const T*>(H), P, Bc, U, gam, exu, fmt == DCDG_FP16, s2, ctx->d_status); \
   }
+#define PEV_DISPATCH(T)                                  \
+  if (U == 16 && Bc == 32) PEV_LAUNCH(T, 16, 32)         \
+  else if (U == 8 && Bc == 32) PEV_LAUNCH(T, 8, 32)      \
+  else switch (U) {                                      \
+    case 8: PEV_LAUNCH(T, 8, 0) break;                   \
+    case 16: PEV_LAUNCH(T, 16, 0) break;                 \
+    case 32: PEV_LAUNCH(T, 32, 0) break;                 \
+    default: PEV_LAUNCH(T, 0, 0) break;                  \
+  }
+  if (fmt == DCDG_FP16)
+    PEV_DISPATCH(__half2)
+  else
+    PEV_DISPATCH(float2)
+#undef PEV_DISPATCH
+#undef PEV_LAUNCH
   ++ctx->launches;
   CUDA_TRY(cudaGetLastError(), "post_eq_variance launch");
   return DCDG_OK;

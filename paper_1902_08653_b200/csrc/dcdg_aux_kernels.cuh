@@ -154,36 +154,101 @@ __global__ void __launch_bounds__(128)
 // A = I + (Ex/N0) H^H H (Gram, detect.cpp:21-28,118-121); Cholesky A = L L^H
 // (numerics.cpp:45-58); sigma^2 = (Ex/U) tr(A^-1) = (Ex/U) ||L^-1||_F^2
 // (the reference sums U Cholesky solves, detect.cpp:122-129).
-// Shared memory per warp: A/L [U][U] + Z [U][U] complex fp32 (U <= 32).
+// The Gram is computed from row chunks of the tile staged in shared memory
+// (column stride PR+1 complex: conflict-free), each lane accumulating a 4x2
+// block of entries with packed FFMA2 (rows broadcast, columns pre-swapped).
+// Shared memory per warp: staged chunk [U][PR+1] + A/L [U][U] + Z [U][U]
+// complex fp32 (U <= 32).
 // ===========================================================================
-template <typename T>
-__global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int P, int BC, int U, float gam,
+constexpr int kPevRows = 32;  // rows staged per chunk
+
+__host__ __device__ constexpr int pev_smem_per_warp(int U) {
+  return (U * (kPevRows + 1) + 2 * U * U) * 8;
+}
+
+// UT > 0: U == UT at compile time (register-resident Cholesky/inverse);
+// BT > 0: B_c == BT at compile time (vectorised staging, unrolled Gram).
+template <typename T, int UT, int BT>
+__global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int P, int BC_, int U_, float gam,
                                                    float ex_over_u, bool round_fp16, float* __restrict__ sigma2,
                                                    unsigned long long* __restrict__ status) {
   extern __shared__ float2 vsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long p = static_cast<long long>(blockIdx.x) * 4 + warp;
   if (p >= P) return;
-  float2* A = vsm + warp * (2 * U * U);  // column-major, lower triangle used
+  const int BC = BT > 0 ? BT : BC_;
+  const int U = UT > 0 ? UT : U_;
+  constexpr int PR = kPevRows;
+  float2* Hs = vsm + warp * (U * (PR + 1) + 2 * U * U);  // staged rows, column-major, stride PR+1
+  float2* A = Hs + U * (PR + 1);                          // column-major, lower triangle used
   float2* Z = A + U * U;
   const T* h = H + static_cast<size_t>(p) * BC * U;
-  const int ntri = U * (U + 1) / 2;
-  for (int e = lane; e < ntri; e += 32) {
-    // e -> (i >= j): column j, row i
-    int j = 0, rem = e;
-    while (rem >= U - j) {
-      rem -= U - j;
-      ++j;
+  // 4x2 entry blocks: block id = lane + 32t, (ib, jb) = (id / njb, id % njb)
+  const int nib = (U + 3) / 4, njb = (U + 1) / 2, nblk = nib * njb;
+  float2 acc[4][4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) acc[t][r][0] = acc[t][r][1] = make_float2(0.f, 0.f);
+  for (int b0 = 0; b0 < BC; b0 += PR) {
+    const int rows = min(PR, BC - b0);
+    if (BT == PR && sizeof(T) == 8) {
+      // whole fp32 tile in one chunk: 16-B loads, two rows per load
+      const float4* t4 = reinterpret_cast<const float4*>(h);
+#pragma unroll
+      for (int i = 0; i < (BT > 0 ? BT * (UT > 0 ? UT : 1) / 64 : 1); ++i) {
+        const int idx = lane + 32 * i;
+        const int j = idx / (PR / 2), rr = idx - j * (PR / 2);
+        const float4 v = __ldg(t4 + idx);
+        Hs[j * (PR + 1) + 2 * rr] = make_float2(v.x, v.y);
+        Hs[j * (PR + 1) + 2 * rr + 1] = make_float2(v.z, v.w);
+      }
+    } else {
+      for (int idx = lane; idx < rows * U; idx += 32) {
+        const int j = idx / rows, b = idx - j * rows;
+        Hs[j * (PR + 1) + b] = ldv(h + static_cast<size_t>(j) * BC, b0 + b);
+      }
     }
-    const int i = j + rem;
-    float gr = 0.f, gi = 0.f;  // conj(h_i)^T h_j
-    for (int b = 0; b < BC; ++b) {
-      const float2 a = ldv(h + static_cast<size_t>(i) * BC, b);
-      const float2 c = ldv(h + static_cast<size_t>(j) * BC, b);
-      gr = fmaf(a.x, c.x, fmaf(a.y, c.y, gr));
-      gi = fmaf(a.x, c.y, fmaf(-a.y, c.x, gi));
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int id = lane + 32 * t;
+      if (id < nblk) {
+        const int i0 = 4 * (id / njb), j0 = 2 * (id % njb);
+#pragma unroll 8
+        for (int b = 0; b < (BT == PR ? PR : rows); ++b) {
+          float2 a[4], c[2], cs[2];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) a[r] = (i0 + r < U) ? Hs[(i0 + r) * (PR + 1) + b] : make_float2(0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            c[q] = (j0 + q < U) ? Hs[(j0 + q) * (PR + 1) + b] : make_float2(0.f, 0.f);
+            cs[q] = make_float2(c[q].y, -c[q].x);
+          }
+          // conj(a) c = a.x (c.x, c.y) + a.y (c.y, -c.x)
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) acc[t][r][q] = ffma2(a[r].y, cs[q], ffma2(a[r].x, c[q], acc[t][r][q]));
+        }
+      }
     }
-    A[j * U + i] = make_float2((i == j ? 1.f : 0.f) + gam * gr, gam * gi);
+    __syncwarp();
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int id = lane + 32 * t;
+    if (id < nblk) {
+      const int i0 = 4 * (id / njb), j0 = 2 * (id % njb);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int i = i0 + r, j = j0 + q;
+          if (i < U && j < U && i >= j)
+            A[j * U + i] = make_float2((i == j ? 1.f : 0.f) + gam * acc[t][r][q].x, gam * acc[t][r][q].y);
+        }
+    }
   }
   __syncwarp();
   float maxdiag = 0.f;  // numerics.cpp:38-41 (pivot floor 1e-14 * max |A_jj|)
@@ -192,6 +257,64 @@ __global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int 
   for (int o = 16; o > 0; o >>= 1) maxdiag = fmaxf(maxdiag, __shfl_xor_sync(0xffffffffu, maxdiag, o));
   const float floor_ = 1e-14f * maxdiag;
   bool singular = false;
+  float tr = 0.f;
+  if (UT > 0) {
+    // Register-resident path (U == UT): lane i holds row i of A and of L;
+    // finished rows of L are published row-major in Z for broadcast reads.
+    constexpr int N = UT > 0 ? UT : 1;
+    float2 a[N], l[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      a[k] = (lane < N && k <= lane) ? A[k * N + lane] : make_float2(0.f, 0.f);
+      l[k] = make_float2(0.f, 0.f);
+    }
+    float2* Lr = Z;  // row-major L
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      if (lane == j) {  // d_j = A_jj - sum_k |L_jk|^2 ; L_jj = sqrt(d_j)   (numerics.cpp:47-52)
+        float d = a[j].x;
+#pragma unroll
+        for (int k = 0; k < j; ++k) d -= l[k].x * l[k].x + l[k].y * l[k].y;
+        if (!(d > floor_)) singular = true;
+        l[j] = make_float2(__fsqrt_rn(fmaxf(d, 1e-30f)), 0.f);
+#pragma unroll
+        for (int k = 0; k <= j; ++k) Lr[j * N + k] = l[k];
+      }
+      __syncwarp();
+      if (lane > j && lane < N) {  // L_ij = (A_ij - sum_{k<j} L_ik conj(L_jk)) / L_jj   (numerics.cpp:53-56)
+        float sr = a[j].x, si = a[j].y;
+#pragma unroll
+        for (int k = 0; k < j; ++k) {
+          const float2 b = Lr[j * N + k];
+          sr -= l[k].x * b.x + l[k].y * b.y;
+          si -= l[k].y * b.x - l[k].x * b.y;
+        }
+        const float inv = __frcp_rn(Lr[j * N + j].x);
+        l[j] = make_float2(sr * inv, si * inv);
+      }
+    }
+    __syncwarp();
+    // X = L^{-1}: lane c holds column c; row i: X_ic = -(sum_{k=c}^{i-1} L_ik X_kc) / L_ii
+    float2 x[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const float linv = __frcp_rn(Lr[i * N + i].x);
+      float sr = 0.f, si = 0.f;
+#pragma unroll
+      for (int k = 0; k < i; ++k) {
+        const float2 lk = Lr[i * N + k];
+        const float2 xk = x[k];  // zero above the diagonal (k < c)
+        sr += lk.x * xk.x - lk.y * xk.y;
+        si += lk.x * xk.y + lk.y * xk.x;
+      }
+      float2 xi;
+      if (lane == i) xi = make_float2(linv, 0.f);
+      else if (lane < i) xi = make_float2(-sr * linv, -si * linv);
+      else xi = make_float2(0.f, 0.f);
+      x[i] = xi;
+      tr = fmaf(xi.x, xi.x, fmaf(xi.y, xi.y, tr));
+    }
+  } else {
   // left-looking Cholesky, lanes parallel over rows i >= j
   for (int j = 0; j < U; ++j) {
     float d = A[j * U + j].x;
@@ -215,7 +338,6 @@ __global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int 
     __syncwarp();
   }
   // columns of L^-1: lane c solves L z = e_c (rows i >= c)
-  float tr = 0.f;
   for (int c = lane; c < U; c += 32) {
     for (int i = c; i < U; ++i) {
       float sr = (i == c) ? 1.f : 0.f, si = 0.f;
@@ -229,6 +351,7 @@ __global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int 
       Z[c * U + i] = z;
       tr = fmaf(z.x, z.x, fmaf(z.y, z.y, tr));
     }
+  }
   }
   tr = warp_sum(tr);
   if (lane == 0) {

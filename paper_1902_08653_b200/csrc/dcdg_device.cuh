@@ -113,7 +113,18 @@ __device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y
 // Build the planar register pair (a, b) once: x + (+0.0) is not an identity
 // under IEEE (it maps -0 to +0), so ptxas keeps the FADD2 result instead of
 // re-pairing the source registers with MOVs before every later use.
-__device__ __forceinline__ float2 pair(float a, float b) { return __fadd2_rn(make_float2(a, b), make_float2(0.f, 0.f)); }
+#ifndef DCDG_PAIR_MODE
+#define DCDG_PAIR_MODE 0
+#endif
+__device__ __forceinline__ float2 pair(float a, float b) {
+#if DCDG_PAIR_MODE == 1
+  // (a, b) = a*(1,0) + b*(0,1) with broadcast operands: 2 packed ops, no MOVs
+  return __ffma2_rn(make_float2(b, b), make_float2(0.f, 1.f), __fmul2_rn(make_float2(a, a), make_float2(1.f, 0.f)));
+#else
+  // x + (+0.0) is not an IEEE identity (-0 -> +0), so ptxas keeps the result
+  return __fadd2_rn(make_float2(a, b), make_float2(0.f, 0.f));
+#endif
+}
 __device__ __forceinline__ float hsum(float2 a) { return a.x + a.y; }
 __device__ __forceinline__ float2 shfl_xor2(float2 v, int o) {
   return make_float2(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));

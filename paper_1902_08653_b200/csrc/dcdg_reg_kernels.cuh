@@ -123,7 +123,8 @@ template <int BC, int U, int G, int W, int MINB, int LB>
 __global__ void __launch_bounds__(32 * W, MINB)
     ul_reg_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
                float2* __restrict__ X) {
-  static_assert(32 % G == 0 && BC % (2 * G) == 0 && U % LB == 0 && (U * LB) % G == 0, "shape");
+  static_assert(32 % G == 0 && BC % (2 * G) == 0 && U % LB == 0 && U % G == 0 && (2 * (U / LB) * (LB * (LB - 1) / 2)) % G == 0,
+                "shape");
   constexpr int NPW = 32 / G, R = BC / G, NP = R / 2;
   constexpr int T = LB * (LB - 1) / 2;  // Gram entries per block
   constexpr int TILE_B = BC * U * 8, Y_B = BC * 8, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
@@ -175,9 +176,10 @@ __global__ void __launch_bounds__(32 * W, MINB)
     __syncwarp();
     if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
 
-    // ---- per-problem scalars: ||h_j||^2 (detect.cpp:86-90) and block Grams
+    // ---- per-problem scalars: ||h_j||^2 (detect.cpp:86-90) and block Grams,
+    // each reduce-scattered over the group (lane k keeps a contiguous slice)
     {
-      float v[U * LB];
+      float v[U];
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         float2 e = fmul2(hr[j][0], hr[j][0]);
@@ -186,6 +188,16 @@ __global__ void __launch_bounds__(32 * W, MINB)
         for (int c = 1; c < NP; ++c) e = ffma2(hi[j][c], hi[j][c], ffma2(hr[j][c], hr[j][c], e));
         v[j] = hsum(e);
       }
+      group_reduce_scatter<G>(v, k);
+#pragma unroll
+      for (int i = 0; i < U / G; ++i) {
+        const float m = __fdividef(1.f, v[i] + kappa);            // m_j = 1/(||h_j||^2 + N0/Ex)
+        mnx[k * (U / G) + i] = make_float4(m, m * v[i], 0.f, 0.f);  // n_j = m_j ||h_j||^2, x_j = 0
+      }
+    }
+    {
+      constexpr int NG = 2 * (U / LB) * T;  // floats of the block Grams
+      float v[NG];
 #pragma unroll
       for (int q = 0; q < U / LB; ++q)
 #pragma unroll
@@ -199,27 +211,20 @@ __global__ void __launch_bounds__(32 * W, MINB)
               gr = ffma2(hi[ja][c], hi[jb][c], ffma2(hr[ja][c], hr[jb][c], gr));
               gi = ffma2(neg2(hi[ja][c]), hr[jb][c], ffma2(hr[ja][c], hi[jb][c], gi));
             }
-            v[U + 2 * e] = hsum(gr);
-            v[U + 2 * e + 1] = hsum(gi);
+            v[2 * e] = hsum(gr);
+            v[2 * e + 1] = hsum(gi);
           }
       group_reduce_scatter<G>(v, k);
-      constexpr int PER = U * LB / G;
       float* gf = reinterpret_cast<float*>(gb);
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int idx = k * PER + i;
-        if (idx < U) {
-          const float m = __fdividef(1.f, v[i] + kappa);  // m_j = 1/(||h_j||^2 + N0/Ex)
-          mnx[idx] = make_float4(m, m * v[i], 0.f, 0.f);  // n_j = m_j ||h_j||^2, x_j = 0
+      for (int i = 0; i < NG / G; ++i) {
+        const int gi = k * (NG / G) + i, e = gi >> 1;
+        if (gi & 1) {  // stored as (Re G, Im G, -Im G, Re G)
+          gf[e * 4 + 1] = v[i];
+          gf[e * 4 + 2] = -v[i];
         } else {
-          const int gi = idx - U, e = gi >> 1;
-          if (gi & 1) {
-            gf[e * 4 + 1] = v[i];
-            gf[e * 4 + 2] = -v[i];
-          } else {
-            gf[e * 4 + 0] = v[i];
-            gf[e * 4 + 3] = v[i];
-          }
+          gf[e * 4 + 0] = v[i];
+          gf[e * 4 + 3] = v[i];
         }
       }
     }

@@ -23,6 +23,8 @@ if fmt == "fp16":
 for _ in range(reps):
     if direction == "ul":
         eng.ul_detect(H, y, n0=n0, K=3, fusion="uniform", want_xhat=False)
+    elif direction == "pev":
+        eng.post_eq_variance(H, n0=n0)
     else:
         eng.dl_precode(H, x, rho=math.sqrt(16), K=3, want_gain=False)
 eng.sync()
