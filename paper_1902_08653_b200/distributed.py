@@ -158,7 +158,7 @@ class DistributedCD:
         if p.world == 1:
             xl, s2 = self.compute.ul_local(H, y, n0=n0, ex=ex, K=K, fusion=fusion)
             out = self.compute.fuse(xl, s2, fusion=fusion, C_total=p.C_total)
-            return (out, None) if async_op else out
+            return _Deferred(None, lambda: out) if async_op else out
         if self.mode == "gather" and p.world <= p.C_total:
             return self._uplink_gather(H, y, n0=n0, ex=ex, K=K, fusion=fusion, async_op=async_op)
         part_sum, wsum, _, _ = self.compute.ul_partial(H, y, n0=n0, ex=ex, K=K, fusion=fusion, C_total=p.C_total,
@@ -202,7 +202,7 @@ class DistributedCD:
             dist.all_to_all_single(srecv.reshape(-1), ssend.reshape(-1))
             sig = srecv.reshape(p.world, chunk, p.C_local).transpose(0, 1).reshape(chunk, p.C_total).contiguous()
         out = self.compute.fuse(recv, sig, fusion=fusion, C_total=p.C_total)
-        return (out, None) if async_op else out
+        return _Deferred(None, lambda: out) if async_op else out
 
     # ---- downlink ---------------------------------------------------------
     def broadcast_symbols(self, s_root, *, src=0):

@@ -88,3 +88,20 @@ def test_distributed_driver_single_gpu(engine, port):
     got = dcd.uplink(to_dev(b["h_tiles"]), to_dev(b["y"]), n0=b["n0"], K=3)
     engine.sync()
     assert rel_err(to_host(got), xhat) <= TOL_FP32
+
+
+def test_graphed_uplink_replays_with_new_inputs(engine, port):
+    from paper_1902_08653_b200 import GraphedUplink
+    b1 = batch(8, 32, 16, S=24, seed=31)
+    b2 = batch(8, 32, 16, S=24, seed=32)
+    H, y = to_dev(b1["h_tiles"]), to_dev(b1["y"])
+    g = GraphedUplink(engine, H, y, n0=b1["n0"], K=3)
+    x1 = to_host(g.replay().clone())
+    H.copy_(to_dev(b2["h_tiles"]))
+    y.copy_(to_dev(b2["y"]))
+    torch.cuda.synchronize()
+    x2 = to_host(g.replay().clone())
+    engine.sync()
+    for b, x in ((b1, x1), (b2, x2)):
+        ref, _, _ = port.ul_detect_batch(b["h_tiles"], b["y"], b["n0"], 1.0, 3, UNIFORM)
+        assert rel_err(x, ref) <= TOL_FP32
