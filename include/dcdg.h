@@ -154,6 +154,33 @@ long long dcdg_last_error_problem(void);
 /* Number of kernel launches issued through this context (for bench.py). */
 uint64_t dcdg_launch_count(dcdg_ctx* ctx);
 
+/* ---- hard decisions and BER --------------------------------- */
+/* Full-H MMSE bias factors of S subcarriers whose C cluster tiles are local
+ * (mmse_bias_factors, detect.cpp:227-242): beta [S][U] fp32,
+ * beta_u = 1 - kappa [(H^H H + kappa I)^-1]_uu, H the stacked C*B_c x U
+ * channel, kappa = N0/E_x (kappa == 0 gives 1).  U <= 32. */
+int dcdg_mmse_bias(dcdg_ctx* ctx, const void* H, int S, int C, int Bc, int U, double n0, double ex,
+                   int fmt, float* beta, void* stream);
+
+/* labels[i] = Constellation::slice(x[i] / beta[i]) (mimo.cpp:111-122; beta
+ * may be NULL): nearest Gray QAM point (qam 4/16/64, energy ex) computed in
+ * fp64, distance ties to the lowest label. */
+int dcdg_slice(dcdg_ctx* ctx, const void* x, int fmt, const float* beta, int64_t n, int qam,
+               double ex, uint8_t* labels, void* stream);
+
+/* *errors += number of bits where labels differ from `bits` (log2(qam) bits
+ * per symbol, MSB first, one byte per bit as dcd::make_batch stores them). */
+int dcdg_bit_errors(dcdg_ctx* ctx, const uint8_t* labels, const uint8_t* bits, int64_t n, int qam,
+                    unsigned long long* errors, void* stream);
+
+/* Downlink receive (downlink_receive_and_ber, precode.cpp:204-233) with every
+ * cluster local: y0 = sum_c H_dl,c x_c, beta[s] = Re(s^H y0)/||s||^2,
+ * labels of (y0 + noise)/beta (noise [S][U] complex fp32 or NULL);
+ * flagged[s] = 1 (labels 0xff) when beta <= 0 or non-finite. */
+int dcdg_dl_receive(dcdg_ctx* ctx, const void* H, const void* x_dl, const void* s,
+                    const float* noise, int S, int C, int Bc, int U, int fmt, int qam, double ex,
+                    uint8_t* labels, float* beta, uint8_t* flagged, void* stream);
+
 /* In-place round of n fp32 values to the nearest binary16 (RNE), widened
  * back: the wire-format rounding of PrecisionScope::messages_only
  * (precision.cpp:43-72, detect.cpp:170-173, precode.cpp:159-160). */

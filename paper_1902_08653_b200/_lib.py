@@ -65,6 +65,12 @@ SIGNATURES = {
     "dcdg_sync_status": (C.c_int, [_vp, _vp]),
     "dcdg_launch_count": (C.c_uint64, [_vp]),
     "dcdg_round_fp16": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
+    "dcdg_mmse_bias": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _vp,
+                                 _vp]),
+    "dcdg_slice": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int64, C.c_int, C.c_double, _vp, _vp]),
+    "dcdg_bit_errors": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int, _vp, _vp]),
+    "dcdg_dl_receive": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.c_double, _vp, _vp, _vp, _vp]),
     "dcdg_convert": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, C.c_int64, _vp]),
     "dcdg_kernel_name": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int]),
 }

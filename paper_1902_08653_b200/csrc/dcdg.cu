@@ -236,36 +236,44 @@ int launch_fuse(dcdg_ctx* ctx, const void* xl, const float* s2, int S, int C, in
   return DCDG_OK;
 }
 
-int launch_post_eq(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, double n0, double ex, int fmt, float* s2,
-                   cudaStream_t st) {
+// Gram/Cholesky kernels: post_eq_variance (mode kPev, one tile per problem) and
+// the full-H MMSE bias factors (mode kBias, the NT cluster tiles of a subcarrier).
+template <int MODE>
+int launch_gram_chol(dcdg_ctx* ctx, const void* H, int P, int NT, int Bc, int U, float a0, float a1, float scale,
+                     int fmt, float* out, cudaStream_t st) {
   const size_t smem = 4 * static_cast<size_t>(dcdg::pev_smem_per_warp(U));
   const int blocks = (P + 3) / 4;
-  const float gam = static_cast<float>(ex / n0);
-  const float exu = static_cast<float>(ex / U);
-#define PEV_LAUNCH(T, UT, BT)                                                                                \
+#define GC_LAUNCH(T, UT, BT)                                                                                \
   {                                                                                                         \
-    auto k = dcdg::post_eq_var<T, UT, BT>;                                                                  \
+    auto k = dcdg::gram_chol<T, UT, BT, MODE>;                                                              \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));           \
-    k<<<blocks, 128, smem, st>>>(static_cast<const T*>(H), P, Bc, U, gam, exu, fmt == DCDG_FP16, s2, ctx->d_status); \
+    k<<<blocks, 128, smem, st>>>(static_cast<const T*>(H), P, NT, Bc, U, a0, a1, scale,                     \
+                                 MODE == dcdg::kPev && fmt == DCDG_FP16, out, ctx->d_status);               \
   }
-#define PEV_DISPATCH(T)                                  \
-  if (U == 16 && Bc == 32) PEV_LAUNCH(T, 16, 32)         \
-  else if (U == 8 && Bc == 32) PEV_LAUNCH(T, 8, 32)      \
-  else switch (U) {                                      \
-    case 8: PEV_LAUNCH(T, 8, 0) break;                   \
-    case 16: PEV_LAUNCH(T, 16, 0) break;                 \
-    case 32: PEV_LAUNCH(T, 32, 0) break;                 \
-    default: PEV_LAUNCH(T, 0, 0) break;                  \
+#define GC_DISPATCH(T)                            \
+  if (U == 16 && Bc == 32) GC_LAUNCH(T, 16, 32)   \
+  else if (U == 8 && Bc == 32) GC_LAUNCH(T, 8, 32) \
+  else switch (U) {                               \
+    case 8: GC_LAUNCH(T, 8, 0) break;             \
+    case 16: GC_LAUNCH(T, 16, 0) break;           \
+    case 32: GC_LAUNCH(T, 32, 0) break;           \
+    default: GC_LAUNCH(T, 0, 0) break;            \
   }
   if (fmt == DCDG_FP16)
-    PEV_DISPATCH(__half2)
+    GC_DISPATCH(__half2)
   else
-    PEV_DISPATCH(float2)
-#undef PEV_DISPATCH
-#undef PEV_LAUNCH
+    GC_DISPATCH(float2)
+#undef GC_DISPATCH
+#undef GC_LAUNCH
   ++ctx->launches;
-  CUDA_TRY(cudaGetLastError(), "post_eq_variance launch");
+  CUDA_TRY(cudaGetLastError(), "gram/cholesky launch");
   return DCDG_OK;
+}
+
+int launch_post_eq(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, double n0, double ex, int fmt, float* s2,
+                   cudaStream_t st) {
+  return launch_gram_chol<dcdg::kPev>(ctx, H, P, 1, Bc, U, 1.f, static_cast<float>(ex / n0),
+                                      static_cast<float>(ex / U), fmt, s2, st);
 }
 
 }  // namespace
@@ -567,6 +575,94 @@ int dcdg_fusion_weights(dcdg_ctx* ctx, const float* sigma2, int S, int C, float*
   dcdg::fusion_weights_kernel<<<(S + 127) / 128, 128, 0, as_stream(stream)>>>(sigma2, S, C, w, ctx->d_status);
   ++ctx->launches;
   CUDA_TRY(cudaGetLastError(), "fusion_weights launch");
+  return DCDG_OK;
+}
+
+namespace {
+int check_qam(int qam, double ex) {
+  if (qam != 4 && qam != 16 && qam != 64) return fail(DCDG_EINVAL, "Constellation::qam: order must be 4, 16 or 64");
+  if (!(ex > 0.0)) return fail(DCDG_EINVAL, "Constellation::qam: symbol energy must be positive");
+  return DCDG_OK;
+}
+int bps_of(int qam) { return qam == 4 ? 2 : qam == 16 ? 4 : 6; }
+}  // namespace
+
+int dcdg_mmse_bias(dcdg_ctx* ctx, const void* H, int S, int C, int Bc, int U, double n0, double ex, int fmt,
+                   float* beta, void* stream) {
+  if (int rc = check_fmt(fmt)) return rc;
+  if (C <= 0 || Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "detector: empty channel matrix");
+  if (n0 < 0.0 || !(ex > 0.0)) return fail(DCDG_EINVAL, "detector: need N0 >= 0 and E_x > 0");
+  if (U > 32) return fail(DCDG_EINVAL, "dcdg_mmse_bias: U > 32 not supported");
+  if (fmt == DCDG_FP16 && (Bc & 1))
+    return fail(DCDG_EINVAL, "dcdg: fp16 row-pair planar tiles need an even antenna count B_c");
+  if (int rc = check_ctx(ctx)) return rc;
+  if (S <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = as_stream(stream);
+  const double kappa = n0 / ex;
+  if (kappa == 0.0) {  // detect.cpp:232: no shrinkage
+    const long long n = static_cast<long long>(S) * U;
+    dcdg::fill_kernel<<<static_cast<int>(std::min<long long>((n + 255) / 256, 2368)), 256, 0, st>>>(beta, n, 1.f);
+    ++ctx->launches;
+    CUDA_TRY(cudaGetLastError(), "fill launch");
+    return DCDG_OK;
+  }
+  return launch_gram_chol<dcdg::kBias>(ctx, H, S, C, Bc, U, static_cast<float>(kappa), 1.f, 0.f, fmt, beta, st);
+}
+
+int dcdg_slice(dcdg_ctx* ctx, const void* x, int fmt, const float* beta, int64_t n, int qam, double ex,
+               uint8_t* labels, void* stream) {
+  if (int rc = check_fmt(fmt)) return rc;
+  if (int rc = check_qam(qam, ex)) return rc;
+  if (int rc = check_ctx(ctx)) return rc;
+  if (n <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
+  if (fmt == DCDG_FP16)
+    dcdg::slice_kernel<__half2><<<blocks, 256, 0, as_stream(stream)>>>(static_cast<const __half2*>(x), beta, n, qam,
+                                                                       ex, labels);
+  else
+    dcdg::slice_kernel<float2><<<blocks, 256, 0, as_stream(stream)>>>(static_cast<const float2*>(x), beta, n, qam, ex,
+                                                                      labels);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "slice launch");
+  return DCDG_OK;
+}
+
+int dcdg_bit_errors(dcdg_ctx* ctx, const uint8_t* labels, const uint8_t* bits, int64_t n, int qam,
+                    unsigned long long* errors, void* stream) {
+  if (int rc = check_qam(qam, 1.0)) return rc;
+  if (int rc = check_ctx(ctx)) return rc;
+  if (n <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
+  dcdg::bit_errors_kernel<<<blocks, 256, 0, as_stream(stream)>>>(labels, bits, n, bps_of(qam), errors);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "bit_errors launch");
+  return DCDG_OK;
+}
+
+int dcdg_dl_receive(dcdg_ctx* ctx, const void* H, const void* x_dl, const void* s, const float* noise, int S, int C,
+                    int Bc, int U, int fmt, int qam, double ex, uint8_t* labels, float* beta, uint8_t* flagged,
+                    void* stream) {
+  if (int rc = check_fmt(fmt)) return rc;
+  if (int rc = check_qam(qam, ex)) return rc;
+  if (C <= 0 || Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "precoder: empty channel matrix");
+  if (U > 32) return fail(DCDG_EINVAL, "dcdg_dl_receive: U > 32 not supported");
+  if (int rc = check_ctx(ctx)) return rc;
+  if (S <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int blocks = (S + 3) / 4;
+  if (fmt == DCDG_FP16)
+    dcdg::dl_receive_kernel<__half2><<<blocks, 128, 0, as_stream(stream)>>>(
+        static_cast<const __half2*>(H), static_cast<const __half2*>(x_dl), static_cast<const __half2*>(s),
+        reinterpret_cast<const float2*>(noise), S, C, Bc, U, qam, ex, labels, beta, flagged);
+  else
+    dcdg::dl_receive_kernel<float2><<<blocks, 128, 0, as_stream(stream)>>>(
+        static_cast<const float2*>(H), static_cast<const float2*>(x_dl), static_cast<const float2*>(s),
+        reinterpret_cast<const float2*>(noise), S, C, Bc, U, qam, ex, labels, beta, flagged);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "dl_receive launch");
   return DCDG_OK;
 }
 

@@ -166,12 +166,20 @@ __host__ __device__ constexpr int pev_smem_per_warp(int U) {
   return (U * (kPevRows + 1) + 2 * U * U) * 8;
 }
 
+// One warp per problem; MODE selects what the Gram/Cholesky serves:
+//   kPev  (post_eq_variance, detect.cpp:112-130): one tile per problem,
+//         A = I + gam*G, out[p] = scale * tr(A^-1);
+//   kBias (mmse_bias_factors, detect.cpp:227-242): the NT = C cluster tiles of a
+//         subcarrier stacked (full-H Gram), A = kappa*I + G,
+//         out[p*U + u] = 1 - kappa * [A^-1]_uu.
 // UT > 0: U == UT at compile time (register-resident Cholesky/inverse);
 // BT > 0: B_c == BT at compile time (vectorised staging, unrolled Gram).
-template <typename T, int UT, int BT>
-__global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int P, int BC_, int U_, float gam,
-                                                   float ex_over_u, bool round_fp16, float* __restrict__ sigma2,
-                                                   unsigned long long* __restrict__ status) {
+enum GramMode { kPev = 0, kBias = 1 };
+
+template <typename T, int UT, int BT, int MODE>
+__global__ void __launch_bounds__(128) gram_chol(const T* __restrict__ H, int P, int NT, int BC_, int U_, float a0,
+                                                 float a1, float scale, bool round_fp16, float* __restrict__ out,
+                                                 unsigned long long* __restrict__ status) {
   extern __shared__ float2 vsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long p = static_cast<long long>(blockIdx.x) * 4 + warp;
@@ -182,7 +190,6 @@ __global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int 
   float2* Hs = vsm + warp * (U * (PR + 1) + 2 * U * U);  // staged rows, column-major, stride PR+1
   float2* A = Hs + U * (PR + 1);                          // column-major, lower triangle used
   float2* Z = A + U * U;
-  const T* h = H + static_cast<size_t>(p) * BC * U;
   // 4x2 entry blocks: block id = lane + 32t, (ib, jb) = (id / njb, id % njb)
   const int nib = (U + 3) / 4, njb = (U + 1) / 2, nblk = nib * njb;
   float2 acc[4][4][2];
@@ -190,6 +197,8 @@ __global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int 
   for (int t = 0; t < 4; ++t)
 #pragma unroll
     for (int r = 0; r < 4; ++r) acc[t][r][0] = acc[t][r][1] = make_float2(0.f, 0.f);
+  for (int tile = 0; tile < NT; ++tile) {
+  const T* h = H + (static_cast<size_t>(p) * NT + tile) * BC * U;
   for (int b0 = 0; b0 < BC; b0 += PR) {
     const int rows = min(PR, BC - b0);
     if (BT == PR && sizeof(T) == 8) {
@@ -235,6 +244,7 @@ __global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int 
     }
     __syncwarp();
   }
+  }  // tiles
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
     const int id = lane + 32 * t;
@@ -245,8 +255,8 @@ __global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int 
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int i = i0 + r, j = j0 + q;
-          if (i < U && j < U && i >= j)
-            A[j * U + i] = make_float2((i == j ? 1.f : 0.f) + gam * acc[t][r][q].x, gam * acc[t][r][q].y);
+          if (i < U && j < U && i >= j)  // A = a0 I + a1 G
+            A[j * U + i] = make_float2((i == j ? a0 : 0.f) + a1 * acc[t][r][q].x, a1 * acc[t][r][q].y);
         }
     }
   }
@@ -353,11 +363,16 @@ __global__ void __launch_bounds__(128) post_eq_var(const T* __restrict__ H, int 
     }
   }
   }
+  if (MODE == kBias) {  // lane u holds [A^-1]_uu = ||column u of L^-1||^2
+    if (lane < U) out[p * U + lane] = 1.f - a0 * tr;
+    if (lane == 0 && singular) record_status(status, p, ST_SINGULAR, 0);
+    return;
+  }
   tr = warp_sum(tr);
   if (lane == 0) {
-    float s2 = ex_over_u * tr;
+    float s2 = scale * tr;
     if (round_fp16) s2 = __half2float(__float2half_rn(s2));
-    sigma2[p] = s2;
+    out[p] = s2;
     if (singular) record_status(status, p, ST_SINGULAR, 0);
   }
 }
@@ -464,6 +479,136 @@ __global__ void fusion_weights_kernel(const float* __restrict__ s2, int S, int C
   }
   if (bad) record_status(status, s * C, ST_BAD_VARIANCE, 0);
   for (int c = 0; c < C; ++c) w[s * C + c] = (1.f / s2[s * C + c]) / total;
+}
+
+// ===========================================================================
+// Hard decisions (§8f): Gray square QAM exactly as Constellation::qam builds
+// it (mimo.cpp:64-109), nearest point by brute force in fp64 with the
+// reference's arithmetic and strict '<' so distance ties go to the lowest
+// label (Constellation::slice, mimo.cpp:111-122).
+// ===========================================================================
+struct Qam {
+  double level[8];  // level_of_label
+  int levels, axis_bits;
+};
+
+__device__ __forceinline__ Qam make_qam(unsigned order, double ex) {
+  Qam q;
+  q.levels = 2;
+  int bits = 2;
+  while (static_cast<unsigned>(q.levels * q.levels) < order) {
+    q.levels <<= 1;
+    bits += 2;
+  }
+  q.axis_bits = bits / 2;
+  const double scale = sqrt(__ddiv_rn(3.0 * ex, 2.0 * (q.levels * q.levels - 1.0)));
+  for (int pos = 0; pos < q.levels; ++pos)
+    q.level[pos ^ (pos >> 1)] = __dmul_rn(scale, 2.0 * pos - (q.levels - 1.0));
+  return q;
+}
+
+__device__ __forceinline__ unsigned slice_qam(const Qam& q, unsigned order, double yr, double yi) {
+  unsigned best = 0;
+  double best_d = 0.0;
+  for (unsigned i = 0; i < order; ++i) {
+    const double dr = __dsub_rn(yr, q.level[i >> q.axis_bits]);
+    const double di = __dsub_rn(yi, q.level[i & (q.levels - 1)]);
+    const double d = __dadd_rn(__dmul_rn(dr, dr), __dmul_rn(di, di));  // std::norm, no contraction
+    if (i == 0 || d < best_d) {
+      best_d = d;
+      best = i;
+    }
+  }
+  return best;
+}
+
+// labels[i] = slice(x[i] / beta[i])   (run_uplink_round's unbiasing, cluster.cpp:196-203)
+template <typename T>
+__global__ void slice_kernel(const T* __restrict__ x, const float* __restrict__ beta, long long n, unsigned order,
+                             double ex, uint8_t* __restrict__ labels) {
+  __shared__ Qam q;
+  if (threadIdx.x == 0) q = make_qam(order, ex);
+  __syncthreads();
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const float2 v = ldc(x, i);
+    double yr = v.x, yi = v.y;
+    if (beta) {
+      const double b = beta[i];
+      yr = __ddiv_rn(yr, b);
+      yi = __ddiv_rn(yi, b);
+    }
+    labels[i] = static_cast<uint8_t>(slice_qam(q, order, yr, yi));
+  }
+}
+
+// errors += popcount(label ^ label(bits)) with bits MSB-first per symbol
+// (demodulate_hard, mimo.cpp:141-150; BER tally cluster.cpp:203-206)
+__global__ void bit_errors_kernel(const uint8_t* __restrict__ labels, const uint8_t* __restrict__ bits, long long n,
+                                  int bps, unsigned long long* __restrict__ errors) {
+  unsigned long long e = 0;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    unsigned ref = 0;
+    for (int k = 0; k < bps; ++k) ref = (ref << 1) | (bits[i * bps + k] & 1u);
+    e += __popc(ref ^ labels[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  if ((threadIdx.x & 31) == 0 && e) atomicAdd(errors, e);
+}
+
+// Downlink receive (downlink_receive_and_ber, precode.cpp:204-233), one warp
+// per subcarrier with every cluster local: y0_u = sum_c h_{c,u}^H x_c,
+// beta = Re(s^H y0)/||s||^2, y = y0 + noise, labels of y/beta; flagged when
+// beta <= 0 or non-finite (the reference then counts half the bits wrong).
+template <typename T>
+__global__ void __launch_bounds__(128) dl_receive_kernel(const T* __restrict__ H, const T* __restrict__ X,
+                                                         const T* __restrict__ Sy, const float2* __restrict__ noise,
+                                                         int S, int C, int BC, int U, unsigned order, double ex,
+                                                         uint8_t* __restrict__ labels, float* __restrict__ beta_out,
+                                                         uint8_t* __restrict__ flagged) {
+  __shared__ Qam q;
+  if (threadIdx.x == 0) q = make_qam(order, ex);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long s = static_cast<long long>(blockIdx.x) * 4 + warp;
+  if (s >= S) return;
+  float yr = 0.f, yi = 0.f;  // lane u: y0_u
+  if (lane < U)
+    for (int c = 0; c < C; ++c) {
+      const T* h = H + ((static_cast<size_t>(s) * C + c) * U + lane) * BC;  // column u of tile c
+      const T* x = X + (static_cast<size_t>(s) * C + c) * BC;
+      for (int b = 0; b < BC; ++b) {
+        const float2 hv = ldv(h, b), xv = ldc(x, b);
+        yr = fmaf(hv.x, xv.x, fmaf(hv.y, xv.y, yr));
+        yi = fmaf(hv.x, xv.y, fmaf(-hv.y, xv.x, yi));
+      }
+    }
+  const float2 sv = lane < U ? ldc(Sy, static_cast<size_t>(s) * U + lane) : make_float2(0.f, 0.f);
+  const float se = warp_sum(sv.x * sv.x + sv.y * sv.y);
+  const float num = warp_sum(sv.x * yr + sv.y * yi);
+  const float b = se > 0.f ? num / se : 0.f;
+  const bool flag = !(b > 0.f) || !isfinite(b);
+  if (lane == 0) {
+    beta_out[s] = b;
+    flagged[s] = flag;
+  }
+  if (lane < U) {
+    if (noise) {
+      const float2 nv = noise[static_cast<size_t>(s) * U + lane];
+      yr += nv.x;
+      yi += nv.y;
+    }
+    labels[static_cast<size_t>(s) * U + lane] =
+        flag ? 0xff : static_cast<uint8_t>(slice_qam(q, order, __ddiv_rn(yr, b), __ddiv_rn(yi, b)));
+  }
+}
+
+__global__ void fill_kernel(float* __restrict__ x, long long n, float v) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    x[i] = v;
 }
 
 __global__ void round_fp16_kernel(float* __restrict__ x, long long n) {

@@ -240,6 +240,60 @@ class Engine:
         check(lib().dcdg_gain_reduce(self._ctx, _ptr(gain_part), _ptr(s), S, Cn, U, fmt, _ptr(g), self._stream(stream)))
         return g
 
+    # ------------------------------------------------------- hard decisions
+    def mmse_bias(self, H, *, n0: float, ex: float = 1.0, stream=None):
+        """Full-H MMSE bias factors beta [S, U] (mmse_bias_factors) of subcarriers
+        whose C cluster tiles H[s, :] are all on this GPU."""
+        fmt = _fmt_of(H)
+        S, Cn, U, Bc = _shape(H, fmt)
+        _need(H, "H")
+        beta = torch.empty((S, U), dtype=torch.float32, device=H.device)
+        check(lib().dcdg_mmse_bias(self._ctx, _ptr(H), S, Cn, Bc, U, float(n0), float(ex), fmt, _ptr(beta),
+                                   self._stream(stream)))
+        return beta
+
+    def slice(self, x, beta=None, *, qam: int = 16, ex: float = 1.0, stream=None):
+        """Gray-QAM labels of x / beta (Constellation::slice), uint8, x's shape."""
+        fmt = _fmt_of(x)
+        shp = _shape(x, fmt)
+        n = math.prod(shp)
+        labels = torch.empty(shp, dtype=torch.uint8, device=x.device)
+        if beta is not None and beta.numel() != n:
+            raise ValueError("beta must have one factor per symbol")
+        check(lib().dcdg_slice(self._ctx, _ptr(x), fmt, _ptr(beta), n, qam, float(ex), _ptr(labels),
+                               self._stream(stream)))
+        return labels
+
+    def bit_errors(self, labels, bits, *, qam: int = 16, stream=None) -> torch.Tensor:
+        """Device counter (int64 tensor of 1) of bit errors vs MSB-first bits."""
+        n = labels.numel()
+        errs = torch.zeros((1,), dtype=torch.int64, device=labels.device)
+        check(lib().dcdg_bit_errors(self._ctx, _ptr(labels.contiguous()), _ptr(bits.contiguous()), n, qam,
+                                    _ptr(errs), self._stream(stream)))
+        return errs
+
+    def dl_receive(self, H, x, s, noise=None, *, qam: int = 16, ex: float = 1.0, stream=None):
+        """(labels [S, U] uint8 (0xff where flagged), beta [S], flagged [S] bool)."""
+        fmt = _fmt_of(H)
+        S, Cn, U, Bc = _shape(H, fmt)
+        dev = H.device
+        labels = torch.empty((S, U), dtype=torch.uint8, device=dev)
+        beta = torch.empty((S,), dtype=torch.float32, device=dev)
+        flagged = torch.empty((S,), dtype=torch.uint8, device=dev)
+        check(lib().dcdg_dl_receive(self._ctx, _ptr(H), _ptr(x), _ptr(s), _ptr(noise), S, Cn, Bc, U, fmt, qam,
+                                    float(ex), _ptr(labels), _ptr(beta), _ptr(flagged), self._stream(stream)))
+        return labels, beta, flagged.bool()
+
+    def uplink_round(self, H, y, bits, *, n0: float, ex: float = 1.0, K: int = 3, fusion="uniform", qam: int = 16,
+                     stream=None):
+        """A device-resident run_uplink_round for the decentralized method
+        (src/cluster.cpp:160-206): detect + fuse, unbias with the full-H
+        factors, slice, count bit errors.  Returns (xhat, labels, errors)."""
+        r = self.ul_detect(H, y, n0=n0, ex=ex, K=K, fusion=fusion, want_local=False, stream=stream)
+        beta = self.mmse_bias(H, n0=n0, ex=ex, stream=stream) if n0 > 0 else None
+        labels = self.slice(r.xhat, beta, qam=qam, ex=ex, stream=stream)
+        return r.xhat, labels, self.bit_errors(labels, bits, qam=qam, stream=stream)
+
     def round_fp16(self, t, stream=None):
         """In-place binary16 rounding of an fp32/complex64 tensor (wire format)."""
         n = t.numel() * (2 if t.is_complex() else 1)
