@@ -307,7 +307,7 @@ template <int BC, int U, int G, int W, int MINB>
 __global__ void __launch_bounds__(32 * W, MINB)
     ul_reg_f16(const __half2* __restrict__ H, const __half2* __restrict__ Y, int P, int K, float kappa,
                __half2* __restrict__ X) {
-  static_assert(32 % G == 0 && BC % (4 * G) == 0 && U % 4 == 0 && (2 * U) % G == 0, "shape");
+  static_assert(32 % G == 0 && BC % (4 * G) == 0 && U % 4 == 0 && U % G == 0, "shape");
   constexpr int NPW = 32 / G, R = BC / G, CH = R / 4, NP = R / 2;
   constexpr int TILE_B = BC * U * 4, Y_B = BC * 4, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
   constexpr int SCAL_B = ul_scal_bytes(U);
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
     if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
 
     {
-      float v[2 * U];
+      float v[U];  // ||h_j||^2 (half2 partials, fp32 group sums)
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         __half2 acc = __hmul2(hre[j][0], hre[j][0]);
@@ -376,6 +376,17 @@ __global__ void __launch_bounds__(32 * W, MINB)
         const float2 f = __half22float2(acc);
         v[j] = f.x + f.y;
       }
+      group_reduce_scatter<G>(v, k);
+#pragma unroll
+      for (int i = 0; i < U / G; ++i) {
+        const float m = __fdividef(1.f, v[i] + kappa);
+        const int idx = k * (U / G) + i;
+        reinterpret_cast<float2*>(mng)[2 * idx] = make_float2(m, m * v[i]);
+        xs[idx] = make_float2(0.f, 0.f);
+      }
+    }
+    {
+      float v[U];  // pair Grams h_{2i+1}^H h_{2i}
 #pragma unroll
       for (int i = 0; i < U / 2; ++i) {
         __half2 gr = z2, gi = z2;
@@ -385,24 +396,15 @@ __global__ void __launch_bounds__(32 * W, MINB)
           gi = __hfma2(hre[2 * i + 1][q], him[2 * i][q], __hfma2(__hneg2(him[2 * i + 1][q]), hre[2 * i][q], gi));
         }
         const float2 fr = __half22float2(gr), fi = __half22float2(gi);
-        v[U + 2 * i] = fr.x + fr.y;
-        v[U + 2 * i + 1] = fi.x + fi.y;
+        v[2 * i] = fr.x + fr.y;
+        v[2 * i + 1] = fi.x + fi.y;
       }
       group_reduce_scatter<G>(v, k);
-      constexpr int PER = 2 * U / G;
       float* mf = reinterpret_cast<float*>(mng);
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int idx = k * PER + i;
-        if (idx < U) {
-          const float m = __fdividef(1.f, v[i] + kappa);
-          mf[idx * 4] = m;
-          mf[idx * 4 + 1] = m * v[i];
-          xs[idx] = make_float2(0.f, 0.f);
-        } else {
-          const int gi = idx - U;
-          mf[((gi >> 1) * 2 + 1) * 4 + 2 + (gi & 1)] = v[i];
-        }
+      for (int i = 0; i < U / G; ++i) {
+        const int gi = k * (U / G) + i;
+        mf[((gi >> 1) * 2 + 1) * 4 + 2 + (gi & 1)] = v[i];
       }
     }
     __syncwarp();
@@ -413,20 +415,15 @@ __global__ void __launch_bounds__(32 * W, MINB)
         const int j0 = 2 * jp, j1 = 2 * jp + 1;
         const float4 s0 = mng[j0], s1 = mng[j1];
         const float2 x0 = xs[j0], x1 = xs[j1];
-        __half2 a0 = z2, a1 = z2, b0 = z2, b1 = z2, c0 = z2, c1 = z2, e0 = z2, e1 = z2;
+        // folded accumulator chains: re = sum hr*r_re + hi*r_im, im = sum hr*r_im - hi*r_re
+        __half2 re0 = z2, im0 = z2, re1 = z2, im1 = z2;
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
-          a0 = __hfma2(hre[j0][q], rre[q], a0);
-          a1 = __hfma2(him[j0][q], rim[q], a1);
-          b0 = __hfma2(hre[j0][q], rim[q], b0);
-          b1 = __hfma2(him[j0][q], rre[q], b1);
-          c0 = __hfma2(hre[j1][q], rre[q], c0);
-          c1 = __hfma2(him[j1][q], rim[q], c1);
-          e0 = __hfma2(hre[j1][q], rim[q], e0);
-          e1 = __hfma2(him[j1][q], rre[q], e1);
+          re0 = __hfma2(him[j0][q], rim[q], __hfma2(hre[j0][q], rre[q], re0));
+          im0 = __hfma2(__hneg2(him[j0][q]), rre[q], __hfma2(hre[j0][q], rim[q], im0));
+          re1 = __hfma2(him[j1][q], rim[q], __hfma2(hre[j1][q], rre[q], re1));
+          im1 = __hfma2(__hneg2(him[j1][q]), rre[q], __hfma2(hre[j1][q], rim[q], im1));
         }
-        const __half2 re0 = __hadd2(a0, a1), im0 = __hsub2(b0, b1);
-        const __half2 re1 = __hadd2(c0, c1), im1 = __hsub2(e0, e1);
         __half2 d0 = __hadd2(__lows2half2(re0, im0), __highs2half2(re0, im0));
         __half2 d1 = __hadd2(__lows2half2(re1, im1), __highs2half2(re1, im1));
 #pragma unroll
@@ -834,20 +831,15 @@ __global__ void __launch_bounds__(32 * W, MINB)
       for (int jp = 0; jp < U / 2; ++jp) {
         const int j0 = 2 * jp, j1 = 2 * jp + 1;
         const float4 s0 = sg[j0], s1 = sg[j1];
-        __half2 a0 = z2, a1 = z2, b0 = z2, b1 = z2, c0 = z2, c1 = z2, e0 = z2, e1 = z2;
+        // folded accumulator chains: re = sum hr*r_re + hi*r_im, im = sum hr*r_im - hi*r_re
+        __half2 re0 = z2, im0 = z2, re1 = z2, im1 = z2;
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
-          a0 = __hfma2(hre[j0][q], xre[q], a0);
-          a1 = __hfma2(him[j0][q], xim[q], a1);
-          b0 = __hfma2(hre[j0][q], xim[q], b0);
-          b1 = __hfma2(him[j0][q], xre[q], b1);
-          c0 = __hfma2(hre[j1][q], xre[q], c0);
-          c1 = __hfma2(him[j1][q], xim[q], c1);
-          e0 = __hfma2(hre[j1][q], xim[q], e0);
-          e1 = __hfma2(him[j1][q], xre[q], e1);
+          re0 = __hfma2(him[j0][q], xim[q], __hfma2(hre[j0][q], xre[q], re0));
+          im0 = __hfma2(__hneg2(him[j0][q]), xre[q], __hfma2(hre[j0][q], xim[q], im0));
+          re1 = __hfma2(him[j1][q], xim[q], __hfma2(hre[j1][q], xre[q], re1));
+          im1 = __hfma2(__hneg2(him[j1][q]), xre[q], __hfma2(hre[j1][q], xim[q], im1));
         }
-        const __half2 re0 = __hadd2(a0, a1), im0 = __hsub2(b0, b1);
-        const __half2 re1 = __hadd2(c0, c1), im1 = __hsub2(e0, e1);
         __half2 d0 = __hadd2(__lows2half2(re0, im0), __highs2half2(re0, im0));
         __half2 d1 = __hadd2(__lows2half2(re1, im1), __highs2half2(re1, im1));
 #pragma unroll
