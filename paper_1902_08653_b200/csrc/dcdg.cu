@@ -89,7 +89,7 @@ template <int BC, int U, int G, int MINB>
 cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
                           cudaStream_t st) {
   constexpr int NPW = 32 / G;
-  constexpr int LB = (U % DCDG_LB_UL == 0 && (2 * (U / DCDG_LB_UL) * (DCDG_LB_UL * (DCDG_LB_UL - 1) / 2)) % G == 0) ? DCDG_LB_UL : 2;
+  constexpr int LB = (U % DCDG_LB_UL == 0) ? DCDG_LB_UL : 2;
   constexpr size_t smem =
       dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U, LB), NPW, kWarps>::kBytes;
   auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps, MINB, LB>;
@@ -197,6 +197,10 @@ const Spec kSpecs[] = {
     SPEC_F32(16, 16, 4),   // B=128, C=8
     SPEC_F32(64, 16, 16),  // B=256, C=4 / B=512, C=8
     SPEC_F32(64, 8, 8),
+    SPEC_F32(128, 16, 32),  // B=128, C=1 / B=256, C=2 / B=512, C=4
+    SPEC_F32(16, 32, 8),    // configs[4]: U=32
+    SPEC_F32(32, 32, 16),
+    SPEC_F32(64, 32, 32),
     SPEC_F16(32, 16, 4),
     SPEC_F16(32, 8, 4),
     SPEC_F16(16, 16, 4),

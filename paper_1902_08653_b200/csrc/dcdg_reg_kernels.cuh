@@ -123,8 +123,7 @@ template <int BC, int U, int G, int W, int MINB, int LB>
 __global__ void __launch_bounds__(32 * W, MINB)
     ul_reg_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
                float2* __restrict__ X) {
-  static_assert(32 % G == 0 && BC % (2 * G) == 0 && U % LB == 0 && U % G == 0 && (2 * (U / LB) * (LB * (LB - 1) / 2)) % G == 0,
-                "shape");
+  static_assert(32 % G == 0 && BC % (2 * G) == 0 && U % LB == 0, "shape");
   constexpr int NPW = 32 / G, R = BC / G, NP = R / 2;
   constexpr int T = LB * (LB - 1) / 2;  // Gram entries per block
   constexpr int TILE_B = BC * U * 8, Y_B = BC * 8, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
@@ -179,7 +178,8 @@ __global__ void __launch_bounds__(32 * W, MINB)
     // ---- per-problem scalars: ||h_j||^2 (detect.cpp:86-90) and block Grams,
     // each reduce-scattered over the group (lane k keeps a contiguous slice)
     {
-      float v[U];
+      constexpr int NV = ((U + G - 1) / G) * G;  // padded to a multiple of the group
+      float v[NV];
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         float2 e = fmul2(hr[j][0], hr[j][0]);
@@ -188,16 +188,22 @@ __global__ void __launch_bounds__(32 * W, MINB)
         for (int c = 1; c < NP; ++c) e = ffma2(hi[j][c], hi[j][c], ffma2(hr[j][c], hr[j][c], e));
         v[j] = hsum(e);
       }
+#pragma unroll
+      for (int j = U; j < NV; ++j) v[j] = 0.f;
       group_reduce_scatter<G>(v, k);
 #pragma unroll
-      for (int i = 0; i < U / G; ++i) {
-        const float m = __fdividef(1.f, v[i] + kappa);            // m_j = 1/(||h_j||^2 + N0/Ex)
-        mnx[k * (U / G) + i] = make_float4(m, m * v[i], 0.f, 0.f);  // n_j = m_j ||h_j||^2, x_j = 0
+      for (int i = 0; i < NV / G; ++i) {
+        const int idx = k * (NV / G) + i;
+        const float m = __fdividef(1.f, v[i] + kappa);       // m_j = 1/(||h_j||^2 + N0/Ex)
+        if (idx < U) mnx[idx] = make_float4(m, m * v[i], 0.f, 0.f);  // n_j = m_j ||h_j||^2, x_j = 0
       }
     }
     {
-      constexpr int NG = 2 * (U / LB) * T;  // floats of the block Grams
+      constexpr int NG0 = 2 * (U / LB) * T;                 // floats of the block Grams
+      constexpr int NG = ((NG0 + G - 1) / G) * G;            // padded to a multiple of the group
       float v[NG];
+#pragma unroll
+      for (int e = NG0; e < NG; ++e) v[e] = 0.f;
 #pragma unroll
       for (int q = 0; q < U / LB; ++q)
 #pragma unroll
@@ -219,6 +225,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
 #pragma unroll
       for (int i = 0; i < NG / G; ++i) {
         const int gi = k * (NG / G) + i, e = gi >> 1;
+        if (gi >= NG0) continue;
         if (gi & 1) {  // stored as (Re G, Im G, -Im G, Re G)
           gf[e * 4 + 1] = v[i];
           gf[e * 4 + 2] = -v[i];

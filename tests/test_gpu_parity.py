@@ -25,6 +25,10 @@ SHAPES = [
     (3, 24, 6),    # generic (odd sizes)
     (1, 128, 16),  # generic, B=128 C=1
     (4, 20, 5),    # generic
+    (4, 32, 32),   # configs[4]: B=128 U=32 C=4
+    (2, 64, 32),   # B=128 U=32 C=2
+    (8, 16, 32),   # B=128 U=32 C=8 (downlink infeasible: B_c < U)
+    (2, 256, 16),  # B=512 C=2: generic, large B_c
 ]
 
 
