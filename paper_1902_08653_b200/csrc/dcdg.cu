@@ -13,6 +13,7 @@
 
 #include "dcdg.h"
 #include "dcdg_aux_kernels.cuh"
+#include "dcdg_mw_kernels.cuh"
 #include "dcdg_reg_kernels.cuh"
 
 struct dcdg_ctx {
@@ -71,10 +72,10 @@ inline size_t esize(int fmt) { return fmt == DCDG_FP16 ? 4 : 8; }
 constexpr int kWarps = DCDG_CTA_WARPS;
 
 template <typename Kern>
-int occupancy_of(Kern kern, size_t smem) {
+int occupancy_of(Kern kern, size_t smem, int threads = 32 * kWarps) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kWarps, smem) != cudaSuccess || occ < 1) occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 1;
   return occ;
 }
 
@@ -85,11 +86,20 @@ using DlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, 
 #ifndef DCDG_LB_UL
 #define DCDG_LB_UL 2
 #endif
+// coordinate block for full-warp groups (G = 32: 5-round reductions, the
+// per-block dependency chain dominates; measured +8% at U = 32 on B200)
+#ifndef DCDG_LB_UL_WIDE
+#define DCDG_LB_UL_WIDE 4
+#endif
+#ifndef DCDG_LB_UL_MW
+#define DCDG_LB_UL_MW DCDG_LB_UL_WIDE
+#endif
 template <int BC, int U, int G, int MINB>
 cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
                           cudaStream_t st) {
   constexpr int NPW = 32 / G;
-  constexpr int LB = (U % DCDG_LB_UL == 0) ? DCDG_LB_UL : 2;
+  constexpr int LBW = G >= 32 ? DCDG_LB_UL_WIDE : DCDG_LB_UL;
+  constexpr int LB = (U % LBW == 0) ? LBW : 2;
   constexpr size_t smem =
       dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U, LB), NPW, kWarps>::kBytes;
   auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps, MINB, LB>;
@@ -160,8 +170,43 @@ cudaError_t launch_dl_f16(dcdg_ctx* ctx, const void* H, const void* S, int P, in
             : launch_dl_f16_k<BC, U, G, MINB, false>(ctx, H, S, P, C, K, rho_c, X, gp, st);
 }
 
+// Multi-warp kernels (one CTA of NW warps per problem, dcdg_mw_kernels.cuh)
+template <int BC, int U, int NW, int MINB>
+cudaError_t launch_ul_mw(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                         cudaStream_t st) {
+  constexpr int LB = DCDG_LB_UL_MW;
+  constexpr size_t smem = dcdg::MwSmem<dcdg::ul_mw_slot_bytes(BC, U, NW), dcdg::ul_scal_bytes(U, LB), NW,
+                                       dcdg::mw_setup_floats(U, LB), 2 * LB>::kBytes;
+  auto kern = dcdg::ul_mw_f32<BC, U, NW, MINB, LB>;
+  static const int occ = occupancy_of(kern, smem, 32 * NW);
+  const int blocks = std::min(P, ctx->sms * occ);
+  kern<<<blocks, 32 * NW, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K, kappa,
+                                      static_cast<float2*>(X));
+  return cudaGetLastError();
+}
+
+template <int BC, int U, int NW, int MINB, bool GAIN>
+cudaError_t launch_dl_mw_k(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
+                           float* gp, cudaStream_t st) {
+  constexpr size_t smem = dcdg::MwSmem<dcdg::dl_mw_slot_bytes(BC, U, NW), dcdg::dl_scal_bytes(U), NW,
+                                       dcdg::mw_setup_floats(U, 2), 4>::kBytes;
+  auto kern = dcdg::dl_mw_f32<BC, U, NW, MINB, GAIN>;
+  static const int occ = occupancy_of(kern, smem, 32 * NW);
+  const int blocks = std::min(P, ctx->sms * occ);
+  kern<<<blocks, 32 * NW, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(S), P, C, K, rho_c,
+                                      static_cast<float2*>(X), gp, ctx->d_status);
+  return cudaGetLastError();
+}
+
+template <int BC, int U, int NW, int MINB>
+cudaError_t launch_dl_mw(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
+                         float* gp, cudaStream_t st) {
+  return gp ? launch_dl_mw_k<BC, U, NW, MINB, true>(ctx, H, S, P, C, K, rho_c, X, gp, st)
+            : launch_dl_mw_k<BC, U, NW, MINB, false>(ctx, H, S, P, C, K, rho_c, X, gp, st);
+}
+
 struct Spec {
-  int bc, u, fmt, g;
+  int bc, u, fmt, g;  // g > 0: lanes per problem; g < 0: -(warps per problem)
   UlLaunch ul;
   DlLaunch dl;
 };
@@ -190,6 +235,10 @@ struct Spec {
 #define DCDG_MIN_WARPS_DL_F16 8
 #endif
 constexpr int minb(int warps) { return warps / kWarps > 0 ? warps / kWarps : 1; }
+constexpr int minb_mw(int warps, int nw) { return warps / nw > 0 ? warps / nw : 1; }
+#define SPEC_MW_F32(BC, U, NW)                                                                  \
+  {BC, U, DCDG_FP32, -(NW), launch_ul_mw<BC, U, NW, minb_mw(DCDG_MIN_WARPS_UL_F32, NW)>, \
+   launch_dl_mw<BC, U, NW, minb_mw(DCDG_MIN_WARPS_UL_F32, NW)>}
 
 const Spec kSpecs[] = {
     SPEC_F32(32, 16, 8),   // north-star target: B=256, C=8, U=16
@@ -201,6 +250,12 @@ const Spec kSpecs[] = {
     SPEC_F32(16, 32, 8),    // configs[4]: U=32
     SPEC_F32(32, 32, 16),
     SPEC_F32(64, 32, 32),
+    SPEC_MW_F32(256, 16, 2),  // large tiles: one CTA of NW warps per problem
+    SPEC_MW_F32(512, 16, 4),
+    SPEC_MW_F32(1024, 16, 8),
+    SPEC_MW_F32(128, 32, 2),
+    SPEC_MW_F32(256, 32, 4),
+    SPEC_MW_F32(512, 32, 8),
     SPEC_F16(32, 16, 4),
     SPEC_F16(32, 8, 4),
     SPEC_F16(16, 16, 4),
@@ -333,7 +388,9 @@ int dcdg_kernel_name(int direction, int Bc, int U, int fmt, char* buf, int len) 
   char tmp[96];
   const char* dir = direction ? "dl" : "ul";
   const char* f = fmt == DCDG_FP16 ? "f16" : "f32";
-  if (s)
+  if (s && s->g < 0)
+    std::snprintf(tmp, sizeof tmp, "%s_mw_%s<%d,%d,%d>", dir, f, Bc, U, -s->g);
+  else if (s)
     std::snprintf(tmp, sizeof tmp, "%s_reg_%s<%d,%d,%d>", dir, f, Bc, U, s->g);
   else
     std::snprintf(tmp, sizeof tmp, "%s_generic_%s", dir, f);

@@ -38,6 +38,16 @@
 
 namespace dcdg {
 
+// Groups of at least this many lanes reduce the block's dot products by
+// reduce-scatter + shared-memory broadcast instead of a full butterfly (fewer
+// shuffles, one more shared-memory round trip on the critical path).
+#ifndef DCDG_SCATTER_MIN_G_UL
+#define DCDG_SCATTER_MIN_G_UL 32
+#endif
+#ifndef DCDG_SCATTER_MIN_G_DL
+#define DCDG_SCATTER_MIN_G_DL 16
+#endif
+
 template <int TILE_B, int VEC_B, int NPW>
 struct Slot {
   static constexpr int kBytes = NPW * (TILE_B + VEC_B);
@@ -93,12 +103,30 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int k) {
   ReduceScatter<G / 2, NV, NV>::run(v, k);
 }
 
-// Per-problem scalar blocks (bytes); +16 skews consecutive groups' blocks
-// across shared-memory banks.  Used by the kernels and their launchers.
-__host__ __device__ constexpr int ul_scal_bytes(int U, int LB = 2) {
-  return U * 16 + (U / LB) * (LB * (LB - 1) / 2) * 16 + 16;
+// Reduce-scatter NV values over a group of G lanes (NV <= G), then finish the
+// sums: afterwards lane k holds the group-wide sum of value k / (G/NV).
+// log2(NV) halving rounds (NV-1 shuffles) + log2(G/NV) single-value rounds —
+// against NV*log2(G) shuffles for a butterfly of every value.  The results
+// are then broadcast through shared memory (one store per value, one vector
+// load per lane).
+template <int G, int NV>
+__device__ __forceinline__ float group_scatter_sum(float (&v)[NV], int k) {
+  static_assert(NV <= G && G % NV == 0, "values must not outnumber the group");
+  ReduceScatter<G / 2, NV, NV>::run(v, k);
+  float s = v[0];
+#pragma unroll
+  for (int o = G / (2 * NV); o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
 }
-__host__ __device__ constexpr int dl_scal_bytes(int U) { return U * 32 + 16; }
+
+// Per-problem scalar blocks (bytes); the uplink block ends with a double
+// buffer of 2 x 2*LB floats for the scatter-sum broadcast, the downlink one
+// with 2 x 4 floats; +16 skews consecutive groups' blocks across shared-memory
+// banks.  Used by the kernels and their launchers.
+__host__ __device__ constexpr int ul_scal_bytes(int U, int LB = 2) {
+  return U * 16 + (U / LB) * (LB * (LB - 1) / 2) * 16 + 16 * LB + 16;
+}
+__host__ __device__ constexpr int dl_scal_bytes(int U) { return U * 32 + 32 + 16; }
 
 // Shared-memory layout of one CTA: [W staging slots][W*NPW scalar blocks][W mbarriers]
 template <int SLOT_B, int SCAL_B, int NPW, int W>
@@ -135,6 +163,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
   unsigned char* slot = smem + warp * SLOT_B;
   float4* mnx = reinterpret_cast<float4*>(smem + L::kScalOff + (warp * NPW + g) * SCAL_B);
   float4* gb = mnx + U;
+  float* dbuf = reinterpret_cast<float*>(gb + (U / LB) * T);  // 2 x 2*LB floats
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff) + warp;
   const int nsets = (P + NPW - 1) / NPW;
   const int nw = gridDim.x * W;
@@ -253,10 +282,26 @@ __global__ void __launch_bounds__(32 * W, MINB)
           }
           d[a] = make_float2(hsum(ar), hsum(ai));
         }
+        if constexpr (2 * LB <= G && G >= DCDG_SCATTER_MIN_G_UL) {
+          // reduce-scatter + shared-memory broadcast (double-buffered per group)
+          float v[2 * LB];
 #pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1)
+          for (int a = 0; a < LB; ++a) {
+            v[2 * a] = d[a].x;
+            v[2 * a + 1] = d[a].y;
+          }
+          const float sum = group_scatter_sum<G, 2 * LB>(v, k);
+          float* db = dbuf + ((t * (U / LB) + q) & 1) * 2 * LB;  // alternates every block
+          if (k % (G / (2 * LB)) == 0) db[k / (G / (2 * LB))] = sum;
+          __syncwarp();
 #pragma unroll
-          for (int a = 0; a < LB; ++a) d[a] = fadd2(d[a], shfl_xor2(d[a], o));
+          for (int a = 0; a < LB; ++a) d[a] = reinterpret_cast<const float2*>(db)[a];
+        } else {
+#pragma unroll
+          for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+            for (int a = 0; a < LB; ++a) d[a] = fadd2(d[a], shfl_xor2(d[a], o));
+        }
         float2 dx[LB];
 #pragma unroll
         for (int a = 0; a < LB; ++a) {
@@ -501,6 +546,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
   float4* ss = reinterpret_cast<float4*>(smem + L::kScalOff + (warp * NPW + g) * SCAL_B);
   float4* gp = ss + U;
   float2* sraw = reinterpret_cast<float2*>(gp + U / 2);
+  float* dbuf = reinterpret_cast<float*>(sraw + U);  // 2 x 4 floats
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff) + warp;
   const int nsets = (P + NPW - 1) / NPW;
   const int nw = gridDim.x * W;
@@ -626,10 +672,21 @@ __global__ void __launch_bounds__(32 * W, MINB)
         }
         float2 d0 = make_float2(hsum(a0), hsum(c0));
         float2 d1 = make_float2(hsum(a1), hsum(c1));
+        if constexpr (4 <= G && G >= DCDG_SCATTER_MIN_G_DL) {
+          float v[4] = {d0.x, d0.y, d1.x, d1.y};
+          const float sum = group_scatter_sum<G, 4>(v, k);
+          float* db = dbuf + ((t * (U / 2) + jp) & 1) * 4;
+          if (k % (G / 4) == 0) db[k / (G / 4)] = sum;
+          __syncwarp();
+          const float4 dd = *reinterpret_cast<const float4*>(db);
+          d0 = make_float2(dd.x, dd.y);
+          d1 = make_float2(dd.z, dd.w);
+        } else {
 #pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) {
-          d0 = fadd2(d0, shfl_xor2(d0, o));
-          d1 = fadd2(d1, shfl_xor2(d1, o));
+          for (int o = G / 2; o > 0; o >>= 1) {
+            d0 = fadd2(d0, shfl_xor2(d0, o));
+            d1 = fadd2(d1, shfl_xor2(d1, o));
+          }
         }
         // resid_u = h~_u^H x - s~_u ; x -= resid_u h~_u   (precode.cpp:89-94)
         const float2 r0 = fadd2(d0, make_float2(-S0.x, -S0.y));

@@ -28,8 +28,31 @@ SHAPES = [
     (4, 32, 32),   # configs[4]: B=128 U=32 C=4
     (2, 64, 32),   # B=128 U=32 C=2
     (8, 16, 32),   # B=128 U=32 C=8 (downlink infeasible: B_c < U)
-    (2, 256, 16),  # B=512 C=2: generic, large B_c
+    (2, 256, 16),  # B=512 C=2: multi-warp (2 warps per problem)
+    (1, 128, 32),  # multi-warp, U=32
+    (2, 256, 32),  # multi-warp, 4 warps
+    (1, 512, 32),  # multi-warp, 8 warps
+    (1, 512, 16),
+    (1, 1024, 16),
 ]
+
+
+@pytest.mark.parametrize("shape,S", [((8, 32, 16), 1200), ((1, 256, 16), 1400), ((1, 512, 32), 400)],
+                         ids=lambda v: str(v))
+def test_persistent_grid_loops(engine, port, shape, S):
+    """More problems than resident warps/CTAs: every persistent worker runs
+    several problems through its staging slot (prefetch + phase flips)."""
+    C, Bc, U = shape
+    b = batch(C, Bc, U, S=S, seed=77)
+    xhat, local, _ = port.ul_detect_batch(b["h_tiles"], b["y"], b["n0"], 1.0, 3, UNIFORM)
+    r = engine.ul_detect(to_dev(b["h_tiles"]), to_dev(b["y"]), n0=b["n0"], K=3)
+    sym = qam_symbols(S, U)
+    x, g = port.dl_precode_batch(b["h_tiles"], sym, float(np.sqrt(U)), 3)
+    d = engine.dl_precode(to_dev(b["h_tiles"]), to_dev(sym), rho=float(np.sqrt(U)), K=3)
+    engine.sync()
+    assert rel_err(to_host(r.x_local), local) <= TOL_FP32
+    assert rel_err(to_host(d.x), x) <= TOL_FP32
+    assert np.max(np.abs(d.gain.cpu().numpy() - g) / np.abs(g)) <= TOL_FP32
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"C{s[0]}_Bc{s[1]}_U{s[2]}")
