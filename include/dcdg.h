@@ -181,6 +181,41 @@ int dcdg_dl_receive(dcdg_ctx* ctx, const void* H, const void* x_dl, const void* 
                     const float* noise, int S, int C, int Bc, int U, int fmt, int qam, double ex,
                     uint8_t* labels, float* beta, uint8_t* flagged, void* stream);
 
+/* ---- BER-sweep building blocks (fp32 only) ---- */
+
+/* Device-side batch synthesis (make_batch + run_uplink_round's observation,
+ * cluster.cpp:80-105,142-145) with a counter-based generator (Philox-4x32-10)
+ * keyed by (seed, purpose, trial = first_trial + s, element): the channel
+ * tiles H [S][C][U][Bc] ~ CN(0,1), y = H x + n [S][C][Bc] with n ~ CN(0,n0)
+ * (y may be NULL), payload bits [S][U*log2(qam)] (one byte per bit, MSB first),
+ * the QAM symbols x [S][U] (sym may be NULL) and downlink receiver noise
+ * [S][U] ~ CN(0,n0) (noise_dl may be NULL).  The channel of global antenna
+ * row b = c*Bc + i does not depend on the cluster split. */
+int dcdg_synth(dcdg_ctx* ctx, int S, int C, int Bc, int U, int qam, double ex, double n0, uint64_t seed,
+               uint64_t first_trial, void* H, void* y, uint8_t* bits, void* sym, void* noise_dl, void* stream);
+
+/* Matched-filter detector over all C clusters of each subcarrier (mf_detect,
+ * detect.cpp:191-218): xhat[s][u] = sum_c h_cu^H y_c / sum_c ||h_cu||^2. */
+int dcdg_mf_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, int Bc, int U, float* xhat,
+                   void* stream);
+
+/* Matched-filter precoder (mf_precode, precode.cpp:171-202): per cluster
+ * x_c = (rho/sqrt(C)) H_c s / ||H_c s||, x_dl [S][C][Bc]. */
+int dcdg_mf_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, int Bc, int U, double rho,
+                    float* x_dl, void* stream);
+
+/* Exact L-MMSE on the full channel of each subcarrier (lmmse_exact,
+ * detect.cpp:54-65): xhat = (H^H H + n0/ex I)^-1 H^H y, Cholesky solve
+ * (numerics.cpp:30-75), the C tiles stacked.  U <= 32. */
+int dcdg_lmmse_exact(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, int Bc, int U, double n0,
+                     double ex, float* xhat, void* stream);
+
+/* Exact min-norm zero-forcing precoder on the full channel (zf_exact,
+ * precode.cpp:31-50) followed by power_scale(x, rho) (rho == 0: raw),
+ * x_dl [S][C][Bc] in the tile order of H.  U <= 32. */
+int dcdg_zf_exact(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, int Bc, int U, double rho,
+                  float* x_dl, void* stream);
+
 /* In-place round of n fp32 values to the nearest binary16 (RNE), widened
  * back: the wire-format rounding of PrecisionScope::messages_only
  * (precision.cpp:43-72, detect.cpp:170-173, precode.cpp:159-160). */

@@ -802,3 +802,53 @@ int dcdo_uplink_observe(const double* h, int b, int u, const uint8_t* bits, unsi
 double dcdo_snr_to_n0(double snr_db, int users, double ex) {
   return (double)users * ex / pow(10.0, snr_db / 10.0);
 }
+
+/* mf_detect, detect.cpp:191-218 (messages in fp64: no rounding). Tiles back to
+ * back, tile c is bc[c] x u column-major; ys concatenated. */
+int dcdo_mf_detect(int nc, const int* bc, int u, const double* h_tiles, const double* ys, double* x_out) {
+  if (nc == 0) return fail(EINVAL_, "mf_detect: no clusters");
+  double* corr = (double*)calloc(2 * (size_t)u, sizeof(double));
+  double* energy = (double*)calloc((size_t)u, sizeof(double));
+  size_t ho = 0, yo = 0;
+  for (int c = 0; c < nc; ++c) {
+    for (int j = 0; j < u; ++j) {
+      double pc[2];
+      const double* col = h_tiles + 2 * (ho + (size_t)j * bc[c]);
+      dcdo_cdotc(col, ys + 2 * yo, bc[c], pc);
+      const double pe = dcdo_norm2sq(col, bc[c]);
+      corr[2 * j] += pc[0];
+      corr[2 * j + 1] += pc[1];
+      energy[j] += pe;
+    }
+    ho += (size_t)bc[c] * u;
+    yo += (size_t)bc[c];
+  }
+  int rc = 0;
+  for (int j = 0; j < u && !rc; ++j) {
+    if (energy[j] == 0.0) {
+      rc = fail(ERUNTIME_, "mf_detect: user %d has zero channel energy", j);
+      break;
+    }
+    x_out[2 * j] = corr[2 * j] / energy[j];
+    x_out[2 * j + 1] = corr[2 * j + 1] / energy[j];
+  }
+  free(corr);
+  free(energy);
+  return rc;
+}
+
+/* mf_precode, precode.cpp:171-202 (fp64): x_c[j] = cdotc(h_dl,c col j, s),
+ * power_scale(x_c, rho/sqrt(C)). Downlink tiles u x bc[c] column-major. */
+int dcdo_mf_precode(int nc, const int* bc, int u, const double* hdl_tiles, const double* s, double rho, double* x) {
+  if (nc == 0) return fail(EINVAL_, "mf_precode: no clusters");
+  const double rho_c = rho / sqrt((double)nc);
+  size_t ho = 0, xo = 0;
+  for (int c = 0; c < nc; ++c) {
+    double* xc = x + 2 * xo;
+    for (int j = 0; j < bc[c]; ++j) dcdo_cdotc(hdl_tiles + 2 * (ho + (size_t)j * u), s, u, xc + 2 * j);
+    if (dcdo_power_scale(xc, bc[c], rho_c)) return fail(ERUNTIME_, "mf_precode: cluster %d produced a zero beamformer", c);
+    ho += (size_t)bc[c] * u;
+    xo += (size_t)bc[c];
+  }
+  return 0;
+}

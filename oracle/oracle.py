@@ -246,6 +246,29 @@ class Oracle:
         self._check(self._f("zf_exact")(_ptr(h_dl), C.c_int(u), C.c_int(b), _ptr(s), _ptr(x)))
         return x
 
+    def mf_detect(self, hs, ys) -> np.ndarray:
+        """mf_detect (detect.cpp:191-218) over cluster blocks hs (B_c x U) and ys."""
+        nc = len(hs)
+        u = hs[0].shape[1]
+        bc = np.array([h.shape[0] for h in hs], dtype=np.int32)
+        tiles = np.concatenate([_cin(h).ravel(order="F") for h in hs])
+        yy = np.concatenate([_cin(y) for y in ys])
+        x = np.zeros(u, np.complex128)
+        self._check(self._f("mf_detect")(C.c_int(nc), bc.ctypes.data_as(C.POINTER(C.c_int)), C.c_int(u),
+                                         _ptr(tiles), _ptr(yy), _ptr(x)))
+        return x
+
+    def mf_precode(self, h_dl_blocks, s, rho) -> np.ndarray:
+        """mf_precode (precode.cpp:171-202): concatenated per-cluster beamformers."""
+        nc = len(h_dl_blocks)
+        s = _cin(s)
+        bc = np.array([h.shape[1] for h in h_dl_blocks], dtype=np.int32)
+        tiles = np.concatenate([_cin(h).ravel(order="F") for h in h_dl_blocks])
+        x = np.zeros(int(bc.sum()), np.complex128)
+        self._check(self._f("mf_precode")(C.c_int(nc), bc.ctypes.data_as(C.POINTER(C.c_int)), C.c_int(s.size),
+                                          _ptr(tiles), _ptr(s), C.c_double(rho), _ptr(x)))
+        return x
+
     def power_scale(self, x, rho) -> np.ndarray:
         x = _cin(x).copy()
         self._check(self._f("power_scale")(_ptr(x), C.c_int(x.size), C.c_double(rho)))

@@ -245,6 +245,34 @@ int dcdref_decentralized_cd_precode(int nc, const int* bc, int u, const double* 
   });
 }
 
+// MF baselines: tiles back to back as in dcdref_decentralized_cd_* above.
+int dcdref_mf_detect(int nc, const int* bc, int u, const double* h_tiles, const double* ys, double* x_out) {
+  return guarded([&] {
+    std::vector<dcd::ClusterData> cl(static_cast<std::size_t>(nc));
+    std::size_t ho = 0, yo = 0;
+    for (int c = 0; c < nc; ++c) {
+      cl[c].h = mat_in(h_tiles + 2 * ho, bc[c], u);
+      cl[c].y = vec_in(ys + 2 * yo, bc[c]);
+      ho += static_cast<std::size_t>(bc[c]) * u;
+      yo += static_cast<std::size_t>(bc[c]);
+    }
+    vec_out(dcd::mf_detect(cl, dcd::PrecisionMode{}), x_out);
+  });
+}
+
+int dcdref_mf_precode(int nc, const int* bc, int u, const double* hdl_tiles, const double* s, double rho,
+                      double* x) {
+  return guarded([&] {
+    std::vector<ComplexMatrix> blocks(static_cast<std::size_t>(nc));
+    std::size_t ho = 0;
+    for (int c = 0; c < nc; ++c) {
+      blocks[c] = mat_in(hdl_tiles + 2 * ho, u, bc[c]);
+      ho += static_cast<std::size_t>(bc[c]) * u;
+    }
+    vec_out(dcd::mf_precode(blocks, vec_in(s, u), rho, dcd::PrecisionMode{}).x, x);
+  });
+}
+
 // ---- system model / RNG ----------------------------------------------------
 uint64_t dcdref_derive_seed(uint64_t master, uint64_t purpose, uint64_t index) {
   return dcd::derive_seed(master, static_cast<dcd::RngPurpose>(purpose), index);

@@ -72,6 +72,13 @@ SIGNATURES = {
     "dcdg_dl_receive": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.c_double, _vp, _vp, _vp, _vp]),
     "dcdg_convert": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, C.c_int64, _vp]),
+    "dcdg_synth": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64,
+                             C.c_uint64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "dcdg_mf_detect": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp]),
+    "dcdg_mf_precode": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _vp, _vp]),
+    "dcdg_lmmse_exact": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, _vp,
+                                   _vp]),
+    "dcdg_zf_exact": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _vp, _vp]),
     "dcdg_kernel_name": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int]),
 }
 

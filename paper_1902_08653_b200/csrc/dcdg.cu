@@ -14,6 +14,7 @@
 #include "dcdg.h"
 #include "dcdg_aux_kernels.cuh"
 #include "dcdg_mw_kernels.cuh"
+#include "dcdg_sweep_kernels.cuh"
 #include "dcdg_reg_kernels.cuh"
 
 struct dcdg_ctx {
@@ -307,7 +308,7 @@ int launch_gram_chol(dcdg_ctx* ctx, const void* H, int P, int NT, int Bc, int U,
     auto k = dcdg::gram_chol<T, UT, BT, MODE>;                                                              \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));           \
     k<<<blocks, 128, smem, st>>>(static_cast<const T*>(H), P, NT, Bc, U, a0, a1, scale,                     \
-                                 MODE == dcdg::kPev && fmt == DCDG_FP16, out, ctx->d_status);               \
+                                 MODE == dcdg::kPev && fmt == DCDG_FP16, out, ctx->d_status, nullptr, nullptr); \
   }
 #define GC_DISPATCH(T)                            \
   if (U == 16 && Bc == 32) GC_LAUNCH(T, 16, 32)   \
@@ -326,6 +327,31 @@ int launch_gram_chol(dcdg_ctx* ctx, const void* H, int P, int NT, int Bc, int U,
 #undef GC_LAUNCH
   ++ctx->launches;
   CUDA_TRY(cudaGetLastError(), "gram/cholesky launch");
+  return DCDG_OK;
+}
+
+// Exact solvers (fp32 tiles): one warp per subcarrier over its C stacked tiles.
+template <int MODE>
+int launch_solve(dcdg_ctx* ctx, const void* H, const void* V, int S, int C, int Bc, int U, float a0, float scale,
+                 float2* xo, cudaStream_t st) {
+  const size_t smem = 4 * static_cast<size_t>(dcdg::pev_smem_per_warp(U));
+  const int blocks = (S + 3) / 4;
+#define SV_LAUNCH(UT)                                                                                        \
+  {                                                                                                          \
+    auto k = dcdg::gram_chol<float2, UT, 0, MODE>;                                                           \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));            \
+    k<<<blocks, 128, smem, st>>>(static_cast<const float2*>(H), S, C, Bc, U, a0, 1.f, scale, false, nullptr, \
+                                 ctx->d_status, static_cast<const float2*>(V), xo);                          \
+  }
+  switch (U) {
+    case 8: SV_LAUNCH(8) break;
+    case 16: SV_LAUNCH(16) break;
+    case 32: SV_LAUNCH(32) break;
+    default: SV_LAUNCH(0) break;
+  }
+#undef SV_LAUNCH
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "exact solver launch");
   return DCDG_OK;
 }
 
@@ -424,6 +450,15 @@ int dcdg_sync_status(dcdg_ctx* ctx, void* stream) {
     case dcdg::ST_BAD_VARIANCE:
       g_err = "fusion_weights: variances must be positive and finite";
       return DCDG_EINVAL;
+    case dcdg::ST_RANK_DEFICIENT:
+      g_err = "zf_exact: channel rows are rank deficient";
+      return DCDG_ENUMERIC;
+    case dcdg::ST_MF_ZERO_ENERGY:
+      g_err = "mf_detect: user " + std::to_string(detail) + " has zero channel energy";
+      return DCDG_ENUMERIC;
+    case dcdg::ST_MF_ZERO_BEAMFORMER:
+      g_err = "mf_precode: cluster " + std::to_string(detail) + " produced a zero beamformer";
+      return DCDG_ENUMERIC;
     default:
       g_err = "dcdg: unknown device status";
       return DCDG_ENUMERIC;
@@ -771,6 +806,91 @@ int dcdg_convert(dcdg_ctx* ctx, const void* src, int src_fmt, void* dst, int dst
   ++ctx->launches;
   CUDA_TRY(cudaGetLastError(), "convert launch");
   return DCDG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// BER-sweep building blocks
+// ---------------------------------------------------------------------------
+int dcdg_synth(dcdg_ctx* ctx, int S, int C, int Bc, int U, int qam, double ex, double n0, uint64_t seed,
+               uint64_t first_trial, void* H, void* y, uint8_t* bits, void* sym, void* noise_dl, void* stream) {
+  if (C <= 0 || Bc <= 0) return fail(DCDG_EINVAL, "make_batch: empty layout");
+  if (U <= 0 || static_cast<long long>(C) * Bc < U) return fail(DCDG_EINVAL, "make_batch: need B >= U >= 1");
+  if (int rc = check_qam(qam, ex)) return rc;
+  if (n0 < 0.0) return fail(DCDG_EINVAL, "awgn: noise power must be nonnegative");
+  if (!H || !bits) return fail(DCDG_EINVAL, "dcdg_synth: null buffer");
+  if (int rc = check_ctx(ctx)) return rc;
+  if (S <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const long long n = static_cast<long long>(S) * C * Bc;
+  const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, static_cast<long long>(ctx->sms) * 8));
+  dcdg::synth_kernel<<<blocks, 256, 0, as_stream(stream)>>>(
+      S, C, Bc, U, seed, first_trial, static_cast<float>(n0), static_cast<unsigned>(qam), ex, static_cast<float2*>(H),
+      static_cast<float2*>(y), bits, static_cast<float2*>(sym), static_cast<float2*>(noise_dl));
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "synth launch");
+  return DCDG_OK;
+}
+
+int dcdg_mf_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, int Bc, int U, float* xhat,
+                   void* stream) {
+  if (C <= 0) return fail(DCDG_EINVAL, "mf_detect: no clusters");
+  if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "detector: empty channel matrix");
+  if (U > 32) return fail(DCDG_EINVAL, "dcdg_mf_detect: U > 32 not supported");
+  if (!H || !y || !xhat) return fail(DCDG_EINVAL, "dcdg_mf_detect: null buffer");
+  if (int rc = check_ctx(ctx)) return rc;
+  if (S <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  dcdg::mf_detect_kernel<<<(S + 3) / 4, 128, 0, as_stream(stream)>>>(
+      static_cast<const float2*>(H), static_cast<const float2*>(y), S, C, Bc, U, reinterpret_cast<float2*>(xhat),
+      ctx->d_status);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "mf_detect launch");
+  return DCDG_OK;
+}
+
+int dcdg_mf_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, int Bc, int U, double rho,
+                    float* x_dl, void* stream) {
+  if (C <= 0) return fail(DCDG_EINVAL, "mf_precode: no clusters");
+  if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "precoder: empty channel matrix");
+  if (!(rho > 0.0)) return fail(DCDG_EINVAL, "power_scale: amplitude must be positive");
+  if (!H || !s || !x_dl) return fail(DCDG_EINVAL, "dcdg_mf_precode: null buffer");
+  if (int rc = check_ctx(ctx)) return rc;
+  const long long P = static_cast<long long>(S) * C;
+  if (P <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const float rho_c = static_cast<float>(rho / std::sqrt(static_cast<double>(C)));
+  dcdg::mf_precode_kernel<<<static_cast<int>((P + 3) / 4), 128, 0, as_stream(stream)>>>(
+      static_cast<const float2*>(H), static_cast<const float2*>(s), static_cast<int>(P), C, Bc, U, rho_c,
+      reinterpret_cast<float2*>(x_dl), ctx->d_status);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "mf_precode launch");
+  return DCDG_OK;
+}
+
+int dcdg_lmmse_exact(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, int Bc, int U, double n0,
+                     double ex, float* xhat, void* stream) {
+  if (C <= 0 || Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "detector: empty channel matrix");
+  if (n0 < 0.0 || !(ex > 0.0)) return fail(DCDG_EINVAL, "detector: need N0 >= 0 and E_x > 0");
+  if (U > 32) return fail(DCDG_EINVAL, "dcdg_lmmse_exact: U > 32 not supported");
+  if (!H || !y || !xhat) return fail(DCDG_EINVAL, "dcdg_lmmse_exact: null buffer");
+  if (int rc = check_ctx(ctx)) return rc;
+  if (S <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  return launch_solve<dcdg::kSolve>(ctx, H, y, S, C, Bc, U, static_cast<float>(n0 / ex), 0.f,
+                                    reinterpret_cast<float2*>(xhat), as_stream(stream));
+}
+
+int dcdg_zf_exact(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, int Bc, int U, double rho,
+                  float* x_dl, void* stream) {
+  if (C <= 0 || Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "precoder: empty channel matrix");
+  if (rho < 0.0 || std::isnan(rho)) return fail(DCDG_EINVAL, "power_scale: amplitude must be positive");
+  if (U > 32) return fail(DCDG_EINVAL, "dcdg_zf_exact: U > 32 not supported");
+  if (!H || !s || !x_dl) return fail(DCDG_EINVAL, "dcdg_zf_exact: null buffer");
+  if (int rc = check_ctx(ctx)) return rc;
+  if (S <= 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  return launch_solve<dcdg::kZf>(ctx, H, s, S, C, Bc, U, 0.f, static_cast<float>(rho),
+                                 reinterpret_cast<float2*>(x_dl), as_stream(stream));
 }
 
 }  // extern "C"

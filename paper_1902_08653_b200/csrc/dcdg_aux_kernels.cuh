@@ -174,12 +174,116 @@ __host__ __device__ constexpr int pev_smem_per_warp(int U) {
 //         out[p*U + u] = 1 - kappa * [A^-1]_uu.
 // UT > 0: U == UT at compile time (register-resident Cholesky/inverse);
 // BT > 0: B_c == BT at compile time (vectorised staging, unrolled Gram).
-enum GramMode { kPev = 0, kBias = 1 };
+//   kSolve (lmmse_exact, detect.cpp:54-65): NT stacked tiles, A = kappa*I + G,
+//         x = A^-1 H^H y by forward/back substitution, xo[p*U + u];
+//   kZf   (zf_exact + power_scale, precode.cpp:31-50,101-111): A = G,
+//         w = A^-1 s, x = H w over the NT tiles scaled to ||x|| = scale,
+//         xo[(p*NT + t)*B_c + i].
+enum GramMode { kPev = 0, kBias = 1, kSolve = 2, kZf = 3 };
 
+// Cholesky solve A w = b with L in shared memory (Lat(i, k) = L_ik, real
+// diagonal): lane i < U holds b_i on entry and returns w_i.  Column-oriented
+// forward (L z = b) and back (L^H w = z) substitution, one broadcast per step.
+template <typename LF>
+__device__ __forceinline__ float2 chol_solve(LF Lat, float2 bi, int U, int lane) {
+  float2 zi = make_float2(0.f, 0.f);
+  for (int j = 0; j < U; ++j) {
+    const float ljj = Lat(j, j).x;
+    const float2 zj = make_float2(__shfl_sync(0xffffffffu, bi.x, j) / ljj, __shfl_sync(0xffffffffu, bi.y, j) / ljj);
+    if (lane == j) zi = zj;
+    if (lane > j && lane < U) {  // b_i -= L_ij z_j
+      const float2 l = Lat(lane, j);
+      bi.x -= l.x * zj.x - l.y * zj.y;
+      bi.y -= l.x * zj.y + l.y * zj.x;
+    }
+  }
+  float2 wi = make_float2(0.f, 0.f);
+  for (int j = U - 1; j >= 0; --j) {
+    const float ljj = Lat(j, j).x;
+    const float2 wj = make_float2(__shfl_sync(0xffffffffu, zi.x, j) / ljj, __shfl_sync(0xffffffffu, zi.y, j) / ljj);
+    if (lane == j) wi = wj;
+    if (lane < j) {  // z_i -= conj(L_ji) w_j
+      const float2 l = Lat(j, lane);
+      zi.x -= l.x * wj.x + l.y * wj.y;
+      zi.y -= l.x * wj.y - l.y * wj.x;
+    }
+  }
+  return wi;
+}
+
+// Right-hand side and output stage of the solve modes (after the Cholesky).
+template <typename T, int MODE, typename LF>
+__device__ __forceinline__ void solve_emit(LF Lat, const T* __restrict__ H, const T* __restrict__ V, long long p, int NT,
+                                           int BC, int U, float scale, bool singular, float2* __restrict__ xo,
+                                           unsigned long long* __restrict__ status, int lane) {
+  float2 b = make_float2(0.f, 0.f);
+  if (lane < U) {
+    if (MODE == kSolve) {  // b_u = sum_t h_tu^H y_t   (cdotc, detect.cpp:61-63)
+      for (int t = 0; t < NT; ++t) {
+        const T* h = H + ((static_cast<size_t>(p) * NT + t) * U + lane) * BC;
+        const T* y = V + (static_cast<size_t>(p) * NT + t) * BC;
+        for (int i = 0; i < BC; ++i) {
+          const float2 hv = ldv(h, i), yv = ldv(y, i);
+          b.x = fmaf(hv.x, yv.x, fmaf(hv.y, yv.y, b.x));
+          b.y = fmaf(hv.x, yv.y, fmaf(-hv.y, yv.x, b.y));
+        }
+      }
+    } else {
+      b = ldc(V, static_cast<size_t>(p) * U + lane);
+    }
+  }
+  const float2 w = chol_solve(Lat, b, U, lane);
+  if (singular && lane == 0) record_status(status, p, MODE == kSolve ? ST_SINGULAR : ST_RANK_DEFICIENT, 0);
+  if (MODE == kSolve) {
+    if (lane < U) xo[static_cast<size_t>(p) * U + lane] = w;
+    return;
+  }
+  // x = H w (x_i = sum_u H_iu w_u, precode.cpp:45-48), then power_scale
+  float e = 0.f;
+  for (int t = 0; t < NT; ++t) {
+    const T* h = H + (static_cast<size_t>(p) * NT + t) * U * BC;
+    float2* x = xo + (static_cast<size_t>(p) * NT + t) * BC;
+    for (int i0 = 0; i0 < BC; i0 += 32) {
+      const int i = i0 + lane;
+      float xr = 0.f, xi = 0.f;
+      for (int u = 0; u < U; ++u) {
+        const float wr = __shfl_sync(0xffffffffu, w.x, u), wi = __shfl_sync(0xffffffffu, w.y, u);
+        if (i < BC) {
+          const float2 hv = ldv(h + static_cast<size_t>(u) * BC, i);
+          xr = fmaf(hv.x, wr, fmaf(-hv.y, wi, xr));
+          xi = fmaf(hv.x, wi, fmaf(hv.y, wr, xi));
+        }
+      }
+      if (i < BC) {
+        x[i] = make_float2(xr, xi);
+        e = fmaf(xr, xr, fmaf(xi, xi, e));
+      }
+    }
+  }
+  if (scale <= 0.f) return;  // raw zf_exact beamformer (no power_scale)
+  e = warp_sum(e);
+  if (e == 0.f) {
+    if (lane == 0 && !singular) record_status(status, p, ST_ZERO_BEAMFORMER, 0);
+    return;
+  }
+  const float g = scale / __fsqrt_rn(e);  // power_scale(x, rho), precode.cpp:101-111
+  for (int t = 0; t < NT; ++t) {
+    float2* x = xo + (static_cast<size_t>(p) * NT + t) * BC;
+    for (int i = lane; i < BC; i += 32) {
+      const float2 v = x[i];
+      x[i] = make_float2(v.x * g, v.y * g);
+    }
+  }
+}
+
+// (the solve modes return after the Cholesky; the inverse that follows is
+// dead code in those instantiations)
+#pragma nv_diag_suppress 128
 template <typename T, int UT, int BT, int MODE>
 __global__ void __launch_bounds__(128) gram_chol(const T* __restrict__ H, int P, int NT, int BC_, int U_, float a0,
                                                  float a1, float scale, bool round_fp16, float* __restrict__ out,
-                                                 unsigned long long* __restrict__ status) {
+                                                 unsigned long long* __restrict__ status,
+                                                 const T* __restrict__ V = nullptr, float2* __restrict__ xo = nullptr) {
   extern __shared__ float2 vsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long p = static_cast<long long>(blockIdx.x) * 4 + warp;
@@ -265,7 +369,11 @@ __global__ void __launch_bounds__(128) gram_chol(const T* __restrict__ H, int P,
   for (int j = lane; j < U; j += 32) maxdiag = fmaxf(maxdiag, fabsf(A[j * U + j].x));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) maxdiag = fmaxf(maxdiag, __shfl_xor_sync(0xffffffffu, maxdiag, o));
-  const float floor_ = 1e-14f * maxdiag;
+  // The reference's floor is ~45 fp64 ulps of the largest pivot.  The
+  // regularised Grams (kPev, kBias, kSolve: A = a0 I + a1 G, positive definite
+  // by construction) keep it; the unregularised ZF Gram takes the same 45 ulps
+  // in fp32, where an exactly rank-deficient G leaves a ~1e-7 rounding residue.
+  const float floor_ = (MODE == kZf ? 45.f * 1.1920929e-7f : 1e-14f) * maxdiag;
   bool singular = false;
   float tr = 0.f;
   if (UT > 0) {
@@ -304,6 +412,12 @@ __global__ void __launch_bounds__(128) gram_chol(const T* __restrict__ H, int P,
       }
     }
     __syncwarp();
+    singular = __any_sync(0xffffffffu, singular);  // pivot j was tested by lane j only
+    if constexpr (MODE >= kSolve) {  // Lr holds every row of L (row j published at step j)
+      solve_emit<T, MODE>([&](int i, int k) { return Lr[i * N + k]; }, H, V, p, NT, BC, U, scale, singular, xo,
+                          status, lane);
+      return;
+    }
     // X = L^{-1}: lane c holds column c; row i: X_ic = -(sum_{k=c}^{i-1} L_ik X_kc) / L_ii
     float2 x[N];
 #pragma unroll
@@ -346,6 +460,11 @@ __global__ void __launch_bounds__(128) gram_chol(const T* __restrict__ H, int P,
     __syncwarp();
     if (lane == 0) A[j * U + j] = make_float2(ljj, 0.f);
     __syncwarp();
+  }
+  if constexpr (MODE >= kSolve) {
+    solve_emit<T, MODE>([&](int i, int k) { return A[k * U + i]; }, H, V, p, NT, BC, U, scale, singular, xo, status,
+                        lane);
+    return;
   }
   // columns of L^-1: lane c solves L z = e_c (rows i >= c)
   for (int c = lane; c < U; c += 32) {
@@ -549,6 +668,10 @@ __global__ void bit_errors_kernel(const uint8_t* __restrict__ labels, const uint
   unsigned long long e = 0;
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (labels[i] == 0xff) {  // flagged downlink trial: half its bits count as errors (precode.cpp:219-223)
+      e += static_cast<unsigned>(bps / 2);
+      continue;
+    }
     unsigned ref = 0;
     for (int k = 0; k < bps; ++k) ref = (ref << 1) | (bits[i * bps + k] & 1u);
     e += __popc(ref ^ labels[i]);

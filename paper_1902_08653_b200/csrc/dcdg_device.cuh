@@ -168,6 +168,9 @@ enum StatusCode : uint32_t {
   ST_ZERO_BEAMFORMER = 2, // precode.cpp:107-108 runtime_error
   ST_SINGULAR = 3,        // numerics.cpp:55-56  runtime_error
   ST_BAD_VARIANCE = 4,    // detect.cpp:138-139  invalid_argument
+  ST_RANK_DEFICIENT = 5,  // precode.cpp:42-43   runtime_error (zf_exact)
+  ST_MF_ZERO_ENERGY = 6,  // detect.cpp:213-215  runtime_error (mf_detect)
+  ST_MF_ZERO_BEAMFORMER = 7,  // precode.cpp:193-196 runtime_error (mf_precode)
 };
 
 __device__ __forceinline__ void record_status(unsigned long long* st, long long p, uint32_t code, uint32_t detail) {

@@ -294,6 +294,60 @@ class Engine:
         labels = self.slice(r.xhat, beta, qam=qam, ex=ex, stream=stream)
         return r.xhat, labels, self.bit_errors(labels, bits, qam=qam, stream=stream)
 
+    # ---- BER-sweep building blocks (fp32) ----------------------------------
+    def synth(self, S: int, C: int, Bc: int, U: int, *, qam: int = 16, ex: float = 1.0, n0: float = 0.0,
+              seed: int = 1, first_trial: int = 0, uplink: bool = True, downlink: bool = False, stream=None):
+        """Device-side batch synthesis (dcdg_synth): returns a dict with
+        H [S, C, U, Bc] complex64, bits [S, U*log2(qam)] uint8, and
+        y [S, C, Bc] (uplink) / sym [S, U] + noise_dl [S, U] (downlink)."""
+        dev = self.device
+        bps = {4: 2, 16: 4, 64: 6}.get(qam, 0)
+        out = {"H": torch.empty((S, C, U, Bc), dtype=torch.complex64, device=dev),
+               "bits": torch.empty((S, U * max(bps, 1)), dtype=torch.uint8, device=dev)}
+        out["y"] = torch.empty((S, C, Bc), dtype=torch.complex64, device=dev) if uplink else None
+        out["sym"] = torch.empty((S, U), dtype=torch.complex64, device=dev) if downlink else None
+        out["noise_dl"] = torch.empty((S, U), dtype=torch.complex64, device=dev) if downlink else None
+        check(lib().dcdg_synth(self._ctx, S, C, Bc, U, qam, float(ex), float(n0), int(seed) & (2**64 - 1),
+                               int(first_trial) & (2**64 - 1), _ptr(out["H"]), _ptr(out["y"]), _ptr(out["bits"]),
+                               _ptr(out["sym"]), _ptr(out["noise_dl"]), self._stream(stream)))
+        return out
+
+    def mf_detect(self, H, y, stream=None):
+        """Matched-filter estimates [S, U] complex64 (mf_detect, detect.cpp:191-218)."""
+        _need(H, "H")
+        S, Cn, U, Bc = H.shape
+        x = torch.empty((S, U), dtype=torch.complex64, device=H.device)
+        check(lib().dcdg_mf_detect(self._ctx, _ptr(H), _ptr(y), S, Cn, Bc, U, _ptr(x), self._stream(stream)))
+        return x
+
+    def mf_precode(self, H, s, *, rho: float, stream=None):
+        """Matched-filter beamformer [S, C, Bc] (mf_precode, precode.cpp:171-202)."""
+        _need(H, "H")
+        S, Cn, U, Bc = H.shape
+        x = torch.empty((S, Cn, Bc), dtype=torch.complex64, device=H.device)
+        check(lib().dcdg_mf_precode(self._ctx, _ptr(H), _ptr(s), S, Cn, Bc, U, float(rho), _ptr(x),
+                                    self._stream(stream)))
+        return x
+
+    def lmmse_exact(self, H, y, *, n0: float, ex: float = 1.0, stream=None):
+        """Exact full-channel L-MMSE estimates [S, U] (lmmse_exact, detect.cpp:54-65)."""
+        _need(H, "H")
+        S, Cn, U, Bc = H.shape
+        x = torch.empty((S, U), dtype=torch.complex64, device=H.device)
+        check(lib().dcdg_lmmse_exact(self._ctx, _ptr(H), _ptr(y), S, Cn, Bc, U, float(n0), float(ex), _ptr(x),
+                                     self._stream(stream)))
+        return x
+
+    def zf_exact(self, H, s, *, rho: float, stream=None):
+        """Exact min-norm ZF beamformer scaled to rho (zf_exact + power_scale,
+        precode.cpp:31-50,101-111; rho == 0: raw), [S, C, Bc]."""
+        _need(H, "H")
+        S, Cn, U, Bc = H.shape
+        x = torch.empty((S, Cn, Bc), dtype=torch.complex64, device=H.device)
+        check(lib().dcdg_zf_exact(self._ctx, _ptr(H), _ptr(s), S, Cn, Bc, U, float(rho), _ptr(x),
+                                  self._stream(stream)))
+        return x
+
     def round_fp16(self, t, stream=None):
         """In-place binary16 rounding of an fp32/complex64 tensor (wire format)."""
         n = t.numel() * (2 if t.is_complex() else 1)

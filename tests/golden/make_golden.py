@@ -138,6 +138,23 @@ def compute(ref):
             lambda: ref.decentralized_cd_precode([cn(8, 32), cn(8, 32), cn(8, 4)], cn(8), 1.0, 3))
     capture("dec_detect_empty", lambda: ref.decentralized_cd_detect([], [], 0.1, 1.0, 3))
 
+    # --- matched-filter baselines (detect.cpp:191-218, precode.cpp:171-202);
+    # appended last so the earlier arrays keep their random draws
+    mh = [cn(32, 8) for _ in range(4)]
+    my = [cn(32) for _ in range(4)]
+    ms = cn(8)
+    out["mf_h"] = np.stack(mh)
+    out["mf_y"] = np.stack(my)
+    out["mf_s"] = ms
+    out["mf_detect"] = ref.mf_detect(mh, my)
+    out["mf_precode"] = ref.mf_precode([h.conj().T for h in mh], ms, np.sqrt(8))
+    mz = [h.copy() for h in mh]
+    for h in mz:
+        h[:, 3] = 0
+    capture("mf_zero_energy", lambda: ref.mf_detect(mz, my))
+    capture("mf_zero_beamformer", lambda: ref.mf_precode([np.zeros((8, 32), complex)] + [h.conj().T for h in mh[1:]],
+                                                          ms, 1.0))
+
     return out, errs
 
 
