@@ -131,3 +131,48 @@ def test_sweep_downlink_flags_and_orders(engine):
     pts = {p.method: p for p in run_ber_sweep(spec, engine)}
     assert pts["exact"].ber <= pts["dcd"].ber * 1.15 + 1e-4 < pts["mf"].ber
     assert pts["dcd"].flagged_trials == 0
+
+
+def test_exact_beats_matched_filter_at_high_snr(engine):
+    # test_harness.cpp:173-191
+    from paper_1902_08653_b200.harness import SweepSpec, run_ber_sweep
+    spec = SweepSpec(methods=("exact", "mf"), users=4, cluster_size=16, clusters=2, snr_db=(12.0,), min_bits=40000,
+                     seed=9)
+    pts = {p.method: p.ber for p in run_ber_sweep(spec, engine)}
+    assert pts["exact"] < pts["mf"] and pts["mf"] > 1e-3
+
+
+def test_downlink_zf_error_free_at_high_snr(engine):
+    # test_harness.cpp:193-208
+    from paper_1902_08653_b200.harness import SweepSpec, run_ber_sweep
+    spec = SweepSpec(direction="downlink", methods=("exact",), users=4, cluster_size=32, clusters=1,
+                     snr_db=(10.0, 30.0), min_bits=20000, seed=11)
+    pts = run_ber_sweep(spec, engine)
+    assert pts[1].ber <= pts[0].ber and pts[1].errors == 0 and pts[0].flagged_trials == 0
+
+
+def test_sweeps_are_reproducible_to_the_csv_bytes(engine, tmp_path):
+    # test_harness.cpp:140-171
+    from paper_1902_08653_b200.harness import SweepSpec, run_ber_sweep
+    spec = SweepSpec(methods=("dcd", "exact"), users=4, cluster_size=16, clusters=2, snr_db=(4.0, 8.0),
+                     t_max=(2,), min_bits=20000, seed=5)
+    a, b = tmp_path / "a.csv", tmp_path / "b.csv"
+    r1, r2 = run_ber_sweep(spec, engine, str(a)), run_ber_sweep(spec, engine, str(b))
+    assert [(p.errors, p.bits) for p in r1] == [(p.errors, p.bits) for p in r2]
+    assert a.read_bytes() == b.read_bytes() and len(r1) == 4
+    assert all(p.bits >= spec.min_bits for p in r1)
+
+
+@pytest.mark.parametrize("direction", ["uplink", "downlink"])
+def test_convergence_study_medians_shrink(engine, direction):
+    # test_harness.cpp:242-262 (fp32 floor instead of fp64)
+    from paper_1902_08653_b200.harness import SweepSpec, run_convergence_study
+    spec = SweepSpec(direction=direction, users=8, cluster_size=32, clusters=1, snr_db=(8.0,), t_max=(6,),
+                     min_bits=10000, seed=13)
+    pts = run_convergence_study(spec, engine, instances=40)
+    assert [p.t for p in pts] == list(range(1, 7))
+    for i, p in enumerate(pts):
+        assert 0.0 <= p.median <= p.p95
+        if i:
+            assert p.median <= pts[i - 1].median * (1 + 1e-6) + 2e-6
+    assert pts[-1].median < 0.05 * pts[0].median
