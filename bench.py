@@ -248,6 +248,7 @@ def run_ours(args):
     eng.sync()
     barrier()
     l0 = eng.launches
+    tr0 = (dcd.traffic.uplink_payload_bytes, dcd.traffic.uplink_bus_bytes, dcd.traffic.messages)
     e0, e1 = _ev(), _ev()
     with ClockSampler(local_rank) as clk:
         barrier()
@@ -258,6 +259,18 @@ def run_ours(args):
         e1.record(stream)
         barrier()
     launches = (eng.launches - l0) // max(args.steps, 1)
+    ksteps = max(args.steps, 1)
+    pay = (dcd.traffic.uplink_payload_bytes - tr0[0]) // ksteps
+    bus = (dcd.traffic.uplink_bus_bytes - tr0[1]) // ksteps
+    interconnect = {
+        "payload_bytes_per_step_per_gpu": int(pay), "bus_bytes_per_step_per_gpu": int(bus),
+        "messages_per_step_per_gpu": int((dcd.traffic.messages - tr0[2]) // ksteps),
+        "model_total_bytes_per_step": int(pay * world),
+        "raw_sample_forwarding_bytes_per_step": int(S_total * B * esz),
+        "reduction_ratio": round(pay * world / (S_total * B * esz), 4),
+        "note": "payload = the reference's MessageLog model for this GPU's clusters (U complex per cluster and "
+                "subcarrier); bus = bytes the issued NCCL collectives move per GPU (NCCL-tests bus factors); "
+                "0 at N=1 (no collective)"}
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -372,6 +385,7 @@ def run_ours(args):
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
+        "interconnect": interconnect,
     }
     if extra:
         line["extra"] = extra

@@ -33,7 +33,7 @@ partitioning and collectives on the gloo backend.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import torch
 import torch.distributed as dist
@@ -109,6 +109,65 @@ class _Groups:
 
 
 # ---------------------------------------------------------------------------
+# interconnect accounting
+# ---------------------------------------------------------------------------
+def bytes_per_complex(t: torch.Tensor) -> int:
+    """Wire size of one complex element of a payload tensor (precision.cpp:8-15):
+    complex128 16, complex64 8, binary16 pair 4."""
+    if t.dtype == torch.complex128:
+        return 16
+    if t.dtype == torch.complex64:
+        return 8
+    if t.dtype == torch.float16:
+        return 4
+    raise ValueError(f"no complex wire format for {t.dtype}")
+
+
+@dataclass
+class Traffic:
+    """What this rank's exchanges moved.
+
+    payload: the reference's MessageLog model (make_message, cluster.cpp:9-22)
+      for this rank's clusters: uplink U complex (+1 real for optimal fusion)
+      per cluster and subcarrier, downlink U complex per cluster and
+      subcarrier (the symbol broadcast).
+    bus: bytes per rank on the interconnect for the collectives actually issued,
+      with the NCCL-tests bus-bandwidth factors: reduce-scatter / all-to-all
+      (W-1)/W of the buffer, broadcast the buffer, all-reduce 2(W-1)/W."""
+    uplink_payload_bytes: int = 0
+    downlink_payload_bytes: int = 0
+    uplink_bus_bytes: int = 0
+    downlink_bus_bytes: int = 0
+    messages: int = 0
+    collectives: list = field(default_factory=list)
+
+    def add_bus(self, kind: str, nbytes: int, world: int, uplink: bool):
+        f = {"reduce_scatter": (world - 1) / world, "all_to_all": (world - 1) / world, "broadcast": 1.0,
+             "all_reduce": 2 * (world - 1) / world}[kind] if world > 1 else 0.0
+        b = int(round(f * nbytes))
+        if uplink:
+            self.uplink_bus_bytes += b
+        else:
+            self.downlink_bus_bytes += b
+        self.collectives.append((kind, nbytes))
+
+
+def interconnect_summary(traffic, total_antennas: int, subcarriers: int, bpc: int) -> dict:
+    """interconnect_summary (cluster.cpp:42-68) over one or more ranks' Traffic:
+    totals of the message model and the reduction ratio against forwarding every
+    antenna sample (B * S complex); plus the bus bytes actually moved."""
+    ts = traffic if isinstance(traffic, (list, tuple)) else [traffic]
+    up = sum(t.uplink_payload_bytes for t in ts)
+    down = sum(t.downlink_payload_bytes for t in ts)
+    base = total_antennas * subcarriers * bpc
+    return {"messages": sum(t.messages for t in ts), "uplink_bytes": up, "downlink_bytes": down,
+            "total_bytes": up + down, "baseline_bytes": base,
+            "reduction_ratio": (up + down) / base if base else 0.0,
+            "uplink_bus_bytes": sum(t.uplink_bus_bytes for t in ts),
+            "downlink_bus_bytes": sum(t.downlink_bus_bytes for t in ts)}
+
+
+# ---------------------------------------------------------------------------
 # per-rank compute back-ends
 # ---------------------------------------------------------------------------
 class CudaCompute:
@@ -147,6 +206,12 @@ class DistributedCD:
         self.compute = compute
         self.mode = mode
         self._groups = _Groups(part)
+        self.traffic = Traffic()
+
+    def _log_uplink(self, S_local: int, U: int, bpc: int, optimal: bool):
+        p = self.part
+        self.traffic.uplink_payload_bytes += S_local * p.C_local * (U * bpc + (bpc // 2 if optimal else 0))
+        self.traffic.messages += S_local * p.C_local
 
     # ---- uplink -----------------------------------------------------------
     def uplink(self, H, y, *, n0, ex=1.0, K=3, fusion="uniform", async_op=False):
@@ -157,6 +222,8 @@ class DistributedCD:
         p = self.part
         if p.world == 1:
             xl, s2 = self.compute.ul_local(H, y, n0=n0, ex=ex, K=K, fusion=fusion)
+            self._log_uplink(xl.shape[0], xl.shape[-1] if xl.dtype != torch.float16 else xl.shape[-2],
+                             bytes_per_complex(xl), fusion == "optimal")
             out = self.compute.fuse(xl, s2, fusion=fusion, C_total=p.C_total)
             return _Deferred(None, lambda: out) if async_op else out
         if self.mode == "gather" and p.world <= p.C_total:
@@ -164,6 +231,7 @@ class DistributedCD:
         part_sum, wsum, _, _ = self.compute.ul_partial(H, y, n0=n0, ex=ex, K=K, fusion=fusion, C_total=p.C_total,
                                                        want_local=False)
         U = part_sum.shape[-1]
+        self._log_uplink(part_sum.shape[0], U, bytes_per_complex(part_sum), fusion == "optimal")
         flat = torch.view_as_real(part_sum).reshape(part_sum.shape[0], 2 * U)
         if fusion == "optimal":
             flat = torch.cat([flat, wsum.reshape(-1, 1), torch.zeros_like(wsum).reshape(-1, 1)], dim=1)
@@ -172,6 +240,7 @@ class DistributedCD:
         out = torch.empty((rows, flat.shape[1]), dtype=flat.dtype, device=flat.device)
         work = dist.reduce_scatter_tensor(out.reshape(-1), flat.contiguous().reshape(-1), op=dist.ReduceOp.SUM,
                                           group=self._groups.group, async_op=async_op)
+        self.traffic.add_bus("reduce_scatter", flat.numel() * flat.element_size(), W, True)
 
         def finish():
             if fusion == "optimal":
@@ -186,8 +255,10 @@ class DistributedCD:
     def _uplink_gather(self, H, y, *, n0, ex, K, fusion, async_op):
         p = self.part
         xl, s2 = self.compute.ul_local(H, y, n0=n0, ex=ex, K=K, fusion=fusion)
+        self._log_uplink(xl.shape[0], xl.shape[2], bytes_per_complex(xl), fusion == "optimal")
         # x_local [S, C_loc, U] (complex64 or f16 pairs) -> chunk r of the subcarriers to rank r
         send = xl.contiguous()
+        self.traffic.add_bus("all_to_all", send.numel() * send.element_size(), p.world, True)
         recv = torch.empty_like(send)
         dist.all_to_all_single(recv.reshape(-1) if recv.dtype != torch.complex64 else torch.view_as_real(recv).reshape(-1),
                                send.reshape(-1) if send.dtype != torch.complex64 else torch.view_as_real(send).reshape(-1))
@@ -198,6 +269,7 @@ class DistributedCD:
         sig = None
         if fusion == "optimal":
             ssend = s2.contiguous()
+            self.traffic.add_bus("all_to_all", ssend.numel() * ssend.element_size(), p.world, True)
             srecv = torch.empty_like(ssend)
             dist.all_to_all_single(srecv.reshape(-1), ssend.reshape(-1))
             sig = srecv.reshape(p.world, chunk, p.C_local).transpose(0, 1).reshape(chunk, p.C_total).contiguous()
@@ -208,7 +280,9 @@ class DistributedCD:
     def broadcast_symbols(self, s_root, *, src=0):
         """Root's [S, U] symbol batch to every rank (the centre -> cluster
         broadcast, src/cluster.cpp:256-259)."""
-        dist.broadcast(s_root if s_root.dtype != torch.complex64 else torch.view_as_real(s_root), src)
+        buf = s_root if not s_root.is_complex() else torch.view_as_real(s_root)
+        dist.broadcast(buf, src)
+        self.traffic.add_bus("broadcast", buf.numel() * buf.element_size(), self.part.world, False)
         return s_root
 
     def downlink(self, H, s, *, rho, K=3):
@@ -216,11 +290,15 @@ class DistributedCD:
         (x_local [S_local, C_local, Bc], effective gain [S] on every rank)."""
         p = self.part
         s_mine = s[p.s_lo:p.s_hi].contiguous()
+        U = s.shape[1]
+        self.traffic.downlink_payload_bytes += s_mine.shape[0] * p.C_local * U * bytes_per_complex(s)
+        self.traffic.messages += s_mine.shape[0] * p.C_local
         x, gpart = self.compute.dl(H, s_mine, rho=rho, K=K, C_total=p.C_total)
         num = torch.zeros((p.S,), dtype=torch.float32, device=gpart.device)
         num[p.s_lo:p.s_hi] = gpart.sum(dim=1)
         if p.world > 1:
             dist.all_reduce(num)
+            self.traffic.add_bus("all_reduce", num.numel() * num.element_size(), p.world, False)
         sf = s.float() if s.dtype == torch.float16 else torch.view_as_real(s)
         se = (sf.reshape(p.S, -1) ** 2).sum(dim=1)
         gain = torch.where(se > 0, num / torch.where(se > 0, se, torch.ones_like(se)), torch.zeros_like(se))

@@ -97,8 +97,9 @@ def _worker(rank, world, port, C, Bc, U, S, mode, fusion, q):
                                                                                      dtype=torch.complex128)
         s = eng.broadcast_symbols(s_root)
         x, gain = eng.downlink(H, s, rho=float(np.sqrt(U)), K=3)
+        t = eng.traffic
         q.put((rank, part.own_lo, part.own_hi, xh.numpy(), part.s_lo, part.s_hi, part.c_lo, part.c_hi, x.numpy(),
-               gain.numpy()))
+               gain.numpy(), {k: v for k, v in vars(t).items() if k != "collectives"}))
     finally:
         dist.destroy_process_group()
 
@@ -133,7 +134,7 @@ def test_distributed_matches_single_process_reference(world, C, mode, fusion, po
     x_ref, g_ref = port.dl_precode_batch(b["h_tiles"], b["x_true"], float(np.sqrt(U)), 3)
     res = _run(world, C, Bc, U, S, mode, fusion)
     covered = np.zeros(S, bool)
-    for (rank, lo, hi, xh, s_lo, s_hi, c_lo, c_hi, x, gain) in res:
+    for (rank, lo, hi, xh, s_lo, s_hi, c_lo, c_hi, x, gain, _) in res:
         assert np.allclose(xh, xhat_ref[lo:hi], rtol=0, atol=1e-12), (rank, np.abs(xh - xhat_ref[lo:hi]).max())
         covered[lo:hi] = True
         assert np.allclose(x, x_ref[s_lo:s_hi, c_lo:c_hi], rtol=0, atol=1e-12)
@@ -153,3 +154,25 @@ def test_partition_layouts():
         partition(8, 3, 0, 16)
     with pytest.raises(ValueError):
         partition(8, 2, 0, 15)
+
+
+def test_interconnect_accounting_matches_the_message_model():
+    """the payload each rank's clusters put on the
+    interconnect equals the reference's MessageLog model (test_cluster.cpp:201-230
+    KAT: B=128, C=4, U=8, 1200 subcarriers -> 307200 bytes in fp32; the CPU
+    stand-in exchanges complex128, i.e. the fp64 model, twice that), and the
+    bus bytes follow the collectives actually issued."""
+    from paper_1902_08653_b200.distributed import Traffic, interconnect_summary
+    S, C, Bc, U, W = 1200, 4, 32, 8, 2
+    res = _run(W, C, Bc, U, S, "gather", "uniform")
+    tr = []
+    for r in res:
+        t = Traffic(**r[-1])
+        tr.append(t)
+        assert t.uplink_bus_bytes == (S // W) * W * (C // W) * U * 16 // 2  # all-to-all of x_local, half stays local
+        assert t.downlink_bus_bytes == S * U * 16 + 2 * (W - 1) * S * 4 // W  # symbol broadcast + gain all-reduce
+    summ = interconnect_summary(tr, total_antennas=C * Bc, subcarriers=S, bpc=16)
+    assert summ["uplink_bytes"] == 2 * 307200
+    assert summ["downlink_bytes"] == S * C * U * 16
+    assert summ["messages"] == 2 * S * C
+    assert summ["reduction_ratio"] == pytest.approx(2 * U / Bc / 1)  # (U up + U down) per cluster vs B_c samples
