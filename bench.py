@@ -336,8 +336,26 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms = float(t.item())
     h2d = H.numel() * H.element_size() + y.numel() * y.element_size()
+
+    # the same host->device bytes with no compute: the PCIe bound of the e2e step
+    def copy_only():
+        for i in range(n_chunks):
+            with torch.cuda.stream(copy_st):
+                Hd[i * cs:(i + 1) * cs].copy_(Hh[i * cs:(i + 1) * cs], non_blocking=True)
+                yd[i * cs:(i + 1) * cs].copy_(yh[i * cs:(i + 1) * cs], non_blocking=True)
+    copy_only()
+    torch.cuda.synchronize(dev)
+    c0, c1 = _ev(), _ev()
+    c0.record(copy_st)
+    for _ in range(n_e2e):
+        copy_only()
+    c1.record(copy_st)
+    torch.cuda.synchronize(dev)
+    c_ms = c0.elapsed_time(c1) / n_e2e
     e2e = {"value": round(S_total * U * BITS / (e_ms * 1e-3) / 1e9, 5), "unit": "Gbps", "ms_per_step": round(e_ms, 4),
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(own * U * 8),
+           "h2d_copy_only_ms": round(c_ms, 4), "h2d_GBps": round(h2d / (c_ms * 1e-3) / 1e9, 2),
+           "frac_of_copy_bound": round(c_ms / e_ms, 4),
            "path": "Engine.ul_detect (C ABI dcdg_ul_detect): pinned host H,y -> device in %d chunks on a copy "
                    "stream overlapped with detection -> host fused estimates" % n_chunks}
 

@@ -1,11 +1,12 @@
-"""Launch the CD kernels a few times at the north-star shape for ncu capture.
-usage: python scripts/prof_kernel.py [ul|dl] [fp32|fp16] [reps] [S]"""
+"""Launch one CD-path kernel a few times for an ncu capture.
+usage: python scripts/prof_kernel.py [ul|dl|pev] [fp32|fp16] [reps] [S] [C B_c U]
+Default shape: the north star (C=8, B_c=32, U=16, S=16800 -> 134 400 problems);
+other shapes are synthesised on the device (dcdg_synth)."""
+import math
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import math  # noqa: E402
-
 import torch  # noqa: E402
 
 from bench import make_inputs  # noqa: E402
@@ -17,7 +18,13 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 4
 S = int(sys.argv[4]) if len(sys.argv) > 4 else 16800
 dev = torch.device("cuda", 0)
 eng = Engine(0)
-H, y, x, n0 = make_inputs(S, 8, dev, 1)
+if len(sys.argv) > 7:
+    C, Bc, U = (int(v) for v in sys.argv[5:8])
+    b = eng.synth(S, C, Bc, U, qam=16, n0=U / 10.0, seed=1, uplink=True, downlink=True)
+    H, y, x, n0 = b["H"], b["y"], b["sym"], U / 10.0
+else:
+    U = 16
+    H, y, x, n0 = make_inputs(S, 8, dev, 1)
 if fmt == "fp16":
     H, y, x = to_fp16_pairs(H), to_fp16_pairs(y), to_fp16(x)
 for _ in range(reps):
@@ -26,7 +33,7 @@ for _ in range(reps):
     elif direction == "pev":
         eng.post_eq_variance(H, n0=n0)
     else:
-        eng.dl_precode(H, x, rho=math.sqrt(16), K=3, want_gain=False)
+        eng.dl_precode(H, x, rho=math.sqrt(U), K=3, want_gain=False)
 eng.sync()
 torch.cuda.synchronize()
 print("done", direction, fmt, eng.launches)
