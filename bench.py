@@ -204,10 +204,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_ONE_GPU=1 (harness self-test only): every rank on cuda:0 with the gloo
+    # control plane, so the multi-rank p2p path runs on a one-GPU box
+    one_gpu = os.environ.get("BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     S_total = args.S * world  # weak scaling: per-GPU work fixed at args.S * C problems
     part = partition(C, world, rank, S_total)
     fmt = args.fmt
@@ -221,61 +229,83 @@ def run_ours(args):
     P = part.S_local * part.C_local
     stream = torch.cuda.current_stream(dev)
 
-    # Multi-GPU: the fusion collective of batch i is left in flight while batch
-    # i+1's detection kernel runs (NCCL stream vs compute stream); it is waited
-    # on only when the next batch has been launched.
-    pending = []
-
-    def step():
-        h = dcd.uplink(H, y, n0=n0, K=K_SWEEPS, fusion=args.fusion, async_op=world > 1)
-        if world > 1:
-            if pending:
-                pending.pop().wait()
-            pending.append(h)
-
-    def drain():
-        while pending:
-            pending.pop().wait()
-
+    # Multi-GPU: with the NCCL modes the fusion collective of batch i is left in
+    # flight while batch i+1's detection kernel runs (NCCL stream vs compute
+    # stream) and is waited on only when the next batch has been launched.  The
+    # p2p mode has no collective: the CD kernel stores into the owners' windows.
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    for _ in range(args.warmup):
-        step()
-    drain()
-    eng.sync()
-    barrier()
-    l0 = eng.launches
-    tr0 = (dcd.traffic.uplink_payload_bytes, dcd.traffic.uplink_bus_bytes, dcd.traffic.messages)
-    e0, e1 = _ev(), _ev()
-    with ClockSampler(local_rank) as clk:
-        barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
+    def timed(d, steps, warmup, sample_clocks=False):
+        pending = []
+
+        def step():
+            h = d.uplink(H, y, n0=n0, K=K_SWEEPS, fusion=args.fusion, async_op=world > 1)
+            if world > 1:
+                if pending:
+                    pending.pop().wait()
+                pending.append(h)
+
+        def drain():
+            while pending:
+                pending.pop().wait()
+
+        for _ in range(warmup):
             step()
         drain()
-        e1.record(stream)
+        eng.sync()
         barrier()
-    launches = (eng.launches - l0) // max(args.steps, 1)
-    ksteps = max(args.steps, 1)
-    pay = (dcd.traffic.uplink_payload_bytes - tr0[0]) // ksteps
-    bus = (dcd.traffic.uplink_bus_bytes - tr0[1]) // ksteps
+        l_a = eng.launches
+        tr_a = (d.traffic.uplink_payload_bytes, d.traffic.uplink_bus_bytes, d.traffic.messages)
+        e0, e1 = _ev(), _ev()
+        clk = ClockSampler(local_rank) if sample_clocks else None
+        if clk:
+            clk.__enter__()
+        try:
+            barrier()
+            e0.record(stream)
+            for _ in range(steps):
+                step()
+            drain()
+            e1.record(stream)
+            barrier()
+        finally:
+            if clk:
+                clk.__exit__(None, None, None)
+        n_launch = (eng.launches - l_a) // max(steps, 1)
+        tr = tuple((b - a) // max(steps, 1) for a, b in zip(
+            tr_a, (d.traffic.uplink_payload_bytes, d.traffic.uplink_bus_bytes, d.traffic.messages)))
+        t = e0.elapsed_time(e1) / steps
+        if world > 1:
+            tt = torch.tensor([t], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t, clk, n_launch, tr
+
+    # (p2p: the first warm-up step maps the exchange windows, a one-time IPC handshake)
+    ms, clk, launches, (pay, bus, msgs) = timed(dcd, args.steps, args.warmup, sample_clocks=True)
+    compare = None
+    if world > 1:
+        # the same step with the NCCL exchange of the other mode, for comparison
+        other = "reduce" if args.mode == "p2p" else "p2p"
+        try:
+            d2 = DistributedCD(part, CudaCompute(eng), mode=other)
+            ms2 = timed(d2, args.steps, args.warmup)[0]
+            compare = {"mode": other, "ms_per_step": round(ms2, 5),
+                       "value": round(S_total * U * BITS / (ms2 * 1e-3) / 1e9, 4), "unit": "Gbps"}
+        except Exception as e:  # reported, never silently substituted for the main line
+            compare = {"mode": other, "error": str(e)[:200]}
     interconnect = {
         "payload_bytes_per_step_per_gpu": int(pay), "bus_bytes_per_step_per_gpu": int(bus),
-        "messages_per_step_per_gpu": int((dcd.traffic.messages - tr0[2]) // ksteps),
+        "messages_per_step_per_gpu": int(msgs),
         "model_total_bytes_per_step": int(pay * world),
         "raw_sample_forwarding_bytes_per_step": int(S_total * B * esz),
         "reduction_ratio": round(pay * world / (S_total * B * esz), 4),
         "note": "payload = the reference's MessageLog model for this GPU's clusters (U complex per cluster and "
-                "subcarrier); bus = bytes the issued NCCL collectives move per GPU (NCCL-tests bus factors); "
-                "0 at N=1 (no collective)"}
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+                "subcarrier); bus = bytes this GPU sends to its peers per step (p2p: the estimates its CD kernel "
+                "stores into other GPUs' exchange windows; NCCL modes: the collective's bus factor); 0 at N=1"}
     value = S_total * U * BITS / (ms * 1e-3) / 1e9  # whole-job Gbps: S_total subcarrier-symbols detected per step
 
     # dominant kernel alone (the CD kernel, same stream) for the roofline
@@ -392,7 +422,8 @@ def run_ours(args):
         "config": {"workload": f"uplink CD L-MMSE detection + {args.fusion} fusion (configs[1])",
                    "B": B, "U": U, "C": C, "B_c": BC, "K": K_SWEEPS, "qam": QAM, "fmt": fmt,
                    "subcarrier_symbols_per_step": S_total, "problems_per_gpu": P, "clusters_per_gpu": part.C_local,
-                   "parallelism": (f"clusters/{world}, fusion {args.mode}" if world > 1 else "single GPU, all clusters"),
+                   "parallelism": (f"clusters/{world}, fusion exchange {args.mode}" if world > 1
+                                   else "single GPU, all clusters"),
                    "l2": f"inputs {alg / 1e6:.0f} MB/GPU > 126 MB L2, no flush needed",
                    "kernel": kernel_name("ul", BC, U, fmt)},
         "batch_latency_ms": round(ms, 5),
@@ -405,6 +436,8 @@ def run_ours(args):
         "clocks": clk.summary(),
         "interconnect": interconnect,
     }
+    if compare:
+        line["exchange_comparison"] = compare
     if extra:
         line["extra"] = extra
     if world == 1 and not args.no_cpu:
@@ -520,7 +553,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--fast", action="store_true", help="skip the secondary (DL, fp16, optimal) lines")
-    ap.add_argument("--mode", choices=["reduce", "gather"], default="reduce", help="multi-GPU fusion exchange")
+    ap.add_argument("--mode", choices=["p2p", "reduce", "gather"], default="p2p",
+                    help="multi-GPU fusion exchange: p2p = fused into the CD kernel over peer memory (NVLink), "
+                         "reduce/gather = NCCL reduce-scatter / all-to-all after the CD kernel")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -231,6 +231,40 @@ int dcdg_convert(dcdg_ctx* ctx, const void* src, int src_fmt, void* dst, int dst
  * writes a short name ("ul_f32_reg<32,16,8>", "ul_generic_f32", …). */
 int dcdg_kernel_name(int direction /*0 UL, 1 DL*/, int Bc, int U, int fmt, char* buf, int len);
 
+/* ---- fused cross-GPU exchange over peer memory (NVLink P2P) ----------------
+ * Replaces "CD kernel, then an NCCL collective" for the uplink fusion of
+ * decentralized_cd_detect (detect.cpp:164-187) across the GPUs of one node:
+ * the CD kernel's epilogue stores each cluster estimate x_c of subcarrier s
+ * straight into the exchange window of the rank that owns s, its last CTA
+ * publishes the batch epoch to every owner (system-scope release), and the
+ * owner's fusion kernel waits for all ranks' epochs and sums the C_total
+ * estimates in ascending cluster order — bitwise the single-GPU result.
+ * One process per GPU; windows are exported with CUDA IPC.
+ *
+ *   dcdg_xwin_create  allocate this rank's window: 2 parity buffers of
+ *                     buf_bytes >= S_own*C_total*U*bytes_per_complex (+256-B
+ *                     pad + S_own*C_total*4 for optimal fusion), S_own = S/world
+ *   dcdg_xwin_handle  DCDG_XWIN_HANDLE_BYTES opaque bytes to send to the peers
+ *   dcdg_xwin_open    map peer `peer`'s window from its handle
+ * Every rank must issue the same sequence of dcdg_ul_detect_xchg calls (the
+ * epoch is a per-window call counter), on one stream per window.  A rank whose
+ * peers never publish gets DCDG_ECUDA from dcdg_sync_status after the window
+ * timeout (default 20 s), not a hang. */
+#define DCDG_XWIN_HANDLE_BYTES 64
+typedef struct dcdg_xwin dcdg_xwin;
+int dcdg_xwin_create(dcdg_ctx* ctx, int world, int rank, int64_t buf_bytes, dcdg_xwin** out);
+int dcdg_xwin_handle(dcdg_xwin* w, void* handle);
+int dcdg_xwin_open(dcdg_xwin* w, int peer, const void* handle);
+int dcdg_xwin_set_timeout(dcdg_xwin* w, int64_t timeout_ns);
+int dcdg_xwin_destroy(dcdg_xwin* w);
+/* Uplink detection of this rank's C clusters [c0, c0+C) of C_total over all S
+ * subcarriers (H [S][C][U][B_c], y [S][C][B_c] as in dcdg_ul_detect), fused
+ * through the windows: xhat [S/world][U] receives the fused estimates of the
+ * subcarriers this rank owns, [rank*S/world, (rank+1)*S/world). */
+int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* y, int S, int C, int c0,
+                        int C_total, int Bc, int U, int K, double n0, double ex, int fmt, int fusion,
+                        float* xhat, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,9 +8,9 @@ compute path is libdcdg.so.  There is no CPU fallback.
 """
 from ._lib import (FP16, FP32, FUSION_OPTIMAL, FUSION_UNIFORM, CudaError, DcdgError, InvalidArgument,  # noqa: F401
                    NumericError)
-from .engine import (DownlinkResult, Engine, GraphedUplink, UplinkResult, complex_empty, from_fp16_pairs,  # noqa: F401
+from .engine import (DownlinkResult, Engine, ExchangeWindow, GraphedUplink, UplinkResult, complex_empty, from_fp16_pairs,  # noqa: F401
                      kernel_name, to_complex64, to_fp16, to_fp16_pairs)
 
-__all__ = ["Engine", "GraphedUplink", "UplinkResult", "DownlinkResult", "FP32", "FP16", "FUSION_OPTIMAL", "FUSION_UNIFORM",
+__all__ = ["Engine", "ExchangeWindow", "GraphedUplink", "UplinkResult", "DownlinkResult", "FP32", "FP16", "FUSION_OPTIMAL", "FUSION_UNIFORM",
            "DcdgError", "InvalidArgument", "NumericError", "CudaError", "kernel_name", "to_fp16", "to_fp16_pairs", "from_fp16_pairs", "to_complex64",
            "complex_empty"]

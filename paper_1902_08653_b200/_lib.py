@@ -80,7 +80,16 @@ SIGNATURES = {
                                    _vp]),
     "dcdg_zf_exact": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _vp, _vp]),
     "dcdg_kernel_name": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int]),
+    "dcdg_xwin_create": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int64, C.POINTER(_vp)]),
+    "dcdg_xwin_handle": (C.c_int, [_vp, _vp]),
+    "dcdg_xwin_open": (C.c_int, [_vp, C.c_int, _vp]),
+    "dcdg_xwin_set_timeout": (C.c_int, [_vp, C.c_int64]),
+    "dcdg_xwin_destroy": (C.c_int, [_vp]),
+    "dcdg_ul_detect_xchg": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _vp, _vp]),
 }
+
+XWIN_HANDLE_BYTES = 64
 
 _lib = None
 

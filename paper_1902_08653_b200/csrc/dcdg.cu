@@ -26,6 +26,21 @@ struct dcdg_ctx {
   size_t scratch_bytes = 0;
 };
 
+// Exchange window of one rank (dcdg_ul_detect_xchg): [flags][parity 0][parity 1]
+// in device memory exported by CUDA IPC; the peers' windows are mapped into
+// this process (NVLink P2P between GPUs, plain device memory on one GPU).
+struct dcdg_xwin {
+  dcdg_ctx* ctx = nullptr;
+  int world = 1, rank = 0;
+  long long buf_bytes = 0;  // one parity buffer
+  unsigned char* base = nullptr;
+  unsigned char* peer[dcdg::kXchgMaxRanks] = {};
+  bool opened[dcdg::kXchgMaxRanks] = {};
+  unsigned int* counter = nullptr;
+  unsigned long long epoch = 0;
+  long long timeout_ns = 20000000000LL;  // 20 s: a missing peer becomes ST_XCHG_TIMEOUT, not a hang
+};
+
 namespace {
 
 thread_local std::string g_err;
@@ -80,7 +95,8 @@ int occupancy_of(Kern kern, size_t smem, int threads = 32 * kWarps) {
   return occ;
 }
 
-using UlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, float, void*, cudaStream_t);
+using UlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, float, void*, const dcdg::XMap*,
+                                 cudaStream_t);
 using DlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, int, float, void*, float*,
                                  cudaStream_t);
 
@@ -95,35 +111,42 @@ using DlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, 
 #ifndef DCDG_LB_UL_MW
 #define DCDG_LB_UL_MW DCDG_LB_UL_WIDE
 #endif
+// xm != nullptr: the fused-exchange instantiation (estimates stored into the
+// owners' exchange windows, last CTA signals; dcdg_ul_detect_xchg).
 template <int BC, int U, int G, int MINB>
 cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
-                          cudaStream_t st) {
+                          const dcdg::XMap* xm, cudaStream_t st) {
   constexpr int NPW = 32 / G;
   constexpr int LBW = G >= 32 ? DCDG_LB_UL_WIDE : DCDG_LB_UL;
   constexpr int LB = (U % LBW == 0) ? LBW : 2;
   constexpr size_t smem =
       dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U, LB), NPW, kWarps>::kBytes;
-  auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps, MINB, LB>;
+  auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps, MINB, LB, false>;
+  auto kx = dcdg::ul_reg_f32<BC, U, G, kWarps, MINB, LB, true>;
   static const int occ = occupancy_of(kern, smem);
+  static const int occx = occupancy_of(kx, smem);
   const int nsets = (P + NPW - 1) / NPW;
-  const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
-  kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K, kappa,
-                                          static_cast<float2*>(X));
+  const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * (xm ? occx : occ));
+  (xm ? kx : kern)<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P,
+                                                       K, kappa, static_cast<float2*>(X), xm ? *xm : dcdg::XMap{});
   return cudaGetLastError();
 }
 
 template <int BC, int U, int G, int MINB>
 cudaError_t launch_ul_f16(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
-                          cudaStream_t st) {
+                          const dcdg::XMap* xm, cudaStream_t st) {
   constexpr int NPW = 32 / G;
   constexpr size_t smem =
       dcdg::CtaSmem<NPW*(BC * U * 4 + BC * 4), dcdg::ul_scal_bytes(U), NPW, kWarps>::kBytes;
-  auto kern = dcdg::ul_reg_f16<BC, U, G, kWarps, MINB>;
+  auto kern = dcdg::ul_reg_f16<BC, U, G, kWarps, MINB, false>;
+  auto kx = dcdg::ul_reg_f16<BC, U, G, kWarps, MINB, true>;
   static const int occ = occupancy_of(kern, smem);
+  static const int occx = occupancy_of(kx, smem);
   const int nsets = (P + NPW - 1) / NPW;
-  const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
-  kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(Y), P, K, kappa,
-                                          static_cast<__half2*>(X));
+  const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * (xm ? occx : occ));
+  (xm ? kx : kern)<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(Y),
+                                                       P, K, kappa, static_cast<__half2*>(X),
+                                                       xm ? *xm : dcdg::XMap{});
   return cudaGetLastError();
 }
 
@@ -174,6 +197,7 @@ cudaError_t launch_dl_f16(dcdg_ctx* ctx, const void* H, const void* S, int P, in
 // Multi-warp kernels (one CTA of NW warps per problem, dcdg_mw_kernels.cuh)
 template <int BC, int U, int NW, int MINB>
 cudaError_t launch_ul_mw(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                         const dcdg::XMap* /*no exchange epilogue: dcdg_ul_detect_xchg uses xchg_put_kernel*/,
                          cudaStream_t st) {
   constexpr int LB = DCDG_LB_UL_MW;
   constexpr size_t smem = dcdg::MwSmem<dcdg::ul_mw_slot_bytes(BC, U, NW), dcdg::ul_scal_bytes(U, LB), NW,
@@ -459,6 +483,9 @@ int dcdg_sync_status(dcdg_ctx* ctx, void* stream) {
     case dcdg::ST_MF_ZERO_BEAMFORMER:
       g_err = "mf_precode: cluster " + std::to_string(detail) + " produced a zero beamformer";
       return DCDG_ENUMERIC;
+    case dcdg::ST_XCHG_TIMEOUT:
+      g_err = "dcdg_ul_detect_xchg: rank " + std::to_string(detail) + " never published this batch";
+      return DCDG_ECUDA;
     default:
       g_err = "dcdg: unknown device status";
       return DCDG_ENUMERIC;
@@ -507,7 +534,7 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
   const float kappa = static_cast<float>(n0 / ex);
   const Spec* spec = find_spec(Bc, U, fmt);
   if (spec) {
-    CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, x_local, st), "ul_detect launch");
+    CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, x_local, nullptr, st), "ul_detect launch");
   } else {
     const size_t smem = 4 * (static_cast<size_t>(Bc) + 2 * U) * sizeof(float2);
     const long long blocks = (P + 3) / 4;
@@ -891,6 +918,172 @@ int dcdg_zf_exact(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, int
   CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
   return launch_solve<dcdg::kZf>(ctx, H, s, S, C, Bc, U, 0.f, static_cast<float>(rho),
                                  reinterpret_cast<float2*>(x_dl), as_stream(stream));
+}
+
+/* ---- fused cross-GPU exchange over peer memory ---------------------------- */
+int dcdg_xwin_create(dcdg_ctx* ctx, int world, int rank, int64_t buf_bytes, dcdg_xwin** out) {
+  if (!out) return fail(DCDG_EINVAL, "dcdg_xwin_create: null output");
+  *out = nullptr;
+  if (world < 1 || world > dcdg::kXchgMaxRanks || rank < 0 || rank >= world)
+    return fail(DCDG_EINVAL, "dcdg_xwin_create: need 1 <= world <= 8 and 0 <= rank < world");
+  if (buf_bytes <= 0) return fail(DCDG_EINVAL, "dcdg_xwin_create: empty window");
+  if (int rc = check_ctx(ctx)) return rc;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  auto* w = new dcdg_xwin;
+  w->ctx = ctx;
+  w->world = world;
+  w->rank = rank;
+  w->buf_bytes = (buf_bytes + 255) & ~int64_t(255);
+  const size_t total = dcdg::kXchgFlagBytes + 2 * static_cast<size_t>(w->buf_bytes);
+  cudaError_t e = cudaMalloc(&w->base, total);
+  if (e == cudaSuccess) e = cudaMemset(w->base, 0, dcdg::kXchgFlagBytes);
+  if (e == cudaSuccess) e = cudaMalloc(&w->counter, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(w->counter, 0, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (w->base) cudaFree(w->base);
+    if (w->counter) cudaFree(w->counter);
+    delete w;
+    return cuda_fail(e, "dcdg_xwin_create");
+  }
+  w->peer[rank] = w->base;
+  w->opened[rank] = true;
+  *out = w;
+  return DCDG_OK;
+}
+
+int dcdg_xwin_handle(dcdg_xwin* w, void* handle) {
+  if (!w || !handle) return fail(DCDG_EINVAL, "dcdg_xwin_handle: null argument");
+  CUDA_TRY(cudaSetDevice(w->ctx->device), "cudaSetDevice");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, w->base), "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == DCDG_XWIN_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle, &h, sizeof h);
+  return DCDG_OK;
+}
+
+int dcdg_xwin_open(dcdg_xwin* w, int peer, const void* handle) {
+  if (!w || !handle) return fail(DCDG_EINVAL, "dcdg_xwin_open: null argument");
+  if (peer < 0 || peer >= w->world) return fail(DCDG_EINVAL, "dcdg_xwin_open: peer out of range");
+  if (peer == w->rank || w->opened[peer]) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(w->ctx->device), "cudaSetDevice");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  void* p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  w->peer[peer] = static_cast<unsigned char*>(p);
+  w->opened[peer] = true;
+  return DCDG_OK;
+}
+
+int dcdg_xwin_set_timeout(dcdg_xwin* w, int64_t timeout_ns) {
+  if (!w || timeout_ns <= 0) return fail(DCDG_EINVAL, "dcdg_xwin_set_timeout: need a window and a positive timeout");
+  w->timeout_ns = timeout_ns;
+  return DCDG_OK;
+}
+
+int dcdg_xwin_destroy(dcdg_xwin* w) {
+  if (!w) return DCDG_OK;
+  cudaSetDevice(w->ctx->device);
+  cudaDeviceSynchronize();
+  for (int q = 0; q < w->world; ++q)
+    if (q != w->rank && w->opened[q] && w->peer[q]) cudaIpcCloseMemHandle(w->peer[q]);
+  if (w->base) cudaFree(w->base);
+  if (w->counter) cudaFree(w->counter);
+  delete w;
+  return DCDG_OK;
+}
+
+int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* y, int S, int C, int c0,
+                        int C_total, int Bc, int U, int K, double n0, double ex, int fmt, int fusion, float* xhat,
+                        void* stream) {
+  if (int rc = check_fmt(fmt)) return rc;
+  // the reference's argument checks first (as dcdg_ul_detect), then the exchange's own
+  if (C <= 0 || S < 0) return fail(DCDG_EINVAL, "decentralized_cd_detect: no clusters");
+  if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "detector: empty channel matrix");
+  if (n0 < 0.0 || !(ex > 0.0)) return fail(DCDG_EINVAL, "detector: need N0 >= 0 and E_x > 0");
+  if (K <= 0) return fail(DCDG_EINVAL, "cd_detect: need at least one sweep");
+  if (fmt == DCDG_FP16 && (Bc & 1))
+    return fail(DCDG_EINVAL, "dcdg: fp16 row-pair planar tiles need an even antenna count B_c");
+  const bool optimal = fusion == DCDG_FUSION_OPTIMAL;
+  if (fusion != DCDG_FUSION_OPTIMAL && fusion != DCDG_FUSION_UNIFORM)
+    return fail(DCDG_EINVAL, "dcdg_ul_detect: unknown fusion mode");
+  if (optimal && !(n0 > 0.0)) return fail(DCDG_EINVAL, "post_eq_variance: need N0 > 0 and E_x > 0");
+  if (!w) return fail(DCDG_EINVAL, "dcdg_ul_detect_xchg: null exchange window");
+  if (c0 < 0 || c0 + C > C_total) return fail(DCDG_EINVAL, "dcdg_ul_detect_xchg: clusters [c0, c0+C) outside C_total");
+  if (S % w->world) return fail(DCDG_EINVAL, "dcdg_ul_detect_xchg: S must divide over the ranks");
+  for (int q = 0; q < w->world; ++q)
+    if (!w->opened[q]) return fail(DCDG_EINVAL, "dcdg_ul_detect_xchg: peer window " + std::to_string(q) + " not open");
+  const int S_own = S / w->world;
+  const long long xbytes = static_cast<long long>(S_own) * C_total * U * static_cast<long long>(esize(fmt));
+  const long long sig_off = (xbytes + 255) & ~255LL;
+  const long long need = sig_off + (optimal ? static_cast<long long>(S_own) * C_total * 4 : 0);
+  if (need > w->buf_bytes) return fail(DCDG_EINVAL, "dcdg_ul_detect_xchg: exchange window too small for this batch");
+  if (!H || !y || !xhat) return fail(DCDG_EINVAL, "dcdg_ul_detect_xchg: null buffer");
+  const long long P = static_cast<long long>(S) * C;
+  if (P > 0x7fffffffLL) return fail(DCDG_EINVAL, "dcdg_ul_detect: batch too large (S*C must fit in int32)");
+  if (int rc = check_ctx(ctx)) return rc;
+  if (P == 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = as_stream(stream);
+
+  dcdg::XMap m{};
+  for (int q = 0; q < w->world; ++q) m.win[q] = w->peer[q];
+  m.counter = w->counter;
+  m.epoch = ++w->epoch;
+  m.buf_bytes = w->buf_bytes;
+  m.sig_off = sig_off;
+  m.world = w->world;
+  m.rank = w->rank;
+  m.S_own = S_own;
+  m.C_local = C;
+  m.c0 = c0;
+  m.C_total = C_total;
+  m.U = U;
+  m.esz = static_cast<int>(esize(fmt));
+  m.parity = static_cast<int>(m.epoch & 1);
+
+  const float kappa = static_cast<float>(n0 / ex);
+  const Spec* spec = find_spec(Bc, U, fmt);
+  if (spec && spec->g > 0 && !optimal) {
+    // fused: the CD kernel stores into the owners' windows and signals
+    CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, nullptr, &m, st), "ul_detect_xchg launch");
+    ++ctx->launches;
+  } else {
+    // CD (+ variances) locally, then one put kernel moves the rows and signals
+    const size_t xl_bytes = static_cast<size_t>(P) * U * esize(fmt);
+    const size_t s2_off = (xl_bytes + 255) & ~size_t(255);
+    if (int rc = ensure_scratch(ctx, s2_off + (optimal ? static_cast<size_t>(P) * 4 : 0))) return rc;
+    void* xl = ctx->scratch;
+    float* s2 = optimal ? reinterpret_cast<float*>(static_cast<unsigned char*>(ctx->scratch) + s2_off) : nullptr;
+    if (int rc = dcdg_ul_detect(ctx, H, y, S, C, C_total, Bc, U, K, n0, ex, fmt, fusion, xl, s2, nullptr, nullptr,
+                                stream))
+      return rc;
+    const int threads = 256;
+    const int blocks = static_cast<int>(std::min<long long>((P * U + P + threads - 1) / threads, 4LL * ctx->sms));
+    if (fmt == DCDG_FP16)
+      dcdg::xchg_put_kernel<__half2><<<blocks, threads, 0, st>>>(static_cast<const __half2*>(xl), s2, P, m);
+    else
+      dcdg::xchg_put_kernel<float2><<<blocks, threads, 0, st>>>(static_cast<const float2*>(xl), s2, P, m);
+    ++ctx->launches;
+    CUDA_TRY(cudaGetLastError(), "xchg_put launch");
+  }
+  // owner side: wait for every rank's epoch, then the ascending-cluster fusion
+  const long long n = static_cast<long long>(S_own) * U;
+  const int threads = 256;
+  const long long blocks = (n + threads - 1) / threads;
+#define XFUSE(T)                                                                                               \
+  dcdg::xchg_fuse_kernel<T><<<blocks, threads, 0, st>>>(w->base, m.epoch, w->world, m.parity, w->buf_bytes,    \
+                                                        sig_off, S_own, C_total, U, optimal, w->timeout_ns,     \
+                                                        reinterpret_cast<float2*>(xhat), ctx->d_status)
+  if (fmt == DCDG_FP16)
+    XFUSE(__half2);
+  else
+    XFUSE(float2);
+#undef XFUSE
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "xchg_fuse launch");
+  return DCDG_OK;
 }
 
 }  // extern "C"

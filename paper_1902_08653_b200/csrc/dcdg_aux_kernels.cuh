@@ -540,6 +540,98 @@ __global__ void fuse_kernel(const T* __restrict__ XL, const float* __restrict__ 
   xhat[idx] = acc;
 }
 
+// ===========================================================================
+// Fused cross-GPU exchange (see XMap in dcdg_device.cuh).
+// xchg_put_kernel: for shapes whose CD kernel has no exchange epilogue, and for
+// the optimal-fusion variances: copy this rank's per-cluster rows into the
+// owners' windows, then signal (last CTA).
+// xchg_fuse_kernel: on the owner, wait until every rank has published this
+// epoch, then the reference's ascending-cluster fusion over the gathered
+// [S_own][C_total] estimates — the arithmetic of fuse_kernel with C == C_total,
+// so the result is bitwise that of a single GPU holding every cluster.
+// ===========================================================================
+template <typename T>
+__global__ void xchg_put_kernel(const T* __restrict__ XL, const float* __restrict__ sigma2, long long P, XMap m) {
+  const long long n = P * m.U;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n + (sigma2 ? P : 0);
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (i < n) {
+      const long long p = i / m.U;
+      const int u = static_cast<int>(i - p * m.U);
+      reinterpret_cast<T*>(xchg_x_dst(m, p))[u] = XL[i];
+    } else {
+      const long long p = i - n;
+      const long long s = p / m.C_local;
+      const int c = static_cast<int>(p - s * m.C_local);
+      const int owner = static_cast<int>(s / m.S_own);
+      const long long s_in = s - static_cast<long long>(owner) * m.S_own;
+      float* dst = reinterpret_cast<float*>(m.win[owner] + kXchgFlagBytes + m.parity * m.buf_bytes + m.sig_off);
+      dst[s_in * m.C_total + m.c0 + c] = sigma2[p];
+    }
+  }
+  xchg_cta_done(m);
+}
+
+__device__ __forceinline__ float2 ldcg_c(const float2* p, size_t i) { return __ldcg(p + i); }
+__device__ __forceinline__ float2 ldcg_c(const __half2* p, size_t i) { return __half22float2(__ldcg(p + i)); }
+
+template <typename T>
+__global__ void xchg_fuse_kernel(const unsigned char* __restrict__ win, unsigned long long epoch, int world,
+                                 int parity, long long buf_bytes, long long sig_off, int S_own, int C_total, int U,
+                                 bool optimal, long long timeout_ns, float2* __restrict__ xhat,
+                                 unsigned long long* __restrict__ status) {
+  __shared__ int abort_;
+  if (threadIdx.x == 0) {
+    abort_ = 0;
+    const unsigned long long* flags = reinterpret_cast<const unsigned long long*>(win);
+    for (int q = 0; q < world && !abort_; ++q) {
+      const unsigned long long t0 = globaltimer_ns();
+      while (ld_acquire_sys(flags + q) < epoch) {
+        if (static_cast<long long>(globaltimer_ns() - t0) > timeout_ns) {
+          if (blockIdx.x == 0) record_status(status, 0, ST_XCHG_TIMEOUT, q);
+          abort_ = 1;
+          break;
+        }
+        __nanosleep(200);
+      }
+    }
+  }
+  __syncthreads();
+  if (abort_) return;
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long long>(S_own) * U) return;
+  const long long s = idx / U;
+  const int u = static_cast<int>(idx - s * U);
+  const unsigned char* buf = win + kXchgFlagBytes + parity * buf_bytes;
+  const T* XL = reinterpret_cast<const T*>(buf);
+  float2 acc = make_float2(0.f, 0.f);
+  if (!optimal) {
+    const float w = 1.f / static_cast<float>(C_total);
+    for (int c = 0; c < C_total; ++c) {
+      const float2 v = ldcg_c(XL, (static_cast<size_t>(s) * C_total + c) * U + u);
+      acc.x = fmaf(w, v.x, acc.x);
+      acc.y = fmaf(w, v.y, acc.y);
+    }
+  } else {
+    const float* sigma2 = reinterpret_cast<const float*>(buf + sig_off);
+    float total = 0.f;
+    bool bad = false;
+    for (int c = 0; c < C_total; ++c) {
+      const float v = __ldcg(sigma2 + s * C_total + c);
+      if (!(v > 0.f) || !isfinite(v)) bad = true;
+      total += 1.f / v;
+    }
+    if (bad && u == 0) record_status(status, s * C_total, ST_BAD_VARIANCE, 0);
+    for (int c = 0; c < C_total; ++c) {
+      const float w = (1.f / __ldcg(sigma2 + s * C_total + c)) / total;
+      const float2 v = ldcg_c(XL, (static_cast<size_t>(s) * C_total + c) * U + u);
+      acc.x = fmaf(w, v.x, acc.x);
+      acc.y = fmaf(w, v.y, acc.y);
+    }
+  }
+  xhat[idx] = acc;
+}
+
 __global__ void fuse_finalize_kernel(float2* __restrict__ xhat, const float* __restrict__ wsum, int S, int U) {
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= static_cast<long long>(S) * U) return;

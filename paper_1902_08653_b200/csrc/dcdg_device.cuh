@@ -171,10 +171,76 @@ enum StatusCode : uint32_t {
   ST_RANK_DEFICIENT = 5,  // precode.cpp:42-43   runtime_error (zf_exact)
   ST_MF_ZERO_ENERGY = 6,  // detect.cpp:213-215  runtime_error (mf_detect)
   ST_MF_ZERO_BEAMFORMER = 7,  // precode.cpp:193-196 runtime_error (mf_precode)
+  ST_XCHG_TIMEOUT = 8,        // fused exchange: a peer's signal never arrived (detail = peer rank)
 };
 
 __device__ __forceinline__ void record_status(unsigned long long* st, long long p, uint32_t code, uint32_t detail) {
   if (st) atomicMin(st, (static_cast<unsigned long long>(p) << 24) | (code << 16) | (detail & 0xffffu));
+}
+
+// ---------------------------------------------------------------------------
+// fused cross-GPU exchange over peer memory (NVLink P2P): the uplink kernels
+// store each cluster estimate straight into the exchange window of the GPU
+// that owns the subcarrier, then the last CTA of the launch signals every
+// owner with a system-scope release store of the batch epoch.
+// Window layout (per rank): [flags: kXchgMaxRanks u64][pad to 256 B]
+//   [parity 0: x [S_own][C_total][U] | sigma2 [S_own][C_total]]
+//   [parity 1: same]
+// ---------------------------------------------------------------------------
+constexpr int kXchgMaxRanks = 8;
+constexpr int kXchgFlagBytes = 256;
+
+struct XMap {
+  unsigned char* win[kXchgMaxRanks];  // every rank's window base (self included), in this process's address space
+  unsigned int* counter;              // local CTA-completion counter (reset by the last CTA)
+  unsigned long long epoch;           // batch epoch written to the owners' flags
+  long long buf_bytes;                // bytes of one parity buffer
+  long long sig_off;                  // offset of the sigma2 region inside a parity buffer
+  int world, rank;
+  int S_own;                          // subcarriers owned per rank
+  int C_local, c0, C_total, U;
+  int esz;                            // bytes per complex of x (8 fp32, 4 fp16)
+  int parity;
+};
+
+// Destination of problem p's estimate (p = s*C_local + c, s global over the batch).
+__device__ __forceinline__ unsigned char* xchg_x_dst(const XMap& m, long long p) {
+  const long long s = p / m.C_local;
+  const int c = static_cast<int>(p - s * m.C_local);
+  const int owner = static_cast<int>(s / m.S_own);
+  const long long s_in = s - static_cast<long long>(owner) * m.S_own;
+  return m.win[owner] + kXchgFlagBytes + m.parity * m.buf_bytes +
+         ((s_in * m.C_total + m.c0 + c) * m.U) * m.esz;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Called by every thread of every CTA after its last remote store: the last
+// CTA to finish publishes the epoch to every owner's flag slot `rank`.
+__device__ __forceinline__ void xchg_cta_done(const XMap& m) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(m.counter, 1u);
+    if (t == gridDim.x - 1) {
+      __threadfence_system();
+      for (int q = 0; q < m.world; ++q)
+        st_release_sys(reinterpret_cast<unsigned long long*>(m.win[q]) + m.rank, m.epoch);
+      *m.counter = 0u;  // next launch on this stream starts from zero
+    }
+  }
 }
 
 }  // namespace dcdg

@@ -147,10 +147,10 @@ struct CtaSmem {
 // Scalar block per problem: float4 mnx[U] = (m_j, n_j, Re x_j, Im x_j) and
 // float4 gb[U/LB][LB(LB-1)/2] = (Re G, Im G, -Im G, Re G).
 // ===========================================================================
-template <int BC, int U, int G, int W, int MINB, int LB>
+template <int BC, int U, int G, int W, int MINB, int LB, bool XCHG = false>
 __global__ void __launch_bounds__(32 * W, MINB)
     ul_reg_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
-               float2* __restrict__ X) {
+               float2* __restrict__ X, const XMap xm) {
   static_assert(32 % G == 0 && BC % (2 * G) == 0 && U % LB == 0, "shape");
   constexpr int NPW = 32 / G, R = BC / G, NP = R / 2;
   constexpr int T = LB * (LB - 1) / 2;  // Gram entries per block
@@ -335,7 +335,9 @@ __global__ void __launch_bounds__(32 * W, MINB)
     __syncwarp();
     const int p = set * NPW + g;
     if (p < P) {
-      float4* xo = reinterpret_cast<float4*>(X + static_cast<size_t>(p) * U);
+      // XCHG: straight into the owning GPU's exchange window (peer memory)
+      float4* xo = XCHG ? reinterpret_cast<float4*>(xchg_x_dst(xm, p))
+                        : reinterpret_cast<float4*>(X + static_cast<size_t>(p) * U);
 #pragma unroll
       for (int i = k; i < U / 2; i += G) {
         const float4 u0 = mnx[2 * i], u1 = mnx[2 * i + 1];
@@ -344,6 +346,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
     }
     __syncwarp();
   }
+  if constexpr (XCHG) xchg_cta_done(xm);
 }
 
 // ===========================================================================
@@ -355,10 +358,10 @@ __global__ void __launch_bounds__(32 * W, MINB)
 // products accumulate in half2 and are reduced as one packed (re, im) half2
 // per shuffle; the per-coordinate scalar update runs in fp32.
 // ===========================================================================
-template <int BC, int U, int G, int W, int MINB>
+template <int BC, int U, int G, int W, int MINB, bool XCHG = false>
 __global__ void __launch_bounds__(32 * W, MINB)
     ul_reg_f16(const __half2* __restrict__ H, const __half2* __restrict__ Y, int P, int K, float kappa,
-               __half2* __restrict__ X) {
+               __half2* __restrict__ X, const XMap xm) {
   static_assert(32 % G == 0 && BC % (4 * G) == 0 && U % 4 == 0 && U % G == 0, "shape");
   constexpr int NPW = 32 / G, R = BC / G, CH = R / 4, NP = R / 2;
   constexpr int TILE_B = BC * U * 4, Y_B = BC * 4, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
@@ -507,7 +510,8 @@ __global__ void __launch_bounds__(32 * W, MINB)
     __syncwarp();
     const int p = set * NPW + g;
     if (p < P) {
-      uint4* xo = reinterpret_cast<uint4*>(X + static_cast<size_t>(p) * U);
+      uint4* xo = XCHG ? reinterpret_cast<uint4*>(xchg_x_dst(xm, p))
+                       : reinterpret_cast<uint4*>(X + static_cast<size_t>(p) * U);
 #pragma unroll
       for (int i = k; i < U / 4; i += G) {
         uint4 w;
@@ -520,6 +524,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
     }
     __syncwarp();
   }
+  if constexpr (XCHG) xchg_cta_done(xm);
 }
 
 // ===========================================================================

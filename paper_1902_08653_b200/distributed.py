@@ -26,6 +26,12 @@ Uplink fusion modes:
             each subcarrier chunk holds all C estimates in ascending cluster
             order and runs the ordinary fusion kernel: the reference's exact
             ascending-c summation order, independent of the GPU count.
+  "p2p"     the gather exchange fused into the CD kernel over peer memory
+            (NVLink P2P, CUDA IPC windows; include/dcdg.h dcdg_ul_detect_xchg):
+            the kernel's epilogue stores each x_c into the owner's window, its
+            last CTA publishes the batch epoch, the owner fuses once every rank
+            has published.  No NCCL call on the data path; bitwise the
+            single-GPU result.  Needs world <= C_total and CudaCompute.
 
 The per-rank compute is pluggable (`compute` objects below): CudaCompute runs
 the CD kernels (libdcdg.so); tests substitute a CPU checker to exercise the
@@ -200,13 +206,17 @@ class CudaCompute:
 # ---------------------------------------------------------------------------
 class DistributedCD:
     def __init__(self, part: ClusterPartition, compute, *, mode: str = "reduce"):
-        if mode not in ("reduce", "gather"):
-            raise ValueError("mode must be 'reduce' or 'gather'")
+        if mode not in ("reduce", "gather", "p2p"):
+            raise ValueError("mode must be 'reduce', 'gather' or 'p2p'")
+        if mode == "p2p" and part.world > part.C_total:
+            raise ValueError("the p2p exchange needs at most one GPU per cluster (world <= C_total)")
         self.part = part
         self.compute = compute
         self.mode = mode
         self._groups = _Groups(part)
         self.traffic = Traffic()
+        self._xwin = None
+        self._xkey = None
 
     def _log_uplink(self, S_local: int, U: int, bpc: int, optimal: bool):
         p = self.part
@@ -226,6 +236,8 @@ class DistributedCD:
                              bytes_per_complex(xl), fusion == "optimal")
             out = self.compute.fuse(xl, s2, fusion=fusion, C_total=p.C_total)
             return _Deferred(None, lambda: out) if async_op else out
+        if self.mode == "p2p":
+            return self._uplink_p2p(H, y, n0=n0, ex=ex, K=K, fusion=fusion, async_op=async_op)
         if self.mode == "gather" and p.world <= p.C_total:
             return self._uplink_gather(H, y, n0=n0, ex=ex, K=K, fusion=fusion, async_op=async_op)
         part_sum, wsum, _, _ = self.compute.ul_partial(H, y, n0=n0, ex=ex, K=K, fusion=fusion, C_total=p.C_total,
@@ -251,6 +263,39 @@ class DistributedCD:
         if async_op:
             return _Deferred(work, finish)
         return finish()
+
+    def _window(self, U: int, fmt: str):
+        """Create this rank's exchange window and map every peer's (one
+        all_gather of the 64-byte IPC handles; collective, all ranks call)."""
+        from .engine import ExchangeWindow
+        p = self.part
+        key = (p.S, U, fmt)
+        if self._xwin is None or self._xkey != key:
+            if self._xwin is not None:
+                self._xwin.close()
+            self._xwin = ExchangeWindow(self.compute.eng, p.world, p.rank, S=p.S, C_total=p.C_total, U=U, fmt=fmt)
+            handles = [None] * p.world
+            dist.all_gather_object(handles, self._xwin.handle())
+            for q, h in enumerate(handles):
+                self._xwin.open(q, h)
+            dist.barrier()
+            self._xkey = key
+        return self._xwin
+
+    def _uplink_p2p(self, H, y, *, n0, ex, K, fusion, async_op):
+        p = self.part
+        if not hasattr(self.compute, "eng"):
+            raise ValueError("the p2p exchange runs the CUDA kernels (CudaCompute)")
+        fp16 = H.dtype == torch.float16
+        U = H.shape[2]
+        esz = 4 if fp16 else 8
+        w = self._window(U, "fp16" if fp16 else "fp32")
+        out = w.ul_detect(H, y, c0=p.c_lo, C_total=p.C_total, n0=n0, ex=ex, K=K, fusion=fusion)
+        S_local = H.shape[0]
+        self._log_uplink(S_local, U, esz, fusion == "optimal")
+        nbytes = S_local * p.C_local * (U * esz + (4 if fusion == "optimal" else 0))
+        self.traffic.add_bus("all_to_all", nbytes, p.world, True)
+        return _Deferred(None, lambda: out) if async_op else out
 
     def _uplink_gather(self, H, y, *, n0, ex, K, fusion, async_op):
         p = self.part

@@ -355,6 +355,67 @@ class Engine:
         return t
 
 
+class ExchangeWindow:
+    """This rank's window of the fused cross-GPU uplink exchange (include/dcdg.h,
+    dcdg_xwin_*): the CD kernel stores each cluster estimate straight into the
+    window of the GPU that owns the subcarrier (peer memory, CUDA IPC) and the
+    owner fuses in ascending cluster order once every rank has published the
+    batch.  ``handle()`` bytes go to the peers (any transport); ``open(peer,
+    handle)`` maps theirs."""
+
+    def __init__(self, eng: Engine, world: int, rank: int, *, S: int, C_total: int, U: int, fmt: str = "fp32",
+                 optimal: bool = True):
+        self.eng, self.world, self.rank = eng, world, rank
+        if S % world:
+            raise ValueError(f"batch of {S} subcarriers must divide over {world} GPUs")
+        esz = 8 if fmt == "fp32" else 4
+        s_own = S // world
+        nbytes = ((s_own * C_total * U * esz + 255) // 256) * 256 + (s_own * C_total * 4 if optimal else 0)
+        self._w = C.c_void_p()
+        check(lib().dcdg_xwin_create(eng._ctx, world, rank, nbytes, C.byref(self._w)))
+
+    def handle(self) -> bytes:
+        buf = C.create_string_buffer(_lib.XWIN_HANDLE_BYTES)
+        check(lib().dcdg_xwin_handle(self._w, buf))
+        return buf.raw
+
+    def open(self, peer: int, handle: bytes):
+        if len(handle) != _lib.XWIN_HANDLE_BYTES:
+            raise ValueError("exchange-window handle has the wrong size")
+        check(lib().dcdg_xwin_open(self._w, peer, C.c_char_p(handle)))
+
+    def set_timeout(self, seconds: float):
+        check(lib().dcdg_xwin_set_timeout(self._w, int(seconds * 1e9)))
+
+    def close(self):
+        if self._w:
+            lib().dcdg_xwin_destroy(self._w)
+            self._w = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def ul_detect(self, H, y, *, c0: int, C_total: int, n0: float, ex: float = 1.0, K: int = 3, fusion="uniform",
+                  xhat=None, stream=None) -> torch.Tensor:
+        """This rank's clusters [c0, c0 + C) over all S subcarriers -> the fused
+        estimates [S/world, U] of the subcarriers it owns."""
+        fmt = _fmt_of(H)
+        S, Cn, U, Bc = _shape(H, fmt)
+        if _shape(y, fmt) != (S, Cn, Bc) or _fmt_of(y) != fmt:
+            raise ValueError("detector: observation length must match antenna count")
+        _need(H, "H")
+        _need(y, "y")
+        if xhat is None:
+            xhat = torch.empty((S // self.world, U), dtype=torch.complex64, device=H.device)
+        check(lib().dcdg_ul_detect_xchg(self.eng._ctx, self._w, _ptr(H), _ptr(y), S, Cn, c0, C_total, Bc, U, K,
+                                        float(n0), float(ex), fmt, _fusion(fusion), _ptr(xhat),
+                                        self.eng._stream(stream)))
+        return xhat
+
+
 def kernel_name(direction: str, bc: int, u: int, fmt: str) -> str:
     return _lib.kernel_name(0 if direction == "ul" else 1, bc, u, FP16 if fmt == "fp16" else FP32)
 

@@ -135,3 +135,20 @@ def test_missing_library_fails_loudly():
     code = "import paper_1902_08653_b200._lib as l; l.lib()"
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True)
     assert r.returncode != 0 and "no CPU fallback" in r.stderr
+
+
+def test_exchange_window_argument_errors_before_any_device_work():
+    """dcdg_xwin_create / dcdg_ul_detect_xchg validate on the host (the fused
+    cross-GPU exchange, include/dcdg.h)."""
+    L = _lib.lib()
+    w = C.c_void_p()
+    _err(L.dcdg_xwin_create(None, 9, 0, 1024, C.byref(w)), DCDG_EINVAL,
+         "dcdg_xwin_create: need 1 <= world <= 8 and 0 <= rank < world")
+    _err(L.dcdg_xwin_create(None, 2, 2, 1024, C.byref(w)), DCDG_EINVAL,
+         "dcdg_xwin_create: need 1 <= world <= 8 and 0 <= rank < world")
+    _err(L.dcdg_xwin_create(None, 2, 0, 0, C.byref(w)), DCDG_EINVAL, "dcdg_xwin_create: empty window")
+    dummy = C.c_void_p(16)
+    _err(L.dcdg_ul_detect_xchg(None, None, dummy, dummy, 16, 4, 0, 8, 32, 16, 0, 1.0, 1.0, FP32, FUSION_UNIFORM,
+                               dummy, None), DCDG_EINVAL, "cd_detect: need at least one sweep")
+    _err(L.dcdg_ul_detect_xchg(None, None, dummy, dummy, 16, 4, 0, 8, 32, 16, 3, 1.0, 1.0, FP32, FUSION_UNIFORM,
+                               dummy, None), DCDG_EINVAL, "dcdg_ul_detect_xchg: null exchange window")

@@ -176,3 +176,12 @@ def test_interconnect_accounting_matches_the_message_model():
     assert summ["downlink_bytes"] == S * C * U * 16
     assert summ["messages"] == 2 * S * C
     assert summ["reduction_ratio"] == pytest.approx(2 * U / Bc / 1)  # (U up + U down) per cluster vs B_c samples
+
+
+def test_p2p_mode_needs_one_gpu_per_cluster_at_most():
+    """The fused peer-memory exchange owns whole clusters per rank (world <= C)."""
+    from paper_1902_08653_b200.distributed import DistributedCD, partition
+    with pytest.raises(ValueError, match="at most one GPU per cluster"):
+        DistributedCD(partition(2, 4, 0, 16), None, mode="p2p")
+    with pytest.raises(ValueError, match="mode must be"):
+        DistributedCD(partition(2, 2, 0, 16), None, mode="nccl")
