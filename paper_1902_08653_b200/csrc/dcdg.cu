@@ -259,6 +259,10 @@ struct Spec {
 #ifndef DCDG_MIN_WARPS_DL_F16
 #define DCDG_MIN_WARPS_DL_F16 8
 #endif
+// lanes per problem of the fp16 north-star kernel (B_c=32, U=16)
+#ifndef DCDG_F16_G_TARGET
+#define DCDG_F16_G_TARGET 4
+#endif
 constexpr int minb(int warps) { return warps / kWarps > 0 ? warps / kWarps : 1; }
 constexpr int minb_mw(int warps, int nw) { return warps / nw > 0 ? warps / nw : 1; }
 #define SPEC_MW_F32(BC, U, NW)                                                                  \
@@ -281,7 +285,7 @@ const Spec kSpecs[] = {
     SPEC_MW_F32(128, 32, 2),
     SPEC_MW_F32(256, 32, 4),
     SPEC_MW_F32(512, 32, 8),
-    SPEC_F16(32, 16, 4),
+    SPEC_F16(32, 16, DCDG_F16_G_TARGET),  // north-star shape, half2
     SPEC_F16(32, 8, 4),
     SPEC_F16(16, 16, 4),
     SPEC_F16(64, 16, 8),

@@ -459,7 +459,9 @@ __global__ void __launch_bounds__(32 * W, MINB)
 #pragma unroll
       for (int i = 0; i < U / G; ++i) {
         const int gi = k * (U / G) + i;
+        // mng[2i+1].zw = (Re G, Im G), mng[2i].zw = (-Im G, Re G) of G = h_{2i+1}^H h_{2i}
         mf[((gi >> 1) * 2 + 1) * 4 + 2 + (gi & 1)] = v[i];
+        mf[((gi >> 1) * 2) * 4 + 3 - (gi & 1)] = (gi & 1) ? -v[i] : v[i];
       }
     }
     __syncwarp();
@@ -488,22 +490,26 @@ __global__ void __launch_bounds__(32 * W, MINB)
         }
         const float2 f0 = __half22float2(d0);
         float2 f1 = __half22float2(d1);
-        const float n0r = fmaf(s0.x, f0.x, s0.y * x0.x), n0i = fmaf(s0.x, f0.y, s0.y * x0.y);
-        const float dx0r = n0r - x0.x, dx0i = n0i - x0.y;
-        f1.x = fmaf(-dx0r, s1.z, fmaf(dx0i, s1.w, f1.x));
-        f1.y = fmaf(-dx0r, s1.w, fmaf(-dx0i, s1.z, f1.y));
-        const float n1r = fmaf(s1.x, f1.x, s1.y * x1.x), n1i = fmaf(s1.x, f1.y, s1.y * x1.y);
-        const float dx1r = n1r - x1.x, dx1i = n1i - x1.y;
-        xs[j0] = make_float2(n0r, n0i);
-        xs[j1] = make_float2(n1r, n1i);
-        const __half2 ndr0 = __float2half2_rn(-dx0r), pdi0 = __float2half2_rn(dx0i), ndi0 = __float2half2_rn(-dx0i);
-        const __half2 ndr1 = __float2half2_rn(-dx1r), pdi1 = __float2half2_rn(dx1i), ndi1 = __float2half2_rn(-dx1i);
+        // scalar update in packed fp32x2 (detect.cpp:100-103), pair-Gram correction of the second dot
+        const float2 n0 = ffma2(s0.x, f0, fmul2(s0.y, x0));
+        const float2 dx0 = fadd2(n0, neg2(x0));
+        f1 = ffma2(-dx0.x, make_float2(s1.z, s1.w), f1);
+        f1 = ffma2(-dx0.y, make_float2(s0.z, s0.w), f1);
+        const float2 n1 = ffma2(s1.x, f1, fmul2(s1.y, x1));
+        const float2 dx1 = fadd2(n1, neg2(x1));
+        xs[j0] = n0;
+        xs[j1] = n1;
+        // one packed conversion per coordinate; the broadcast halves and signs
+        // are HFMA2 operand modifiers
+        const __half2 h0 = __float22half2_rn(dx0), h1 = __float22half2_rn(dx1);
+        const __half2 r0 = __low2half2(h0), i0 = __high2half2(h0);
+        const __half2 r1 = __low2half2(h1), i1 = __high2half2(h1);
 #pragma unroll
-        for (int q = 0; q < NP; ++q) {
-          rre[q] = __hfma2(ndr0, hre[j0][q], __hfma2(pdi0, him[j0][q], rre[q]));
-          rim[q] = __hfma2(ndr0, him[j0][q], __hfma2(ndi0, hre[j0][q], rim[q]));
-          rre[q] = __hfma2(ndr1, hre[j1][q], __hfma2(pdi1, him[j1][q], rre[q]));
-          rim[q] = __hfma2(ndr1, him[j1][q], __hfma2(ndi1, hre[j1][q], rim[q]));
+        for (int q = 0; q < NP; ++q) {  // r -= dx_j h_j   (caxpy, detect.cpp:104)
+          rre[q] = __hfma2(__hneg2(r0), hre[j0][q], __hfma2(i0, him[j0][q], rre[q]));
+          rim[q] = __hfma2(__hneg2(r0), him[j0][q], __hfma2(__hneg2(i0), hre[j0][q], rim[q]));
+          rre[q] = __hfma2(__hneg2(r1), hre[j1][q], __hfma2(i1, him[j1][q], rre[q]));
+          rim[q] = __hfma2(__hneg2(r1), him[j1][q], __hfma2(__hneg2(i1), hre[j1][q], rim[q]));
         }
       }
     }
@@ -878,7 +884,10 @@ __global__ void __launch_bounds__(32 * W, MINB)
       } else {
         const int gi = idx - U;
         const int a = (gi >> 1) * 2 + 1;
-        sgf[a * 4 + 2 + (gi & 1)] = vv[i] * (pn[a] * pn[a - 1]);
+        // sg[2i+1].zw = (Re G~, Im G~), sg[2i].zw = (-Im G~, Re G~)
+        const float gv = vv[i] * (pn[a] * pn[a - 1]);
+        sgf[a * 4 + 2 + (gi & 1)] = gv;
+        sgf[(a - 1) * 4 + 3 - (gi & 1)] = (gi & 1) ? -gv : gv;
       }
     }
 #pragma unroll
@@ -918,18 +927,20 @@ __global__ void __launch_bounds__(32 * W, MINB)
         }
         const float2 f0 = __half22float2(d0);
         float2 f1 = __half22float2(d1);
-        const float r0r = f0.x - s0.x, r0i = f0.y - s0.y;
-        f1.x = fmaf(-r0r, s1.z, fmaf(r0i, s1.w, f1.x));
-        f1.y = fmaf(-r0r, s1.w, fmaf(-r0i, s1.z, f1.y));
-        const float r1r = f1.x - s1.x, r1i = f1.y - s1.y;
-        const __half2 ndr0 = __float2half2_rn(-r0r), pdi0 = __float2half2_rn(r0i), ndi0 = __float2half2_rn(-r0i);
-        const __half2 ndr1 = __float2half2_rn(-r1r), pdi1 = __float2half2_rn(r1i), ndi1 = __float2half2_rn(-r1i);
+        // resid_u = h~_u^H x - s~_u (precode.cpp:89-94) in packed fp32x2, pair-Gram correction
+        const float2 q0 = fadd2(f0, make_float2(-s0.x, -s0.y));
+        f1 = ffma2(-q0.x, make_float2(s1.z, s1.w), f1);
+        f1 = ffma2(-q0.y, make_float2(s0.z, s0.w), f1);
+        const float2 q1 = fadd2(f1, make_float2(-s1.x, -s1.y));
+        const __half2 h0 = __float22half2_rn(q0), h1 = __float22half2_rn(q1);
+        const __half2 r0 = __low2half2(h0), i0 = __high2half2(h0);
+        const __half2 r1 = __low2half2(h1), i1 = __high2half2(h1);
 #pragma unroll
-        for (int q = 0; q < NP; ++q) {
-          xre[q] = __hfma2(ndr0, hre[j0][q], __hfma2(pdi0, him[j0][q], xre[q]));
-          xim[q] = __hfma2(ndr0, him[j0][q], __hfma2(ndi0, hre[j0][q], xim[q]));
-          xre[q] = __hfma2(ndr1, hre[j1][q], __hfma2(pdi1, him[j1][q], xre[q]));
-          xim[q] = __hfma2(ndr1, him[j1][q], __hfma2(ndi1, hre[j1][q], xim[q]));
+        for (int q = 0; q < NP; ++q) {  // x -= resid_u h~_u
+          xre[q] = __hfma2(__hneg2(r0), hre[j0][q], __hfma2(i0, him[j0][q], xre[q]));
+          xim[q] = __hfma2(__hneg2(r0), him[j0][q], __hfma2(__hneg2(i0), hre[j0][q], xim[q]));
+          xre[q] = __hfma2(__hneg2(r1), hre[j1][q], __hfma2(i1, him[j1][q], xre[q]));
+          xim[q] = __hfma2(__hneg2(r1), him[j1][q], __hfma2(__hneg2(i1), hre[j1][q], xim[q]));
         }
       }
     }

@@ -1,0 +1,31 @@
+"""Time post_eq_variance (optimal-fusion sigma^2) at the north-star shape:
+python scripts/pev_bench.py [S] (set DCDG_LIB_PATH to compare builds)."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from bench import make_inputs  # noqa: E402
+from paper_1902_08653_b200 import Engine, to_fp16_pairs  # noqa: E402
+
+S = int(sys.argv[1]) if len(sys.argv) > 1 else 16800
+eng = Engine(0)
+H, y, x, n0 = make_inputs(S, 8, torch.device("cuda", 0), 1)
+out = {"lib": os.environ.get("DCDG_LIB_PATH", "default")}
+for fmt, Hh in (("fp32", H), ("fp16", to_fp16_pairs(H))):
+    s2 = torch.empty((S, 8), dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        eng.post_eq_variance(Hh, n0=n0, out=s2)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        eng.post_eq_variance(Hh, n0=n0, out=s2)
+    e1.record()
+    torch.cuda.synchronize()
+    out[f"pev_{fmt}_ms"] = round(e0.elapsed_time(e1) / 10, 4)
+    out[f"pev_{fmt}_checksum"] = float(s2.double().sum())
+eng.sync()
+print(json.dumps(out))
