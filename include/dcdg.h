@@ -244,10 +244,12 @@ int dcdg_kernel_name(int direction /*0 UL, 1 DL*/, int Bc, int U, int fmt, char*
  *   dcdg_xwin_create  allocate this rank's window: 2 parity buffers of
  *                     buf_bytes >= S_own*C_total*U*bytes_per_complex (+256-B
  *                     pad + S_own*C_total*4 for optimal fusion), S_own = S/world
+ *                     (uplink), see dcdg_dl_precode_xchg for the downlink
  *   dcdg_xwin_handle  DCDG_XWIN_HANDLE_BYTES opaque bytes to send to the peers
  *   dcdg_xwin_open    map peer `peer`'s window from its handle
- * Every rank must issue the same sequence of dcdg_ul_detect_xchg calls (the
- * epoch is a per-window call counter), on one stream per window.  A rank whose
+ * Every rank must issue the same sequence of dcdg_ul_detect_xchg /
+ * dcdg_dl_precode_xchg calls (the epochs are per-window call counters), on one
+ * stream per window.  A rank whose
  * peers never publish gets DCDG_ECUDA from dcdg_sync_status after the window
  * timeout (default 20 s), not a hang. */
 #define DCDG_XWIN_HANDLE_BYTES 64
@@ -264,6 +266,17 @@ int dcdg_xwin_destroy(dcdg_xwin* w);
 int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* y, int S, int C, int c0,
                         int C_total, int Bc, int U, int K, double n0, double ex, int fmt, int fusion,
                         float* xhat, void* stream);
+/* Downlink precoding of this rank's clusters [c0, c0+C) with decentralized_cd_precode's
+ * exchanges (precode.cpp:136-169) over the windows: the root's symbols s [S][U]
+ * (read on rank `root` only) are stored into every rank's window (the centre ->
+ * cluster broadcast), each rank precodes from its own window into x_dl [S*C][B_c]
+ * (power-scaled to rho/sqrt(C_total)), publishes its per-cluster gain shares
+ * into every window, and gain [S] (optional, every rank) is the effective gain
+ * summed over all C_total clusters in ascending order — bitwise the single-GPU
+ * value.  Window size: S*U*bytes_per_complex (+256-B pad) + S*C_total*4. */
+int dcdg_dl_precode_xchg(dcdg_ctx* ctx, dcdg_xwin* w, int root, const void* H, const void* s, int S, int C,
+                         int c0, int C_total, int Bc, int U, int K, double rho, int fmt, void* x_dl,
+                         float* gain, void* stream);
 
 #ifdef __cplusplus
 }

@@ -87,6 +87,8 @@ SIGNATURES = {
     "dcdg_xwin_destroy": (C.c_int, [_vp]),
     "dcdg_ul_detect_xchg": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _vp, _vp]),
+    "dcdg_dl_precode_xchg": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_int, C.c_double, C.c_int, _vp, _vp, _vp]),
 }
 
 XWIN_HANDLE_BYTES = 64

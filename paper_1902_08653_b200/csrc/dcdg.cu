@@ -37,7 +37,8 @@ struct dcdg_xwin {
   unsigned char* peer[dcdg::kXchgMaxRanks] = {};
   bool opened[dcdg::kXchgMaxRanks] = {};
   unsigned int* counter = nullptr;
-  unsigned long long epoch = 0;
+  unsigned long long epoch = 0;     // uplink calls
+  unsigned long long dl_epoch = 0;  // downlink calls
   long long timeout_ns = 20000000000LL;  // 20 s: a missing peer becomes ST_XCHG_TIMEOUT, not a hang
 };
 
@@ -488,7 +489,7 @@ int dcdg_sync_status(dcdg_ctx* ctx, void* stream) {
       g_err = "mf_precode: cluster " + std::to_string(detail) + " produced a zero beamformer";
       return DCDG_ENUMERIC;
     case dcdg::ST_XCHG_TIMEOUT:
-      g_err = "dcdg_ul_detect_xchg: rank " + std::to_string(detail) + " never published this batch";
+      g_err = "fused exchange: rank " + std::to_string(detail) + " never published this batch";
       return DCDG_ECUDA;
     default:
       g_err = "dcdg: unknown device status";
@@ -1035,6 +1036,8 @@ int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* 
   for (int q = 0; q < w->world; ++q) m.win[q] = w->peer[q];
   m.counter = w->counter;
   m.epoch = ++w->epoch;
+  m.flag_slot = 0;  // uplink: rank q publishes to slot q
+  m.per_rank = 1;
   m.buf_bytes = w->buf_bytes;
   m.sig_off = sig_off;
   m.world = w->world;
@@ -1087,6 +1090,100 @@ int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* 
 #undef XFUSE
   ++ctx->launches;
   CUDA_TRY(cudaGetLastError(), "xchg_fuse launch");
+  return DCDG_OK;
+}
+
+int dcdg_dl_precode_xchg(dcdg_ctx* ctx, dcdg_xwin* w, int root, const void* H, const void* s, int S, int C, int c0,
+                         int C_total, int Bc, int U, int K, double rho, int fmt, void* x_dl, float* gain,
+                         void* stream) {
+  if (int rc = check_fmt(fmt)) return rc;
+  // the reference's checks (as dcdg_dl_precode), then the exchange's own
+  if (C <= 0 || S < 0) return fail(DCDG_EINVAL, "decentralized_cd_precode: no clusters");
+  if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "precoder: empty channel matrix");
+  if (Bc < U)
+    return fail(DCDG_EINVAL, "decentralized_cd_precode: cluster " + std::to_string(c0) + " has " +
+                                 std::to_string(Bc) + " antennas for " + std::to_string(U) +
+                                 " users; local zero-forcing needs B_c >= U");
+  if (K <= 0) return fail(DCDG_EINVAL, "cd_precode: need at least one sweep");
+  if (fmt == DCDG_FP16 && (Bc & 1))
+    return fail(DCDG_EINVAL, "dcdg: fp16 row-pair planar tiles need an even antenna count B_c");
+  if (rho < 0.0 || std::isnan(rho)) return fail(DCDG_EINVAL, "power_scale: amplitude must be positive");
+  if (!w) return fail(DCDG_EINVAL, "dcdg_dl_precode_xchg: null exchange window");
+  if (root < 0 || root >= w->world) return fail(DCDG_EINVAL, "dcdg_dl_precode_xchg: root out of range");
+  if (c0 < 0 || c0 + C > C_total) return fail(DCDG_EINVAL, "dcdg_dl_precode_xchg: clusters [c0, c0+C) outside C_total");
+  for (int q = 0; q < w->world; ++q)
+    if (!w->opened[q]) return fail(DCDG_EINVAL, "dcdg_dl_precode_xchg: peer window " + std::to_string(q) + " not open");
+  const long long sbytes = static_cast<long long>(S) * U * static_cast<long long>(esize(fmt));
+  const long long gain_off = (sbytes + 255) & ~255LL;
+  if (gain_off + static_cast<long long>(S) * C_total * 4 > w->buf_bytes)
+    return fail(DCDG_EINVAL, "dcdg_dl_precode_xchg: exchange window too small for this batch");
+  if (!H || !x_dl || (w->rank == root && !s)) return fail(DCDG_EINVAL, "dcdg_dl_precode_xchg: null buffer");
+  const long long P = static_cast<long long>(S) * C;
+  if (P > 0x7fffffffLL) return fail(DCDG_EINVAL, "dcdg_dl_precode: batch too large (S*C must fit in int32)");
+  if (int rc = check_ctx(ctx)) return rc;
+  if (P == 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = as_stream(stream);
+
+  dcdg::XMap m{};
+  for (int q = 0; q < w->world; ++q) m.win[q] = w->peer[q];
+  m.counter = w->counter;
+  m.epoch = ++w->dl_epoch;
+  m.buf_bytes = w->buf_bytes;
+  m.sig_off = gain_off;
+  m.world = w->world;
+  m.rank = w->rank;
+  m.C_local = C;
+  m.c0 = c0;
+  m.C_total = C_total;
+  m.U = U;
+  m.esz = static_cast<int>(esize(fmt));
+  m.parity = static_cast<int>(m.epoch & 1);
+  const int threads = 256;
+  // 1. root: the centre -> cluster symbol broadcast as stores into every window
+  if (w->rank == root) {
+    m.flag_slot = dcdg::kSlotSymbols;
+    m.per_rank = 0;
+    const long long n = static_cast<long long>(S) * U;
+    const int blocks = static_cast<int>(std::max(1LL, std::min<long long>((n + threads - 1) / threads, 4LL * ctx->sms)));
+    if (fmt == DCDG_FP16)
+      dcdg::xchg_symbols_push_kernel<__half2><<<blocks, threads, 0, st>>>(static_cast<const __half2*>(s), n, m);
+    else
+      dcdg::xchg_symbols_push_kernel<float2><<<blocks, threads, 0, st>>>(static_cast<const float2*>(s), n, m);
+    ++ctx->launches;
+    CUDA_TRY(cudaGetLastError(), "xchg_symbols_push launch");
+  }
+  // 2. every rank: wait for the symbols, precode from its own window
+  dcdg::xchg_wait_kernel<<<1, 32, 0, st>>>(w->base, dcdg::kSlotSymbols, 1, m.epoch, w->timeout_ns, ctx->d_status);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "xchg_wait launch");
+  const void* Sy = w->base + dcdg::kXchgFlagBytes + m.parity * w->buf_bytes;
+  if (int rc = ensure_scratch(ctx, static_cast<size_t>(P) * sizeof(float))) return rc;
+  float* gp = static_cast<float*>(ctx->scratch);
+  if (int rc = dcdg_dl_precode(ctx, H, Sy, S, C, C_total, Bc, U, K, rho, fmt, x_dl, gp, nullptr, stream)) return rc;
+  // 3. gain shares into every window, then the ascending-cluster effective gain.
+  //    (Always run: the gain exchange is also the acknowledgement that lets the
+  //    root reuse this parity's symbol buffer two calls later.)
+  m.flag_slot = dcdg::kSlotGain;
+  m.per_rank = 1;
+  {
+    const int blocks = static_cast<int>(std::max(1LL, std::min<long long>((P + threads - 1) / threads, 4LL * ctx->sms)));
+    dcdg::xchg_gain_put_kernel<<<blocks, threads, 0, st>>>(gp, P, m);
+    ++ctx->launches;
+    CUDA_TRY(cudaGetLastError(), "xchg_gain_put launch");
+  }
+  const int gblocks = gain ? (S + threads - 1) / threads : 1;
+#define XGAIN(T)                                                                                                \
+  dcdg::xchg_gain_fuse_kernel<T><<<gblocks, threads, 0, st>>>(w->base, m.epoch, w->world, m.parity, w->buf_bytes, \
+                                                              gain_off, S, C_total, U, w->timeout_ns, gain,      \
+                                                              ctx->d_status)
+  if (fmt == DCDG_FP16)
+    XGAIN(__half2);
+  else
+    XGAIN(float2);
+#undef XGAIN
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "xchg_gain_fuse launch");
   return DCDG_OK;
 }
 

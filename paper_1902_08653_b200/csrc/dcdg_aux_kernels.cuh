@@ -580,24 +580,7 @@ __global__ void xchg_fuse_kernel(const unsigned char* __restrict__ win, unsigned
                                  int parity, long long buf_bytes, long long sig_off, int S_own, int C_total, int U,
                                  bool optimal, long long timeout_ns, float2* __restrict__ xhat,
                                  unsigned long long* __restrict__ status) {
-  __shared__ int abort_;
-  if (threadIdx.x == 0) {
-    abort_ = 0;
-    const unsigned long long* flags = reinterpret_cast<const unsigned long long*>(win);
-    for (int q = 0; q < world && !abort_; ++q) {
-      const unsigned long long t0 = globaltimer_ns();
-      while (ld_acquire_sys(flags + q) < epoch) {
-        if (static_cast<long long>(globaltimer_ns() - t0) > timeout_ns) {
-          if (blockIdx.x == 0) record_status(status, 0, ST_XCHG_TIMEOUT, q);
-          abort_ = 1;
-          break;
-        }
-        __nanosleep(200);
-      }
-    }
-  }
-  __syncthreads();
-  if (abort_) return;
+  if (!xchg_block_wait(win, 0, world, epoch, timeout_ns, status)) return;
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= static_cast<long long>(S_own) * U) return;
   const long long s = idx / U;
@@ -630,6 +613,65 @@ __global__ void xchg_fuse_kernel(const unsigned char* __restrict__ win, unsigned
     }
   }
   xhat[idx] = acc;
+}
+
+// Downlink (decentralized_cd_precode, precode.cpp:136-169, across GPUs):
+// xchg_symbols_push_kernel (root): store the centre's symbol batch into the
+// symbol region of every rank's window (the centre -> cluster broadcast as
+// NVLink stores), then publish kSlotSymbols.  Each rank's DL kernel then reads
+// its symbols from its own window after xchg_wait_kernel.
+template <typename T>
+__global__ void xchg_symbols_push_kernel(const T* __restrict__ s, long long n, XMap m) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const T v = s[i];
+    for (int q = 0; q < m.world; ++q)
+      reinterpret_cast<T*>(m.win[q] + kXchgFlagBytes + m.parity * m.buf_bytes)[i] = v;
+  }
+  xchg_cta_done(m);
+}
+
+__global__ void xchg_wait_kernel(const unsigned char* __restrict__ win, int slot0, int n, unsigned long long epoch,
+                                 long long timeout_ns, unsigned long long* __restrict__ status) {
+  xchg_block_wait(win, slot0, n, epoch, timeout_ns, status);
+}
+
+// Every rank's per-cluster gain shares Re(s^H H_dl,c x_c) gathered into every
+// window as [S][C_total] (kSlotGain + rank published when done).
+__global__ void xchg_gain_put_kernel(const float* __restrict__ gain_part, long long P, XMap m) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < P;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long s = i / m.C_local;
+    const int c = static_cast<int>(i - s * m.C_local);
+    const float v = gain_part[i];
+    for (int q = 0; q < m.world; ++q)
+      reinterpret_cast<float*>(m.win[q] + kXchgFlagBytes + m.parity * m.buf_bytes + m.sig_off)[s * m.C_total + m.c0 + c] = v;
+  }
+  xchg_cta_done(m);
+}
+
+// Wait for every rank's gain shares, then assemble_blocks' effective gain
+// (precode.cpp:123-131) with gain_reduce_kernel's arithmetic over all C_total
+// clusters in ascending order: bitwise the single-GPU gain.
+template <typename T>
+__global__ void xchg_gain_fuse_kernel(const unsigned char* __restrict__ win, unsigned long long epoch, int world,
+                                      int parity, long long buf_bytes, long long gain_off, int S, int C_total, int U,
+                                      long long timeout_ns, float* __restrict__ gain,
+                                      unsigned long long* __restrict__ status) {
+  if (!xchg_block_wait(win, kSlotGain, world, epoch, timeout_ns, status)) return;
+  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (!gain || s >= S) return;
+  const unsigned char* buf = win + kXchgFlagBytes + parity * buf_bytes;
+  const T* Sy = reinterpret_cast<const T*>(buf);
+  const float* part = reinterpret_cast<const float*>(buf + gain_off);
+  float se = 0.f;
+  for (int u = 0; u < U; ++u) {
+    const float2 v = ldcg_c(Sy, static_cast<size_t>(s) * U + u);
+    se = fmaf(v.y, v.y, fmaf(v.x, v.x, se));
+  }
+  float num = 0.f;
+  for (int c = 0; c < C_total; ++c) num += __ldcg(part + s * C_total + c);
+  gain[s] = se > 0.f ? num / se : 0.f;
 }
 
 __global__ void fuse_finalize_kernel(float2* __restrict__ xhat, const float* __restrict__ wsum, int S, int U) {

@@ -190,10 +190,18 @@ __device__ __forceinline__ void record_status(unsigned long long* st, long long 
 constexpr int kXchgMaxRanks = 8;
 constexpr int kXchgFlagBytes = 256;
 
+// Flag slots (u64) at the start of every window: uplink estimates published by
+// rank q -> slot q; downlink symbols pushed by the root -> kSlotSymbols;
+// downlink gain shares published by rank q -> kSlotGain + q.
+constexpr int kSlotSymbols = 8;
+constexpr int kSlotGain = 16;
+
 struct XMap {
   unsigned char* win[kXchgMaxRanks];  // every rank's window base (self included), in this process's address space
   unsigned int* counter;              // local CTA-completion counter (reset by the last CTA)
   unsigned long long epoch;           // batch epoch written to the owners' flags
+  int flag_slot;                      // xchg_cta_done publishes to slot flag_slot (+ rank if per_rank)
+  int per_rank;
   long long buf_bytes;                // bytes of one parity buffer
   long long sig_off;                  // offset of the sigma2 region inside a parity buffer
   int world, rank;
@@ -227,8 +235,35 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
+// Thread 0 of the block waits until slots [slot0, slot0 + n) of the local
+// window's flags reach `epoch` (acquire, system scope); a peer that never
+// publishes within timeout_ns is recorded as ST_XCHG_TIMEOUT.  Returns false
+// (for the whole block) on timeout.
+__device__ __forceinline__ bool xchg_block_wait(const unsigned char* win, int slot0, int n, unsigned long long epoch,
+                                                long long timeout_ns, unsigned long long* status) {
+  __shared__ int ok_;
+  if (threadIdx.x == 0) {
+    ok_ = 1;
+    const unsigned long long* flags = reinterpret_cast<const unsigned long long*>(win);
+    for (int q = 0; q < n && ok_; ++q) {
+      const unsigned long long t0 = globaltimer_ns();
+      while (ld_acquire_sys(flags + slot0 + q) < epoch) {
+        if (static_cast<long long>(globaltimer_ns() - t0) > timeout_ns) {
+          if (blockIdx.x == 0) record_status(status, 0, ST_XCHG_TIMEOUT, q);
+          ok_ = 0;
+          break;
+        }
+        __nanosleep(200);
+      }
+    }
+  }
+  __syncthreads();
+  return ok_ != 0;
+}
+
 // Called by every thread of every CTA after its last remote store: the last
-// CTA to finish publishes the epoch to every owner's flag slot `rank`.
+// CTA to finish publishes the epoch to flag slot flag_slot (+ rank) of every
+// rank's window.
 __device__ __forceinline__ void xchg_cta_done(const XMap& m) {
   __threadfence_system();
   __syncthreads();
@@ -236,8 +271,9 @@ __device__ __forceinline__ void xchg_cta_done(const XMap& m) {
     const unsigned t = atomicAdd(m.counter, 1u);
     if (t == gridDim.x - 1) {
       __threadfence_system();
+      const int slot = m.flag_slot + (m.per_rank ? m.rank : 0);
       for (int q = 0; q < m.world; ++q)
-        st_release_sys(reinterpret_cast<unsigned long long*>(m.win[q]) + m.rank, m.epoch);
+        st_release_sys(reinterpret_cast<unsigned long long*>(m.win[q]) + slot, m.epoch);
       *m.counter = 0u;  // next launch on this stream starts from zero
     }
   }

@@ -138,8 +138,9 @@ class Traffic:
       per cluster and subcarrier, downlink U complex per cluster and
       subcarrier (the symbol broadcast).
     bus: bytes per rank on the interconnect for the collectives actually issued,
-      with the NCCL-tests bus-bandwidth factors: reduce-scatter / all-to-all
-      (W-1)/W of the buffer, broadcast the buffer, all-reduce 2(W-1)/W."""
+      with the NCCL-tests bus-bandwidth factors: reduce-scatter / all-to-all /
+      all-gather (W-1)/W of the buffer, broadcast the buffer, all-reduce
+      2(W-1)/W (the p2p exchanges are accounted as the collective they replace)."""
     uplink_payload_bytes: int = 0
     downlink_payload_bytes: int = 0
     uplink_bus_bytes: int = 0
@@ -149,7 +150,7 @@ class Traffic:
 
     def add_bus(self, kind: str, nbytes: int, world: int, uplink: bool):
         f = {"reduce_scatter": (world - 1) / world, "all_to_all": (world - 1) / world, "broadcast": 1.0,
-             "all_reduce": 2 * (world - 1) / world}[kind] if world > 1 else 0.0
+             "all_gather": (world - 1) / world, "all_reduce": 2 * (world - 1) / world}[kind] if world > 1 else 0.0
         b = int(round(f * nbytes))
         if uplink:
             self.uplink_bus_bytes += b
@@ -324,7 +325,10 @@ class DistributedCD:
     # ---- downlink ---------------------------------------------------------
     def broadcast_symbols(self, s_root, *, src=0):
         """Root's [S, U] symbol batch to every rank (the centre -> cluster
-        broadcast, src/cluster.cpp:256-259)."""
+        broadcast, src/cluster.cpp:256-259).  In p2p mode the broadcast is part
+        of downlink() (NVLink stores into every window), so this is a no-op."""
+        if self.mode == "p2p":
+            return s_root
         buf = s_root if not s_root.is_complex() else torch.view_as_real(s_root)
         dist.broadcast(buf, src)
         self.traffic.add_bus("broadcast", buf.numel() * buf.element_size(), self.part.world, False)
@@ -334,6 +338,8 @@ class DistributedCD:
         """H: [S_local, C_local, U, Bc]; s: the broadcast [S, U] batch.  Returns
         (x_local [S_local, C_local, Bc], effective gain [S] on every rank)."""
         p = self.part
+        if self.mode == "p2p":
+            return self._downlink_p2p(H, s, rho=rho, K=K)
         s_mine = s[p.s_lo:p.s_hi].contiguous()
         U = s.shape[1]
         self.traffic.downlink_payload_bytes += s_mine.shape[0] * p.C_local * U * bytes_per_complex(s)
@@ -347,6 +353,26 @@ class DistributedCD:
         sf = s.float() if s.dtype == torch.float16 else torch.view_as_real(s)
         se = (sf.reshape(p.S, -1) ** 2).sum(dim=1)
         gain = torch.where(se > 0, num / torch.where(se > 0, se, torch.ones_like(se)), torch.zeros_like(se))
+        return x, gain
+
+
+    def _downlink_p2p(self, H, s, *, rho, K):
+        """decentralized_cd_precode's exchanges over peer memory
+        (dcdg_dl_precode_xchg): rank 0 (the centre) stores its symbols into
+        every window, every rank precodes its clusters from its own window and
+        gathers all C_total gain shares; no NCCL call."""
+        p = self.part
+        if not hasattr(self.compute, "eng"):
+            raise ValueError("the p2p exchange runs the CUDA kernels (CudaCompute)")
+        fp16 = H.dtype == torch.float16
+        U = H.shape[2]
+        esz = 4 if fp16 else 8
+        w = self._window(U, "fp16" if fp16 else "fp32")
+        x, gain = w.dl_precode(H, s if p.rank == 0 else None, root=0, c0=p.c_lo, C_total=p.C_total, rho=rho, K=K)
+        self.traffic.downlink_payload_bytes += p.S * p.C_local * U * esz
+        self.traffic.messages += p.S * p.C_local
+        self.traffic.add_bus("broadcast", p.S * U * esz, p.world, False)
+        self.traffic.add_bus("all_gather", p.S * p.C_total * 4, p.world, False)
         return x, gain
 
 

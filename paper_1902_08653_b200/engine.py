@@ -370,7 +370,9 @@ class ExchangeWindow:
             raise ValueError(f"batch of {S} subcarriers must divide over {world} GPUs")
         esz = 8 if fmt == "fp32" else 4
         s_own = S // world
-        nbytes = ((s_own * C_total * U * esz + 255) // 256) * 256 + (s_own * C_total * 4 if optimal else 0)
+        ul = ((s_own * C_total * U * esz + 255) // 256) * 256 + (s_own * C_total * 4 if optimal else 0)
+        dl = ((S * U * esz + 255) // 256) * 256 + S * C_total * 4
+        nbytes = max(ul, dl)
         self._w = C.c_void_p()
         check(lib().dcdg_xwin_create(eng._ctx, world, rank, nbytes, C.byref(self._w)))
 
@@ -414,6 +416,27 @@ class ExchangeWindow:
                                         float(n0), float(ex), fmt, _fusion(fusion), _ptr(xhat),
                                         self.eng._stream(stream)))
         return xhat
+
+
+    def dl_precode(self, H, s, *, root: int = 0, c0: int, C_total: int, rho: float, K: int = 3, want_gain=True,
+                   x=None, stream=None):
+        """This rank's clusters [c0, c0 + C) over all S subcarriers; `s` [S, U]
+        is read on the root only (the centre's symbols).  Returns (x_dl
+        [S, C, Bc], effective gain [S] or None) on every rank."""
+        fmt = _fmt_of(H)
+        S, Cn, U, Bc = _shape(H, fmt)
+        _need(H, "H")
+        if self.rank == root:
+            if s is None or _shape(s, fmt) != (S, U) or _fmt_of(s) != fmt:
+                raise ValueError("precoder: symbol vector length must match the users")
+            _need(s, "s")
+        if x is None:
+            x = complex_empty((S, Cn, Bc), fmt, H.device)
+        gain = torch.empty((S,), dtype=torch.float32, device=H.device) if want_gain else None
+        check(lib().dcdg_dl_precode_xchg(self.eng._ctx, self._w, root, _ptr(H), _ptr(s if self.rank == root else None),
+                                         S, Cn, c0, C_total, Bc, U, K, float(rho), fmt, _ptr(x), _ptr(gain),
+                                         self.eng._stream(stream)))
+        return x, gain
 
 
 def kernel_name(direction: str, bc: int, u: int, fmt: str) -> str:

@@ -54,6 +54,29 @@ def test_single_rank_window_is_bitwise_single_gpu(engine, port, shape, fmt, fusi
     w.close()
 
 
+@pytest.mark.parametrize("shape,fmt", [((8, 32, 16), "fp32"), ((8, 32, 16), "fp16"), ((2, 64, 8), "fp32"),
+                                       ((3, 24, 6), "fp32")])
+def test_single_rank_downlink_window_is_bitwise_single_gpu(engine, port, shape, fmt):
+    from helpers import qam_symbols
+    from paper_1902_08653_b200 import ExchangeWindow
+    C, BC, U = shape
+    S = 64
+    b = batch(C, BC, U, 16, S, seed=12)
+    H = to_dev(b["h_tiles"], fmt, pairs=True)
+    sym = to_dev(qam_symbols(S, U), fmt)
+    rho = float(np.sqrt(U))
+    want = engine.dl_precode(H, sym, rho=rho, K=3, want_gain=True)
+    engine.sync()
+    w = ExchangeWindow(engine, 1, 0, S=S, C_total=C, U=U, fmt=fmt)
+    for _ in range(3):
+        x, gain = w.dl_precode(H, sym, root=0, c0=0, C_total=C, rho=rho, K=3)
+        engine.sync()
+        assert torch.equal(x.view(torch.float32) if x.dtype != torch.float16 else x,
+                           want.x.view(torch.float32) if want.x.dtype != torch.float16 else want.x)
+        assert torch.equal(gain, want.gain)
+    w.close()
+
+
 def test_window_argument_errors(engine):
     from paper_1902_08653_b200 import ExchangeWindow, InvalidArgument
     with pytest.raises(InvalidArgument):
@@ -103,6 +126,16 @@ def _rank_main(rank, world, port_, fmt, fusion, out_dir):
     np.save(os.path.join(out_dir, f"r{rank}.npy"), torch.stack(outs).numpy())
     traffic = dcd.traffic.uplink_bus_bytes
     np.save(os.path.join(out_dir, f"t{rank}.npy"), np.array([traffic]))
+    # downlink: rank 0 (the centre) pushes its symbols, every rank precodes its clusters
+    if fusion == "uniform":
+        sy = torch.randn((S, U), dtype=torch.complex64, generator=g)
+        syd = sy.cuda() if fmt == "fp32" else torch.view_as_real(sy).to(torch.float16).cuda().contiguous()
+        dres = []
+        for _ in range(3):
+            xd, gain = dcd.downlink(Hl, dcd.broadcast_symbols(syd), rho=4.0, K=3)
+            dres.append((xd.cpu(), gain.cpu()))
+        eng.sync()
+        torch.save(dres, os.path.join(out_dir, f"d{rank}.pt"))
     # a rank whose peer never publishes: DCDG_ECUDA after the window timeout, no hang
     dist.barrier()
     if rank == 0:
@@ -142,5 +175,19 @@ def test_two_ranks_on_one_gpu_bitwise(engine, tmp_path, fmt, fusion):
         esz = 8 if fmt == "fp32" else 4
         per = S * 4 * U * esz + (S * 4 * 4 if fusion == "optimal" else 0)
         assert int(np.load(tmp_path / f"t{r}.npy")[0]) == 3 * per // 2
+    if fusion == "uniform":
+        g = torch.Generator().manual_seed(5)
+        torch.randn((S, C, U, BC), dtype=torch.complex64, generator=g)
+        torch.randn((S, C, BC), dtype=torch.complex64, generator=g)
+        sy = torch.randn((S, U), dtype=torch.complex64, generator=g)
+        syd = sy.cuda() if fmt == "fp32" else torch.view_as_real(sy).to(torch.float16).cuda().contiguous()
+        want_dl = engine.dl_precode(H, syd, rho=4.0, K=3, want_gain=True)
+        engine.sync()
+        for r in range(2):
+            for xd, gain in torch.load(tmp_path / f"d{r}.pt"):
+                wx = want_dl.x[:, 4 * r:4 * (r + 1)].cpu()
+                assert torch.equal(torch.view_as_real(xd) if xd.is_complex() else xd,
+                                   torch.view_as_real(wx) if wx.is_complex() else wx)
+                assert torch.equal(gain, want_dl.gain.cpu())
     msg = (tmp_path / "timeout.txt").read_text()
     assert "CudaError" in msg and "never published" in msg, msg
