@@ -1078,7 +1078,7 @@ int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* 
   // owner side: wait for every rank's epoch, then the ascending-cluster fusion
   const long long n = static_cast<long long>(S_own) * U;
   const int threads = 256;
-  const long long blocks = (n + threads - 1) / threads;
+  const long long blocks = std::max(1LL, std::min<long long>((n + threads - 1) / threads, 2LL * ctx->sms));
 #define XFUSE(T)                                                                                               \
   dcdg::xchg_fuse_kernel<T><<<blocks, threads, 0, st>>>(w->base, m.epoch, w->world, m.parity, w->buf_bytes,    \
                                                         sig_off, S_own, C_total, U, optimal, w->timeout_ns,     \
@@ -1172,7 +1172,7 @@ int dcdg_dl_precode_xchg(dcdg_ctx* ctx, dcdg_xwin* w, int root, const void* H, c
     ++ctx->launches;
     CUDA_TRY(cudaGetLastError(), "xchg_gain_put launch");
   }
-  const int gblocks = gain ? (S + threads - 1) / threads : 1;
+  const int gblocks = gain ? std::max(1, std::min((S + threads - 1) / threads, 2 * ctx->sms)) : 1;
 #define XGAIN(T)                                                                                                \
   dcdg::xchg_gain_fuse_kernel<T><<<gblocks, threads, 0, st>>>(w->base, m.epoch, w->world, m.parity, w->buf_bytes, \
                                                               gain_off, S, C_total, U, w->timeout_ns, gain,      \

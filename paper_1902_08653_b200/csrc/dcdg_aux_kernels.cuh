@@ -558,7 +558,7 @@ __global__ void xchg_put_kernel(const T* __restrict__ XL, const float* __restric
     if (i < n) {
       const long long p = i / m.U;
       const int u = static_cast<int>(i - p * m.U);
-      reinterpret_cast<T*>(xchg_x_dst(m, p))[u] = XL[i];
+      reinterpret_cast<T*>(xchg_x_dst(m, static_cast<int>(p)))[u] = XL[i];
     } else {
       const long long p = i - n;
       const long long s = p / m.C_local;
@@ -580,39 +580,43 @@ __global__ void xchg_fuse_kernel(const unsigned char* __restrict__ win, unsigned
                                  int parity, long long buf_bytes, long long sig_off, int S_own, int C_total, int U,
                                  bool optimal, long long timeout_ns, float2* __restrict__ xhat,
                                  unsigned long long* __restrict__ status) {
+  // one system-scope acquire per block; the grid is sized to the SMs and
+  // strides over the (subcarrier, user) outputs
   if (!xchg_block_wait(win, 0, world, epoch, timeout_ns, status)) return;
-  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= static_cast<long long>(S_own) * U) return;
-  const long long s = idx / U;
-  const int u = static_cast<int>(idx - s * U);
   const unsigned char* buf = win + kXchgFlagBytes + parity * buf_bytes;
   const T* XL = reinterpret_cast<const T*>(buf);
-  float2 acc = make_float2(0.f, 0.f);
-  if (!optimal) {
-    const float w = 1.f / static_cast<float>(C_total);
-    for (int c = 0; c < C_total; ++c) {
-      const float2 v = ldcg_c(XL, (static_cast<size_t>(s) * C_total + c) * U + u);
-      acc.x = fmaf(w, v.x, acc.x);
-      acc.y = fmaf(w, v.y, acc.y);
+  const float* sigma2 = reinterpret_cast<const float*>(buf + sig_off);
+  const long long n = static_cast<long long>(S_own) * U;
+  for (long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; idx < n;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long s = idx / U;
+    const int u = static_cast<int>(idx - s * U);
+    float2 acc = make_float2(0.f, 0.f);
+    if (!optimal) {
+      const float w = 1.f / static_cast<float>(C_total);
+      for (int c = 0; c < C_total; ++c) {
+        const float2 v = ldcg_c(XL, (static_cast<size_t>(s) * C_total + c) * U + u);
+        acc.x = fmaf(w, v.x, acc.x);
+        acc.y = fmaf(w, v.y, acc.y);
+      }
+    } else {
+      float total = 0.f;
+      bool bad = false;
+      for (int c = 0; c < C_total; ++c) {
+        const float v = __ldcg(sigma2 + s * C_total + c);
+        if (!(v > 0.f) || !isfinite(v)) bad = true;
+        total += 1.f / v;
+      }
+      if (bad && u == 0) record_status(status, s * C_total, ST_BAD_VARIANCE, 0);
+      for (int c = 0; c < C_total; ++c) {
+        const float w = (1.f / __ldcg(sigma2 + s * C_total + c)) / total;
+        const float2 v = ldcg_c(XL, (static_cast<size_t>(s) * C_total + c) * U + u);
+        acc.x = fmaf(w, v.x, acc.x);
+        acc.y = fmaf(w, v.y, acc.y);
+      }
     }
-  } else {
-    const float* sigma2 = reinterpret_cast<const float*>(buf + sig_off);
-    float total = 0.f;
-    bool bad = false;
-    for (int c = 0; c < C_total; ++c) {
-      const float v = __ldcg(sigma2 + s * C_total + c);
-      if (!(v > 0.f) || !isfinite(v)) bad = true;
-      total += 1.f / v;
-    }
-    if (bad && u == 0) record_status(status, s * C_total, ST_BAD_VARIANCE, 0);
-    for (int c = 0; c < C_total; ++c) {
-      const float w = (1.f / __ldcg(sigma2 + s * C_total + c)) / total;
-      const float2 v = ldcg_c(XL, (static_cast<size_t>(s) * C_total + c) * U + u);
-      acc.x = fmaf(w, v.x, acc.x);
-      acc.y = fmaf(w, v.y, acc.y);
-    }
+    xhat[idx] = acc;
   }
-  xhat[idx] = acc;
 }
 
 // Downlink (decentralized_cd_precode, precode.cpp:136-169, across GPUs):
@@ -659,19 +663,21 @@ __global__ void xchg_gain_fuse_kernel(const unsigned char* __restrict__ win, uns
                                       long long timeout_ns, float* __restrict__ gain,
                                       unsigned long long* __restrict__ status) {
   if (!xchg_block_wait(win, kSlotGain, world, epoch, timeout_ns, status)) return;
-  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (!gain || s >= S) return;
+  if (!gain) return;
   const unsigned char* buf = win + kXchgFlagBytes + parity * buf_bytes;
   const T* Sy = reinterpret_cast<const T*>(buf);
   const float* part = reinterpret_cast<const float*>(buf + gain_off);
-  float se = 0.f;
-  for (int u = 0; u < U; ++u) {
-    const float2 v = ldcg_c(Sy, static_cast<size_t>(s) * U + u);
-    se = fmaf(v.y, v.y, fmaf(v.x, v.x, se));
+  for (long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; s < S;
+       s += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float se = 0.f;
+    for (int u = 0; u < U; ++u) {
+      const float2 v = ldcg_c(Sy, static_cast<size_t>(s) * U + u);
+      se = fmaf(v.y, v.y, fmaf(v.x, v.x, se));
+    }
+    float num = 0.f;
+    for (int c = 0; c < C_total; ++c) num += __ldcg(part + s * C_total + c);
+    gain[s] = se > 0.f ? num / se : 0.f;
   }
-  float num = 0.f;
-  for (int c = 0; c < C_total; ++c) num += __ldcg(part + s * C_total + c);
-  gain[s] = se > 0.f ? num / se : 0.f;
 }
 
 __global__ void fuse_finalize_kernel(float2* __restrict__ xhat, const float* __restrict__ wsum, int S, int U) {

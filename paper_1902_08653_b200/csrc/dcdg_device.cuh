@@ -212,13 +212,14 @@ struct XMap {
 };
 
 // Destination of problem p's estimate (p = s*C_local + c, s global over the batch).
-__device__ __forceinline__ unsigned char* xchg_x_dst(const XMap& m, long long p) {
-  const long long s = p / m.C_local;
-  const int c = static_cast<int>(p - s * m.C_local);
-  const int owner = static_cast<int>(s / m.S_own);
-  const long long s_in = s - static_cast<long long>(owner) * m.S_own;
+// (P = S*C_local < 2^31 is checked on the host: 32-bit index math.)
+__device__ __forceinline__ unsigned char* xchg_x_dst(const XMap& m, int p) {
+  const int s = p / m.C_local;
+  const int c = p - s * m.C_local;
+  const int owner = s / m.S_own;
+  const int s_in = s - owner * m.S_own;
   return m.win[owner] + kXchgFlagBytes + m.parity * m.buf_bytes +
-         ((s_in * m.C_total + m.c0 + c) * m.U) * m.esz;
+         static_cast<long long>((s_in * m.C_total + m.c0 + c) * m.U) * m.esz;
 }
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
