@@ -384,10 +384,39 @@ int launch_solve(dcdg_ctx* ctx, const void* H, const void* V, int S, int C, int 
   return DCDG_OK;
 }
 
+// U = 16 runs two problems per warp (pev16_pair_kernel) for the common antenna
+// counts; everything else the one-warp-per-problem gram_chol.
+template <typename T, int BT>
+int launch_pev16(dcdg_ctx* ctx, const void* H, int P, float gam, float scale, bool rnd, float* s2, cudaStream_t st) {
+  constexpr size_t smem = 4 * (2 * 16 * (BT + 1) + 4 * 16 * 16) * sizeof(float2);
+  auto k = dcdg::pev16_pair_kernel<T, BT>;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  (void)attr;
+  k<<<(P + 7) / 8, 128, smem, st>>>(static_cast<const T*>(H), P, gam, scale, rnd, s2, ctx->d_status);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "post_eq_variance launch");
+  return DCDG_OK;
+}
+
+#ifndef DCDG_PEV_PAIR
+#define DCDG_PEV_PAIR 1
+#endif
 int launch_post_eq(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, double n0, double ex, int fmt, float* s2,
                    cudaStream_t st) {
-  return launch_gram_chol<dcdg::kPev>(ctx, H, P, 1, Bc, U, 1.f, static_cast<float>(ex / n0),
-                                      static_cast<float>(ex / U), fmt, s2, st);
+  const float gam = static_cast<float>(ex / n0), scale = static_cast<float>(ex / U);
+  if (DCDG_PEV_PAIR && U == 16) {
+    const bool rnd = fmt == DCDG_FP16;
+#define PEV16(BT)                                                                                  \
+  if (Bc == BT)                                                                                    \
+    return fmt == DCDG_FP16 ? launch_pev16<__half2, BT>(ctx, H, P, gam, scale, rnd, s2, st)        \
+                            : launch_pev16<float2, BT>(ctx, H, P, gam, scale, rnd, s2, st);
+    PEV16(32)
+    PEV16(16)
+    PEV16(64)
+#undef PEV16
+  }
+  return launch_gram_chol<dcdg::kPev>(ctx, H, P, 1, Bc, U, 1.f, gam, scale, fmt, s2, st);
 }
 
 }  // namespace

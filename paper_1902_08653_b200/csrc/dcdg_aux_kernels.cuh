@@ -497,6 +497,161 @@ __global__ void __launch_bounds__(128) gram_chol(const T* __restrict__ H, int P,
 }
 
 // ===========================================================================
+// Post-equalization variance for U = 16, two problems per warp (optimal
+// fusion, detect.cpp:112-130).  The Gram of each problem uses the whole warp
+// (lane = one 4x2 block of the 16x16 Gram, tiles staged in shared memory as in
+// gram_chol); the factorisation then runs both problems at once, one half-warp
+// each: lane (h, i) holds row i of A_h in registers, the left-looking Cholesky
+// publishes finished rows of L_h row-major in shared memory, and lane (h, c)
+// accumulates column c of L_h^{-1} (tr A^-1 = ||L^-1||_F^2, summed over the
+// half).  gram_chol's factorisation keeps half the warp idle at U = 16; here
+// every lane works, so the scalar Cholesky/inverse stream serves two problems.
+// ===========================================================================
+template <typename T, int BT>
+__global__ void __launch_bounds__(128) pev16_pair_kernel(const T* __restrict__ H, int P, float gam, float scale,
+                                                         bool round_fp16, float* __restrict__ out,
+                                                         unsigned long long* __restrict__ status) {
+  constexpr int N = 16, PR = BT;  // users, staged rows
+  extern __shared__ float2 psm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float2* Hs = psm + warp * (2 * N * (PR + 1) + 4 * N * N);  // 2 staged tiles, column stride PR+1
+  float2* A = Hs + 2 * N * (PR + 1);                        // 2 x [16][16] column-major (lower used)
+  float2* Lr = A + 2 * N * N;                               // 2 x [16][16] row-major L
+  const long long p0 = (static_cast<long long>(blockIdx.x) * 4 + warp) * 2;
+  if (p0 >= P) return;
+  // ---- stage both tiles (the second clamped to P-1 when P is odd)
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const long long p = min(p0 + t, static_cast<long long>(P) - 1);
+    const T* h = H + static_cast<size_t>(p) * BT * N;
+    float2* hs = Hs + t * N * (PR + 1);
+    if constexpr (sizeof(T) == 8 && BT % 2 == 0) {
+      const float4* t4 = reinterpret_cast<const float4*>(h);
+#pragma unroll
+      for (int i = 0; i < BT * N / 64; ++i) {
+        const int idx = lane + 32 * i;
+        const int j = idx / (BT / 2), rr = idx - j * (BT / 2);
+        const float4 v = __ldg(t4 + idx);
+        hs[j * (PR + 1) + 2 * rr] = make_float2(v.x, v.y);
+        hs[j * (PR + 1) + 2 * rr + 1] = make_float2(v.z, v.w);
+      }
+    } else {
+      for (int idx = lane; idx < BT * N; idx += 32) {
+        const int j = idx / BT, b = idx - j * BT;
+        hs[j * (PR + 1) + b] = ldv(h + static_cast<size_t>(j) * BT, b);
+      }
+    }
+  }
+  __syncwarp();
+  // ---- Grams: lane -> 4x2 block (rows 4*ib.., columns 2*jb..) of G_t; A_t = I + gam G_t
+  const int i0 = 4 * (lane >> 3), j0 = 2 * (lane & 7);
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const float2* hs = Hs + t * N * (PR + 1);
+    float2 acc[4][2];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+#pragma unroll 8
+    for (int b = 0; b < PR; ++b) {
+      float2 a[4], c[2], cs[2];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = hs[(i0 + r) * (PR + 1) + b];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        c[q] = hs[(j0 + q) * (PR + 1) + b];
+        cs[q] = make_float2(c[q].y, -c[q].x);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) acc[r][q] = ffma2(a[r].y, cs[q], ffma2(a[r].x, c[q], acc[r][q]));
+    }
+    float2* At = A + t * N * N;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int i = i0 + r, j = j0 + q;
+        if (i >= j)  // detect.cpp:118-121
+          At[j * N + i] = make_float2((i == j ? 1.f : 0.f) + gam * acc[r][q].x, gam * acc[r][q].y);
+      }
+  }
+  __syncwarp();
+  // ---- factorisation, half-warp h = problem p0 + h, lane i = row i
+  const int hf = lane >> 4, i = lane & 15;
+  const float2* Ah = A + hf * N * N;
+  float2* Lh = Lr + hf * N * N;
+  float maxdiag = fabsf(Ah[i * N + i].x);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) maxdiag = fmaxf(maxdiag, __shfl_xor_sync(0xffffffffu, maxdiag, o));
+  const float floor_ = 1e-14f * maxdiag;  // numerics.cpp:38-41,55-56
+  float2 a[N], l[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    a[k] = (k <= i) ? Ah[k * N + i] : make_float2(0.f, 0.f);
+    l[k] = make_float2(0.f, 0.f);
+  }
+  bool singular = false;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    if (i == j) {  // d_j = A_jj - sum_k |L_jk|^2 ; L_jj = sqrt(d_j)   (numerics.cpp:47-52)
+      float d = a[j].x;
+#pragma unroll
+      for (int k = 0; k < j; ++k) d -= l[k].x * l[k].x + l[k].y * l[k].y;
+      if (!(d > floor_)) singular = true;
+      l[j] = make_float2(__fsqrt_rn(fmaxf(d, 1e-30f)), 0.f);
+#pragma unroll
+      for (int k = 0; k <= j; ++k) Lh[j * N + k] = l[k];
+    }
+    __syncwarp();
+    if (i > j) {  // L_ij = (A_ij - sum_{k<j} L_ik conj(L_jk)) / L_jj   (numerics.cpp:53-56)
+      float sr = a[j].x, si = a[j].y;
+#pragma unroll
+      for (int k = 0; k < j; ++k) {
+        const float2 b = Lh[j * N + k];
+        sr -= l[k].x * b.x + l[k].y * b.y;
+        si -= l[k].y * b.x - l[k].x * b.y;
+      }
+      const float inv = __frcp_rn(Lh[j * N + j].x);
+      l[j] = make_float2(sr * inv, si * inv);
+    }
+  }
+  __syncwarp();
+  // X = L^-1: lane (h, c) holds column c; X_ic = -(sum_{k=c}^{i-1} L_ik X_kc) / L_ii
+  const int c = i;
+  float tr = 0.f;
+  float2 x[N];
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    const float linv = __frcp_rn(Lh[r * N + r].x);
+    float sr = 0.f, si = 0.f;
+#pragma unroll
+    for (int k = 0; k < r; ++k) {
+      const float2 lk = Lh[r * N + k];
+      const float2 xk = x[k];  // zero above the diagonal (k < c)
+      sr += lk.x * xk.x - lk.y * xk.y;
+      si += lk.x * xk.y + lk.y * xk.x;
+    }
+    float2 v;
+    if (c == r) v = make_float2(linv, 0.f);
+    else if (c < r) v = make_float2(-sr * linv, -si * linv);
+    else v = make_float2(0.f, 0.f);
+    x[r] = v;
+    tr = fmaf(v.x, v.x, fmaf(v.y, v.y, tr));
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+  const unsigned sing = __ballot_sync(0xffffffffu, singular);
+  const long long p = p0 + hf;
+  if (i == 0 && p < P) {
+    float s2 = scale * tr;
+    if (round_fp16) s2 = __half2float(__float2half_rn(s2));
+    out[p] = s2;
+    if ((sing >> (16 * hf)) & 0xffffu) record_status(status, p, ST_SINGULAR, 0);
+  }
+}
+
+// ===========================================================================
 // Fusion (detect.cpp:132-145,180-187): one thread per (subcarrier, user),
 // ascending cluster order.  Full fusion (C == C_total) reproduces the
 // reference's weights; partial fusion (C < C_total, multi-GPU) emits
