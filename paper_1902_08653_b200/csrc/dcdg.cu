@@ -388,7 +388,7 @@ int launch_solve(dcdg_ctx* ctx, const void* H, const void* V, int S, int C, int 
 // counts; everything else the one-warp-per-problem gram_chol.
 template <typename T, int BT>
 int launch_pev16(dcdg_ctx* ctx, const void* H, int P, float gam, float scale, bool rnd, float* s2, cudaStream_t st) {
-  constexpr size_t smem = 4 * (2 * 16 * (BT + 1) + 4 * 16 * 16) * sizeof(float2);
+  constexpr size_t smem = 4 * (2 * 16 * (BT + 1) + 2 * 16 * 16) * sizeof(float2);
   auto k = dcdg::pev16_pair_kernel<T, BT>;
   static const cudaError_t attr =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

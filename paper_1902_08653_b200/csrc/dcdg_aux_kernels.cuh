@@ -514,9 +514,9 @@ __global__ void __launch_bounds__(128) pev16_pair_kernel(const T* __restrict__ H
   constexpr int N = 16, PR = BT;  // users, staged rows
   extern __shared__ float2 psm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float2* Hs = psm + warp * (2 * N * (PR + 1) + 4 * N * N);  // 2 staged tiles, column stride PR+1
+  float2* Hs = psm + warp * (2 * N * (PR + 1) + 2 * N * N);  // 2 staged tiles, column stride PR+1
   float2* A = Hs + 2 * N * (PR + 1);                        // 2 x [16][16] column-major (lower used)
-  float2* Lr = A + 2 * N * N;                               // 2 x [16][16] row-major L
+  float2* Lr = Hs;                                          // 2 x [16][16] row-major L, over the tiles
   const long long p0 = (static_cast<long long>(blockIdx.x) * 4 + warp) * 2;
   if (p0 >= P) return;
   // ---- stage both tiles (the second clamped to P-1 when P is odd)
@@ -548,23 +548,27 @@ __global__ void __launch_bounds__(128) pev16_pair_kernel(const T* __restrict__ H
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
     const float2* hs = Hs + t * N * (PR + 1);
-    float2 acc[4][2];
+    // conj(a) c = (a.x c.x + a.y c.y, a.x c.y - a.y c.x): accumulate
+    // P = sum a.x (c.x, c.y) and Q = sum a.y (c.x, c.y), combine once per entry
+    float2 pa[4][2], qa[4][2];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) pa[r][q] = qa[r][q] = make_float2(0.f, 0.f);
 #pragma unroll 8
     for (int b = 0; b < PR; ++b) {
-      float2 a[4], c[2], cs[2];
+      float2 a[4], c[2];
 #pragma unroll
       for (int r = 0; r < 4; ++r) a[r] = hs[(i0 + r) * (PR + 1) + b];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        c[q] = hs[(j0 + q) * (PR + 1) + b];
-        cs[q] = make_float2(c[q].y, -c[q].x);
-      }
+      for (int q = 0; q < 2; ++q) c[q] = hs[(j0 + q) * (PR + 1) + b];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int q = 0; q < 2; ++q) acc[r][q] = ffma2(a[r].y, cs[q], ffma2(a[r].x, c[q], acc[r][q]));
+        for (int q = 0; q < 2; ++q) {
+          pa[r][q] = ffma2(a[r].x, c[q], pa[r][q]);
+          qa[r][q] = ffma2(a[r].y, c[q], qa[r][q]);
+        }
     }
     float2* At = A + t * N * N;
 #pragma unroll
@@ -572,11 +576,12 @@ __global__ void __launch_bounds__(128) pev16_pair_kernel(const T* __restrict__ H
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int i = i0 + r, j = j0 + q;
+        const float gr = pa[r][q].x + qa[r][q].y, gi = pa[r][q].y - qa[r][q].x;
         if (i >= j)  // detect.cpp:118-121
-          At[j * N + i] = make_float2((i == j ? 1.f : 0.f) + gam * acc[r][q].x, gam * acc[r][q].y);
+          At[j * N + i] = make_float2((i == j ? 1.f : 0.f) + gam * gr, gam * gi);
       }
   }
-  __syncwarp();
+  __syncwarp();  // the staged tiles are dead from here: Lr reuses their space
   // ---- factorisation, half-warp h = problem p0 + h, lane i = row i
   const int hf = lane >> 4, i = lane & 15;
   const float2* Ah = A + hf * N * N;
