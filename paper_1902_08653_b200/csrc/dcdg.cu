@@ -16,6 +16,7 @@
 #include "dcdg_mw_kernels.cuh"
 #include "dcdg_sweep_kernels.cuh"
 #include "dcdg_reg_kernels.cuh"
+#include "dcdg_split_kernels.cuh"
 
 struct dcdg_ctx {
   int device = 0;
@@ -231,18 +232,57 @@ cudaError_t launch_dl_mw(dcdg_ctx* ctx, const void* H, const void* S, int P, int
             : launch_dl_mw_k<BC, U, NW, MINB, false>(ctx, H, S, P, C, K, rho_c, X, gp, st);
 }
 
-struct Spec {
-  int bc, u, fmt, g;  // g > 0: lanes per problem; g < 0: -(warps per problem)
-  UlLaunch ul;
-  DlLaunch dl;
-};
+// Kernel of one direction: kind 0 register-resident (a = lanes per problem),
+// 1 multi-warp (a = warps per problem), 2 split tile (a = lanes, b = register
+// columns; dcdg_split_kernels.cuh).
+// Split-tile kernels (dcdg_split_kernels.cuh): one-warp CTAs, grid = SMs x occupancy.
+template <int BC, int U, int G, int JR, int MINB>
+cudaError_t launch_ul_split(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                            const dcdg::XMap* /*exchange via xchg_put_kernel*/, cudaStream_t st) {
+  constexpr int NPW = 32 / G;
+  constexpr size_t smem = dcdg::split_cols_bytes(BC, U, JR, G) + NPW * dcdg::ul_scal_bytes(U, 2);
+  auto kern = dcdg::ul_split_f32<BC, U, G, JR, MINB, 1>;
+  static const int occ = occupancy_of(kern, smem, 32);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int blocks = std::min(nsets, ctx->sms * occ);
+  kern<<<blocks, 32, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K, kappa,
+                                 static_cast<float2*>(X));
+  return cudaGetLastError();
+}
 
-#define SPEC_F32(BC, U, G)                                                           \
-  {BC, U, DCDG_FP32, G, launch_ul_f32<BC, U, G, minb(DCDG_MIN_WARPS_UL_F32)>, \
-   launch_dl_f32<BC, U, G, minb(DCDG_MIN_WARPS_DL_F32)>}
-#define SPEC_F16(BC, U, G)                                                           \
-  {BC, U, DCDG_FP16, G, launch_ul_f16<BC, U, G, minb(DCDG_MIN_WARPS_UL_F16)>, \
-   launch_dl_f16<BC, U, G, minb(DCDG_MIN_WARPS_DL_F16)>}
+template <int BC, int U, int G, int JR, int MINB, bool GAIN>
+cudaError_t launch_dl_split_k(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
+                              float* gp, cudaStream_t st) {
+  constexpr int NPW = 32 / G;
+  constexpr size_t smem = dcdg::split_cols_bytes(BC, U, JR, G) + NPW * dcdg::dl_scal_bytes(U);
+  auto kern = dcdg::dl_split_f32<BC, U, G, JR, MINB, GAIN>;
+  static const int occ = occupancy_of(kern, smem, 32);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int blocks = std::min(nsets, ctx->sms * occ);
+  kern<<<blocks, 32, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(S), P, C, K, rho_c,
+                                 static_cast<float2*>(X), gp, ctx->d_status);
+  return cudaGetLastError();
+}
+
+template <int BC, int U, int G, int JR, int MINB>
+cudaError_t launch_dl_split(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
+                            float* gp, cudaStream_t st) {
+  return gp ? launch_dl_split_k<BC, U, G, JR, MINB, true>(ctx, H, S, P, C, K, rho_c, X, gp, st)
+            : launch_dl_split_k<BC, U, G, JR, MINB, false>(ctx, H, S, P, C, K, rho_c, X, gp, st);
+}
+
+struct KDesc {
+  int kind, a, b;
+};
+constexpr int kReg = 0, kMw = 1, kSplit = 2;
+
+struct Spec {
+  int bc, u, fmt;
+  UlLaunch ul;
+  KDesc ulk;
+  DlLaunch dl;
+  KDesc dlk;
+};
 
 // Register-resident specialisations: B_c*U/G complex per lane = 128 regs of
 // channel for fp32 (64-128 for fp16).  Everything else runs the generic path.
@@ -260,36 +300,48 @@ struct Spec {
 #ifndef DCDG_MIN_WARPS_DL_F16
 #define DCDG_MIN_WARPS_DL_F16 8
 #endif
+#ifndef DCDG_MIN_WARPS_SPLIT
+#define DCDG_MIN_WARPS_SPLIT 8
+#endif
 // lanes per problem of the fp16 north-star kernel (B_c=32, U=16)
 #ifndef DCDG_F16_G_TARGET
 #define DCDG_F16_G_TARGET 4
 #endif
 constexpr int minb(int warps) { return warps / kWarps > 0 ? warps / kWarps : 1; }
 constexpr int minb_mw(int warps, int nw) { return warps / nw > 0 ? warps / nw : 1; }
-#define SPEC_MW_F32(BC, U, NW)                                                                  \
-  {BC, U, DCDG_FP32, -(NW), launch_ul_mw<BC, U, NW, minb_mw(DCDG_MIN_WARPS_UL_F32, NW)>, \
-   launch_dl_mw<BC, U, NW, minb_mw(DCDG_MIN_WARPS_UL_F32, NW)>}
 
+#define UL_REG(BC, U, G) launch_ul_f32<BC, U, G, minb(DCDG_MIN_WARPS_UL_F32)>, KDesc{kReg, G, 0}
+#define DL_REG(BC, U, G) launch_dl_f32<BC, U, G, minb(DCDG_MIN_WARPS_DL_F32)>, KDesc{kReg, G, 0}
+#define UL_MW(BC, U, NW) launch_ul_mw<BC, U, NW, minb_mw(DCDG_MIN_WARPS_UL_F32, NW)>, KDesc{kMw, NW, 0}
+#define DL_MW(BC, U, NW) launch_dl_mw<BC, U, NW, minb_mw(DCDG_MIN_WARPS_UL_F32, NW)>, KDesc{kMw, NW, 0}
+#define UL_SPLIT(BC, U, G, JR) launch_ul_split<BC, U, G, JR, DCDG_MIN_WARPS_SPLIT>, KDesc{kSplit, G, JR}
+#define DL_SPLIT(BC, U, G, JR) launch_dl_split<BC, U, G, JR, DCDG_MIN_WARPS_SPLIT>, KDesc{kSplit, G, JR}
+#define UL_F16(BC, U, G) launch_ul_f16<BC, U, G, minb(DCDG_MIN_WARPS_UL_F16)>, KDesc{kReg, G, 0}
+#define DL_F16(BC, U, G) launch_dl_f16<BC, U, G, minb(DCDG_MIN_WARPS_DL_F16)>, KDesc{kReg, G, 0}
+
+// Measured on B200 (profiles/r01_configs4_sweep.json, scripts/lab/lab_split2.cu):
+// the split tile wins wherever the register kernel needs G >= 16 lanes or
+// several warps per problem; at B_c = 32, U = 16 the register kernel stays.
 const Spec kSpecs[] = {
-    SPEC_F32(32, 16, 8),   // north-star target: B=256, C=8, U=16
-    SPEC_F32(32, 8, 4),    // paper / config 1: B_c=32, U=8
-    SPEC_F32(16, 16, 4),   // B=128, C=8
-    SPEC_F32(64, 16, 16),  // B=256, C=4 / B=512, C=8
-    SPEC_F32(64, 8, 8),
-    SPEC_F32(128, 16, 32),  // B=128, C=1 / B=256, C=2 / B=512, C=4
-    SPEC_F32(16, 32, 8),    // configs[4]: U=32
-    SPEC_F32(32, 32, 16),
-    SPEC_F32(64, 32, 32),
-    SPEC_MW_F32(256, 16, 2),  // large tiles: one CTA of NW warps per problem
-    SPEC_MW_F32(512, 16, 4),
-    SPEC_MW_F32(1024, 16, 8),
-    SPEC_MW_F32(128, 32, 2),
-    SPEC_MW_F32(256, 32, 4),
-    SPEC_MW_F32(512, 32, 8),
-    SPEC_F16(32, 16, DCDG_F16_G_TARGET),  // north-star shape, half2
-    SPEC_F16(32, 8, 4),
-    SPEC_F16(16, 16, 4),
-    SPEC_F16(64, 16, 8),
+    {32, 16, DCDG_FP32, UL_REG(32, 16, 8), DL_REG(32, 16, 8)},  // north-star target: B=256, C=8, U=16
+    {32, 8, DCDG_FP32, UL_REG(32, 8, 4), DL_REG(32, 8, 4)},     // paper / config 1: B_c=32, U=8
+    {16, 16, DCDG_FP32, UL_REG(16, 16, 4), DL_REG(16, 16, 4)},  // B=128, C=8
+    {64, 16, DCDG_FP32, UL_REG(64, 16, 16), DL_REG(64, 16, 16)},  // B=256, C=4 / B=512, C=8
+    {64, 8, DCDG_FP32, UL_REG(64, 8, 8), DL_REG(64, 8, 8)},
+    {128, 16, DCDG_FP32, UL_SPLIT(128, 16, 16, 8), DL_REG(128, 16, 32)},  // B=128,C=1 / 256,2 / 512,4
+    {16, 32, DCDG_FP32, UL_REG(16, 32, 8), DL_REG(16, 32, 8)},    // configs[4]: U=32
+    {32, 32, DCDG_FP32, UL_SPLIT(32, 32, 8, 16), DL_SPLIT(32, 32, 8, 16)},
+    {64, 32, DCDG_FP32, UL_SPLIT(64, 32, 16, 16), DL_SPLIT(64, 32, 16, 16)},
+    {128, 32, DCDG_FP32, UL_SPLIT(128, 32, 32, 16), DL_SPLIT(128, 32, 32, 16)},
+    {256, 16, DCDG_FP32, UL_SPLIT(256, 16, 32, 8), DL_SPLIT(256, 16, 32, 8)},
+    {512, 16, DCDG_FP32, UL_SPLIT(512, 16, 32, 4), DL_MW(512, 16, 4)},
+    {256, 32, DCDG_FP32, UL_SPLIT(256, 32, 32, 8), DL_SPLIT(256, 32, 32, 8)},
+    {512, 32, DCDG_FP32, UL_SPLIT(512, 32, 32, 4), DL_MW(512, 32, 8)},
+    {1024, 16, DCDG_FP32, UL_MW(1024, 16, 8), DL_MW(1024, 16, 8)},  // one CTA of 8 warps per problem
+    {32, 16, DCDG_FP16, UL_F16(32, 16, DCDG_F16_G_TARGET), DL_F16(32, 16, DCDG_F16_G_TARGET)},  // half2 target
+    {32, 8, DCDG_FP16, UL_F16(32, 8, 4), DL_F16(32, 8, 4)},
+    {16, 16, DCDG_FP16, UL_F16(16, 16, 4), DL_F16(16, 16, 4)},
+    {64, 16, DCDG_FP16, UL_F16(64, 16, 8), DL_F16(64, 16, 8)},
 };
 
 const Spec* find_spec(int bc, int u, int fmt) {
@@ -472,10 +524,13 @@ int dcdg_kernel_name(int direction, int Bc, int U, int fmt, char* buf, int len) 
   char tmp[96];
   const char* dir = direction ? "dl" : "ul";
   const char* f = fmt == DCDG_FP16 ? "f16" : "f32";
-  if (s && s->g < 0)
-    std::snprintf(tmp, sizeof tmp, "%s_mw_%s<%d,%d,%d>", dir, f, Bc, U, -s->g);
-  else if (s)
-    std::snprintf(tmp, sizeof tmp, "%s_reg_%s<%d,%d,%d>", dir, f, Bc, U, s->g);
+  const KDesc* kd = s ? (direction ? &s->dlk : &s->ulk) : nullptr;
+  if (kd && kd->kind == kMw)
+    std::snprintf(tmp, sizeof tmp, "%s_mw_%s<%d,%d,%d>", dir, f, Bc, U, kd->a);
+  else if (kd && kd->kind == kSplit)
+    std::snprintf(tmp, sizeof tmp, "%s_split_%s<%d,%d,%d,%d>", dir, f, Bc, U, kd->a, kd->b);
+  else if (kd)
+    std::snprintf(tmp, sizeof tmp, "%s_reg_%s<%d,%d,%d>", dir, f, Bc, U, kd->a);
   else
     std::snprintf(tmp, sizeof tmp, "%s_generic_%s", dir, f);
   if (buf && len > 0) {
@@ -1081,7 +1136,7 @@ int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* 
 
   const float kappa = static_cast<float>(n0 / ex);
   const Spec* spec = find_spec(Bc, U, fmt);
-  if (spec && spec->g > 0 && !optimal) {
+  if (spec && spec->ulk.kind == kReg && !optimal) {
     // fused: the CD kernel stores into the owners' windows and signals
     CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, nullptr, &m, st), "ul_detect_xchg launch");
     ++ctx->launches;

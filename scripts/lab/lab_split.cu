@@ -30,7 +30,13 @@ __global__ void fill_normal(float* p, size_t n, uint32_t seed, float scale) {
   }
 }
 
-constexpr int BC = 32, U = 16, K = 3;
+#ifndef LAB_U
+#define LAB_U 16
+#endif
+#ifndef LAB_GREF
+#define LAB_GREF 8
+#endif
+constexpr int BC = 32, U = LAB_U, K = 3;
 static int g_sms = 148;
 
 template <typename Kern>
@@ -116,27 +122,31 @@ int main(int argc, char** argv) {
   CK(cudaDeviceSynchronize());
   const float kappa = 1.6f;
   const double bytes = (double)P * (BC * U + BC + U) * 8;
+  std::printf("U=%d, %d problems\n", U, P);
 
   // the current hot-path kernel (reference for timing and results)
   std::vector<Result> res;
   {
-    constexpr int G = 8, NPW = 4, LB = 2;
+    constexpr int G = LAB_GREF, NPW = 32 / G, LB = 2;
     constexpr size_t smem = dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U, LB), NPW, 1>::kBytes;
     auto k = dcdg::ul_reg_f32<BC, U, G, 1, 8, LB>;
     const int occ = occ_of(k, smem, 32);
     const int blocks = std::min((P + NPW - 1) / NPW, g_sms * occ);
-    auto launch = [&] { k<<<blocks, 32, smem>>>(H, Y, P, K, kappa, Xref); };
+    auto launch = [&] { k<<<blocks, 32, smem>>>(H, Y, P, K, kappa, Xref, dcdg::XMap{}); };
     launch();
     CK(cudaDeviceSynchronize());
-    res.push_back(run("ul_reg_f32<32,16,8> (current)", launch, occ, regs_of(k), Xref, Xref, P, reps));
+    res.push_back(run("ul_reg_f32 (current)", launch, occ, regs_of(k), Xref, Xref, P, reps));
     res.back().maxrel = 0;
   }
+#if LAB_U == 32
+  res.push_back(run_split<16, 8, 1, 8>("split U=32 G=8 JR=16 MINB=8", H, Y, kappa, Xref, X, P, reps));
+  res.push_back(run_split<12, 8, 1, 8>("split U=32 G=8 JR=12 MINB=8", H, Y, kappa, Xref, X, P, reps));
+  res.push_back(run_split<8, 12, 1, 8>("split U=32 G=8 JR=8 MINB=12", H, Y, kappa, Xref, X, P, reps));
+  res.push_back(run_split<16, 12, 1, 16>("split U=32 G=16 JR=16 MINB=12", H, Y, kappa, Xref, X, P, reps));
+  res.push_back(run_split<16, 16, 1, 16>("split U=32 G=16 JR=16 MINB=16", H, Y, kappa, Xref, X, P, reps));
+#else
   res.push_back(run_split<8, 16, 1>("split G=8 JR=8 MINB=16 PF=1", H, Y, kappa, Xref, X, P, reps));
-  res.push_back(run_split<8, 9, 1, 4>("split G=4 JR=8 MINB=9 PF=1", H, Y, kappa, Xref, X, P, reps));
-  res.push_back(run_split<8, 9, 2, 4>("split G=4 JR=8 MINB=9 PF=2", H, Y, kappa, Xref, X, P, reps));
-  res.push_back(run_split<6, 10, 1, 4>("split G=4 JR=6 MINB=10 PF=1", H, Y, kappa, Xref, X, P, reps));
-  res.push_back(run_split<10, 8, 1, 4>("split G=4 JR=10 MINB=8 PF=1", H, Y, kappa, Xref, X, P, reps));
-  res.push_back(run_split<4, 8, 1, 4>("split G=4 JR=4 MINB=8 PF=1", H, Y, kappa, Xref, X, P, reps));
+#endif
   for (const auto& r : res)
     std::printf("%-34s %8.4f ms  %7.1f GB/s  %5.1f%% of 6546.6  occ %2d  regs %3d  maxrel %.2e\n", r.name, r.ms,
                 bytes / r.ms / 1e6, 100.0 * bytes / r.ms / 1e6 / 6546.6, r.occ, r.regs, r.maxrel);
