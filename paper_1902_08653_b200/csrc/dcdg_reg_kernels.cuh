@@ -535,10 +535,12 @@ __global__ void __launch_bounds__(32 * W, MINB)
 
 // ===========================================================================
 // Downlink, fp32, packed row pairs (see ul_reg_f32).  The dual rows h_u are
-// the uplink columns (conj_rows, precode.cpp:19-27), normalised in registers
-// (p_u = 1/||h_u||, precode.cpp:69-87).  Scalar block per problem:
-// float4 ss[U] = (Re s~_u, Im s~_u, p_u, -), s~_u = p_u s_u;
-// float4 gp[U/2] = (Re G~, Im G~, -Im G~, Re G~), G~ = h~_{2i+1}^H h~_{2i};
+// the uplink columns (conj_rows, precode.cpp:19-27).  The reference
+// normalises them (p_u = 1/||h_u||, precode.cpp:69-87); here they stay raw and
+// the normalisation moves into the scalars: x -= q_u (h_u^H x - s_u) h_u with
+// q_u = 1/||h_u||^2 is the normalised update exactly.  Scalar block per problem:
+// float4 ss[U] = (Re q_u s_u, Im q_u s_u, q_u, -);
+// float4 gp[U/2] = (Re G, Im G, -Im G, Re G), G = h_{2i+1}^H h_{2i};
 // float2 sraw[U] (the received symbols).
 // ===========================================================================
 template <int BC, int U, int G, int W, int MINB, bool GAIN>
@@ -622,45 +624,28 @@ __global__ void __launch_bounds__(32 * W, MINB)
     int zero_user = -1;
     float* sf = reinterpret_cast<float*>(ss);
     float* gf = reinterpret_cast<float*>(gp);
+    // The rows stay unnormalised: with q_u = 1/||h_u||^2 the normalised update
+    // (precode.cpp:69-94) x -= (h~_u^H x - s~_u) h~_u is x -= q_u (h_u^H x - s_u) h_u,
+    // so the scalar block holds (q_u s_u, q_u) and the raw pair Gram.
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int idx = k * PER + i;
       if (idx < U) {
         if (vv[i] == 0.f && zero_user < 0) zero_user = idx;
-        const float pinv = rsqrtf(vv[i]);
-        sf[idx * 4 + 2] = pinv;  // p_u = 1/||h_u||
-        sf[idx * 4 + 3] = vv[i] * pinv;
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int idx = k * PER + i;
-      if (idx < U) {
-        const float2 s = sraw[idx];
-        const float pj = sf[idx * 4 + 2];
-        sf[idx * 4] = s.x * pj;  // s~_u = p_u s_u
-        sf[idx * 4 + 1] = s.y * pj;
+        const float q = __frcp_rn(vv[i]);
+        const float2 sv = sraw[idx];
+        sf[idx * 4 + 0] = q * sv.x;
+        sf[idx * 4 + 1] = q * sv.y;
+        sf[idx * 4 + 2] = q;
       } else {
         const int gi = idx - U, pr = gi >> 1;
-        const float val = vv[i] * (sf[(2 * pr + 1) * 4 + 2] * sf[(2 * pr) * 4 + 2]);  // G~ = p_a p_b G
         if (gi & 1) {
-          gf[pr * 4 + 1] = val;
-          gf[pr * 4 + 2] = -val;
+          gf[pr * 4 + 1] = vv[i];
+          gf[pr * 4 + 2] = -vv[i];
         } else {
-          gf[pr * 4 + 0] = val;
-          gf[pr * 4 + 3] = val;
+          gf[pr * 4 + 0] = vv[i];
+          gf[pr * 4 + 3] = vv[i];
         }
-      }
-    }
-    // normalise the rows held in registers
-#pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const float pj = sf[j * 4 + 2];
-#pragma unroll
-      for (int c = 0; c < NP; ++c) {
-        hr[j][c] = fmul2(pj, hr[j][c]);
-        hi[j][c] = fmul2(pj, hi[j][c]);
       }
     }
     __syncwarp();
@@ -699,11 +684,11 @@ __global__ void __launch_bounds__(32 * W, MINB)
             d1 = fadd2(d1, shfl_xor2(d1, o));
           }
         }
-        // resid_u = h~_u^H x - s~_u ; x -= resid_u h~_u   (precode.cpp:89-94)
-        const float2 r0 = fadd2(d0, make_float2(-S0.x, -S0.y));
-        d1 = ffma2(-r0.x, make_float2(GG.x, GG.y), d1);
+        // r_u = q_u (h_u^H x - s_u) ; x -= r_u h_u   (precode.cpp:89-94 on unnormalised rows)
+        const float2 r0 = ffma2(S0.z, d0, make_float2(-S0.x, -S0.y));
+        d1 = ffma2(-r0.x, make_float2(GG.x, GG.y), d1);  // h_1^H (x - r_0 h_0) = d_1 - r_0 G_10
         d1 = ffma2(-r0.y, make_float2(GG.z, GG.w), d1);
-        const float2 r1 = fadd2(d1, make_float2(-S1.x, -S1.y));
+        const float2 r1 = ffma2(S1.z, d1, make_float2(-S1.x, -S1.y));
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
           xr[c] = ffma2(r0.y, hi[j0][c], ffma2(-r0.x, hr[j0][c], xr[c]));
@@ -725,7 +710,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
       xr[c] = fmul2(gsc, xr[c]);
       xi[c] = fmul2(gsc, xi[c]);
     }
-    // gain share Re(s^H H_dl,c x_c) = Re(v^H x_c), v = H_c s = sum_u (s_u ||h_u||) h~_u
+    // gain share Re(s^H H_dl,c x_c) = Re(v^H x_c), v = H_c s = sum_u s_u h_u
     float gq = 0.f;
     if (GAIN) {
       float2 vr[NP], vi[NP];
@@ -734,8 +719,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         const float2 sj = sraw[j];
-        const float nj = ss[j].w;
-        const float cr = sj.x * nj, ci = sj.y * nj;
+        const float cr = sj.x, ci = sj.y;
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
           vr[c] = ffma2(-ci, hi[j][c], ffma2(cr, hr[j][c], vr[c]));

@@ -268,9 +268,8 @@ __global__ void __launch_bounds__(32, MINB)
 }
 
 // ===========================================================================
-// Downlink, fp32, split tile (see dl_reg_f32 for the algorithm and the scalar
-// block layout).  Rows are normalised in place: register columns in registers,
-// shared-memory columns once in shared memory.
+// Downlink, fp32, split tile (see dl_reg_f32 for the algorithm, the
+// unnormalised-row form of the update and the scalar block layout).
 // ===========================================================================
 template <int BC, int U, int G, int JR, int MINB, bool GAIN>
 __global__ void __launch_bounds__(32, MINB)
@@ -367,55 +366,27 @@ __global__ void __launch_bounds__(32, MINB)
     int zero_user = -1;
     float* sf = reinterpret_cast<float*>(ss);
     float* gf = reinterpret_cast<float*>(gp);
+    // unnormalised rows, normalisation in the scalars (see dl_reg_f32):
+    // x -= q_u (h_u^H x - s_u) h_u, q_u = 1/||h_u||^2
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int idx = k * PER + i;
       if (idx < U) {
         if (vv[i] == 0.f && zero_user < 0) zero_user = idx;
-        const float pinv = rsqrtf(vv[i]);
-        sf[idx * 4 + 2] = pinv;  // p_u = 1/||h_u||
-        sf[idx * 4 + 3] = vv[i] * pinv;
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int idx = k * PER + i;
-      if (idx < U) {
+        const float q = __frcp_rn(vv[i]);
         const float2 sv = sraw[idx];
-        const float pj = sf[idx * 4 + 2];
-        sf[idx * 4] = sv.x * pj;  // s~_u = p_u s_u
-        sf[idx * 4 + 1] = sv.y * pj;
+        sf[idx * 4 + 0] = q * sv.x;
+        sf[idx * 4 + 1] = q * sv.y;
+        sf[idx * 4 + 2] = q;
       } else {
         const int gi2 = idx - U, pr = gi2 >> 1;
-        const float val = vv[i] * (sf[(2 * pr + 1) * 4 + 2] * sf[(2 * pr) * 4 + 2]);  // G~ = p_a p_b G
         if (gi2 & 1) {
-          gf[pr * 4 + 1] = val;
-          gf[pr * 4 + 2] = -val;
+          gf[pr * 4 + 1] = vv[i];
+          gf[pr * 4 + 2] = -vv[i];
         } else {
-          gf[pr * 4 + 0] = val;
-          gf[pr * 4 + 3] = val;
+          gf[pr * 4 + 0] = vv[i];
+          gf[pr * 4 + 3] = vv[i];
         }
-      }
-    }
-    // normalise the rows: register columns in registers, the others in place
-#pragma unroll
-    for (int j = 0; j < JR; ++j) {
-      const float pj = sf[j * 4 + 2];
-#pragma unroll
-      for (int c = 0; c < NP; ++c) {
-        hr[j][c] = fmul2(pj, hr[j][c]);
-        hi[j][c] = fmul2(pj, hi[j][c]);
-      }
-    }
-#pragma unroll
-    for (int j = JR; j < U; ++j) {
-      const float pj = sf[j * 4 + 2];
-#pragma unroll
-      for (int c = 0; c < NP; ++c) {
-        float4 v = hs[((j - JR) * NP + c) * G + k];
-        const float2 a = fmul2(pj, make_float2(v.x, v.y)), b = fmul2(pj, make_float2(v.z, v.w));
-        hs[((j - JR) * NP + c) * G + k] = make_float4(a.x, a.y, b.x, b.y);
       }
     }
     __syncwarp();
@@ -457,11 +428,11 @@ __global__ void __launch_bounds__(32, MINB)
             d1 = fadd2(d1, shfl_xor2(d1, o));
           }
         }
-        // resid_u = h~_u^H x - s~_u ; x -= resid_u h~_u   (precode.cpp:89-94)
-        const float2 r0 = fadd2(d0, make_float2(-S0.x, -S0.y));
+        // r_u = q_u (h_u^H x - s_u) ; x -= r_u h_u   (precode.cpp:89-94 on unnormalised rows)
+        const float2 r0 = ffma2(S0.z, d0, make_float2(-S0.x, -S0.y));
         d1 = ffma2(-r0.x, make_float2(GG.x, GG.y), d1);
         d1 = ffma2(-r0.y, make_float2(GG.z, GG.w), d1);
-        const float2 r1 = fadd2(d1, make_float2(-S1.x, -S1.y));
+        const float2 r1 = ffma2(S1.z, d1, make_float2(-S1.x, -S1.y));
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
           xr[c] = ffma2(r0.y, ai[c], ffma2(-r0.x, ar[c], xr[c]));
@@ -483,7 +454,7 @@ __global__ void __launch_bounds__(32, MINB)
       xr[c] = fmul2(gsc, xr[c]);
       xi[c] = fmul2(gsc, xi[c]);
     }
-    // gain share Re(s^H H_dl,c x_c) = Re(v^H x_c), v = H_c s = sum_u (s_u ||h_u||) h~_u
+    // gain share Re(s^H H_dl,c x_c) = Re(v^H x_c), v = H_c s = sum_u s_u h_u
     float gq = 0.f;
     if (GAIN) {
       float2 vr[NP], vi[NP];
@@ -494,8 +465,7 @@ __global__ void __launch_bounds__(32, MINB)
         float2 ar[NP], ai[NP];
         SplitCols<JR, NP, G>::get(j, hr, hi, hs, k, ar, ai);
         const float2 sj = sraw[j];
-        const float nj = ss[j].w;
-        const float cr = sj.x * nj, ci = sj.y * nj;
+        const float cr = sj.x, ci = sj.y;
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
           vr[c] = ffma2(-ci, ai[c], ffma2(cr, ar[c], vr[c]));
