@@ -851,36 +851,19 @@ __global__ void __launch_bounds__(32 * W, MINB)
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int idx = k * PER + i;
-      if (idx < U) {
+      if (idx < U) {  // unnormalised rows (see dl_reg_f32): (q_u s_u) and q_u = 1/||h_u||^2
         if (vv[i] == 0.f && zero_user < 0) zero_user = idx;
-        pn[idx] = rsqrtf(vv[i]);
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int idx = k * PER + i;
-      if (idx < U) {
-        const float2 s = sraw[idx];
-        const float pj = pn[idx];
-        sgf[idx * 4] = s.x * pj;
-        sgf[idx * 4 + 1] = s.y * pj;
+        const float q = __frcp_rn(vv[i]);
+        const float2 sv = sraw[idx];
+        pn[idx] = q;
+        sgf[idx * 4] = q * sv.x;
+        sgf[idx * 4 + 1] = q * sv.y;
       } else {
         const int gi = idx - U;
         const int a = (gi >> 1) * 2 + 1;
-        // sg[2i+1].zw = (Re G~, Im G~), sg[2i].zw = (-Im G~, Re G~)
-        const float gv = vv[i] * (pn[a] * pn[a - 1]);
-        sgf[a * 4 + 2 + (gi & 1)] = gv;
-        sgf[(a - 1) * 4 + 3 - (gi & 1)] = (gi & 1) ? -gv : gv;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const __half2 p2 = __float2half2_rn(pn[j]);
-#pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        hre[j][q] = __hmul2(p2, hre[j][q]);
-        him[j][q] = __hmul2(p2, him[j][q]);
+        // sg[2i+1].zw = (Re G, Im G), sg[2i].zw = (-Im G, Re G), raw pair Gram
+        sgf[a * 4 + 2 + (gi & 1)] = vv[i];
+        sgf[(a - 1) * 4 + 3 - (gi & 1)] = (gi & 1) ? -vv[i] : vv[i];
       }
     }
     __syncwarp();
@@ -911,16 +894,17 @@ __global__ void __launch_bounds__(32 * W, MINB)
         }
         const float2 f0 = __half22float2(d0);
         float2 f1 = __half22float2(d1);
-        // resid_u = h~_u^H x - s~_u (precode.cpp:89-94) in packed fp32x2, pair-Gram correction
-        const float2 q0 = fadd2(f0, make_float2(-s0.x, -s0.y));
+        // r_u = q_u (h_u^H x - s_u) (precode.cpp:89-94 on raw rows) in packed fp32x2, pair-Gram correction
+        const float2 qq = *reinterpret_cast<const float2*>(pn + j0);
+        const float2 q0 = ffma2(qq.x, f0, make_float2(-s0.x, -s0.y));
         f1 = ffma2(-q0.x, make_float2(s1.z, s1.w), f1);
         f1 = ffma2(-q0.y, make_float2(s0.z, s0.w), f1);
-        const float2 q1 = fadd2(f1, make_float2(-s1.x, -s1.y));
+        const float2 q1 = ffma2(qq.y, f1, make_float2(-s1.x, -s1.y));
         const __half2 h0 = __float22half2_rn(q0), h1 = __float22half2_rn(q1);
         const __half2 r0 = __low2half2(h0), i0 = __high2half2(h0);
         const __half2 r1 = __low2half2(h1), i1 = __high2half2(h1);
 #pragma unroll
-        for (int q = 0; q < NP; ++q) {  // x -= resid_u h~_u
+        for (int q = 0; q < NP; ++q) {  // x -= r_u h_u
           xre[q] = __hfma2(__hneg2(r0), hre[j0][q], __hfma2(i0, him[j0][q], xre[q]));
           xim[q] = __hfma2(__hneg2(r0), him[j0][q], __hfma2(__hneg2(i0), hre[j0][q], xim[q]));
           xre[q] = __hfma2(__hneg2(r1), hre[j1][q], __hfma2(i1, him[j1][q], xre[q]));
