@@ -3,7 +3,7 @@
 // (B_c=32, U=16, K=3, 134,400 problems) on identical random inputs and
 // reports the max per-problem relative difference to it.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -lineinfo \
-//        -I paper_1902_08653_b200/csrc -I scripts/lab scripts/lab/lab_split.cu -o lab/lab_split
+//        -I paper_1902_08653_b200/csrc scripts/lab/lab_split.cu -o lab/lab_split
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
