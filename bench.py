@@ -297,6 +297,40 @@ def run_ours(args):
                        "value": round(S_total * U * BITS / (ms2 * 1e-3) / 1e9, 4), "unit": "Gbps"}
         except Exception as e:  # reported, never silently substituted for the main line
             compare = {"mode": other, "error": str(e)[:200]}
+    # configs[2] across the GPUs: the distributed downlink step (symbol broadcast
+    # from rank 0, local precoding, effective-gain exchange), same protocol
+    downlink = None
+    if world > 1 and fmt == "fp32":
+        try:
+            g_s = torch.Generator(device=dev)
+            g_s.manual_seed(99)
+            lv = torch.tensor([-3.0, -1.0, 1.0, 3.0], device=dev) / math.sqrt(10.0)
+            idx = torch.randint(0, 4, (S_total, U, 2), device=dev, generator=g_s)
+            s_sym = torch.complex(lv[idx[..., 0]], lv[idx[..., 1]]).contiguous()
+            rho = math.sqrt(U)
+
+            def dl_step():
+                dcd.downlink(H, dcd.broadcast_symbols(s_sym), rho=rho, K=K_SWEEPS)
+
+            for _ in range(args.warmup):
+                dl_step()
+            barrier()
+            d0, d1 = _ev(), _ev()
+            barrier()
+            d0.record(stream)
+            for _ in range(args.steps):
+                dl_step()
+            d1.record(stream)
+            barrier()
+            dms = d0.elapsed_time(d1) / args.steps
+            tt = torch.tensor([dms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dms = float(tt.item())
+            downlink = {"workload": "downlink CD ZF precoding + power split + effective gain (configs[2])",
+                        "mode": args.mode, "ms_per_step": round(dms, 5),
+                        "value": round(S_total * U * BITS / (dms * 1e-3) / 1e9, 4), "unit": "Gbps"}
+        except Exception as e:  # reported, never silently substituted
+            downlink = {"mode": args.mode, "error": str(e)[:200]}
     interconnect = {
         "payload_bytes_per_step_per_gpu": int(pay), "bus_bytes_per_step_per_gpu": int(bus),
         "messages_per_step_per_gpu": int(msgs),
@@ -438,6 +472,8 @@ def run_ours(args):
     }
     if compare:
         line["exchange_comparison"] = compare
+    if downlink:
+        line["downlink_distributed"] = downlink
     if extra:
         line["extra"] = extra
     if world == 1 and not args.no_cpu:
