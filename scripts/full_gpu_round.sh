@@ -7,15 +7,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu --fast > gpurun_out/b_ncu.log 2>&1
-mkdir -p /tmp/reps
-args=""
-for k in "ul fp32 4480" "dl fp32 4480" "ul fp16 2240" "dl fp16 2240" "pev fp32 4096"; do
-  set -- $k
-  timeout 300 ncu --set full --clock-control none --import-source on -k regex:"reg_f|gram_chol" -s 2 -c 1 \
-    -o /tmp/reps/full_$1_$2 python scripts/prof_kernel.py $1 $2 4 > /dev/null 2>&1
-  args="$args ${1}_${2}_32_16=/tmp/reps/full_$1_$2.ncu-rep:134400:$3"
-done
-python scripts/ncu_summary.py gpurun_out/ncu_summary.json $args > /dev/null 2>&1
+bash scripts/ncu_captures.sh
 for f in /tmp/reps/*.ncu-rep; do
   ncu -i $f --page source --csv --print-source sass > /tmp/reps/$(basename $f .ncu-rep).src.csv 2>/dev/null
   python scripts/stall_summary.py /tmp/reps/$(basename $f .ncu-rep).src.csv > gpurun_out/stalls_$(basename $f .ncu-rep).txt 2>&1

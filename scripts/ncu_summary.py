@@ -74,7 +74,11 @@ def main():
         name, spec = arg.split("=", 1)
         parts = spec.split(":")
         rep = parts[0]
-        launches = summarise(rep)
+        try:
+            launches = summarise(rep)
+        except Exception as e:  # a capture that did not happen: say so, keep the others
+            summary[name] = {"error": str(e)[:200]}
+            continue
         d = launches[0]
         if len(parts) >= 3:
             problems, per = int(parts[1]), float(parts[2])
