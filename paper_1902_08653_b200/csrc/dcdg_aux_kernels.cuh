@@ -535,6 +535,23 @@ __global__ void __launch_bounds__(128) pev16_pair_kernel(const T* __restrict__ H
         hs[j * (PR + 1) + 2 * rr] = make_float2(v.x, v.y);
         hs[j * (PR + 1) + 2 * rr + 1] = make_float2(v.z, v.w);
       }
+    } else if constexpr (sizeof(T) == 4 && BT % 4 == 0) {
+      // fp16 row-pair planar tile: one 16-B load = rows 4q..4q+3 of a column
+      // as {re0, re1, im0, im1, re2, re3, im2, im3}
+      const uint4* t4 = reinterpret_cast<const uint4*>(h);
+#pragma unroll
+      for (int i = 0; i < BT * N / 128; ++i) {
+        const int idx = lane + 32 * i;
+        const int j = idx / (BT / 4), q = idx - j * (BT / 4);
+        const uint4 v = __ldg(t4 + idx);
+        const float2 re01 = __half22float2(u32_as_h2(v.x)), im01 = __half22float2(u32_as_h2(v.y));
+        const float2 re23 = __half22float2(u32_as_h2(v.z)), im23 = __half22float2(u32_as_h2(v.w));
+        float2* dst = hs + j * (PR + 1) + 4 * q;
+        dst[0] = make_float2(re01.x, im01.x);
+        dst[1] = make_float2(re01.y, im01.y);
+        dst[2] = make_float2(re23.x, im23.x);
+        dst[3] = make_float2(re23.y, im23.y);
+      }
     } else {
       for (int idx = lane; idx < BT * N; idx += 32) {
         const int j = idx / BT, b = idx - j * BT;
@@ -590,58 +607,64 @@ __global__ void __launch_bounds__(128) pev16_pair_kernel(const T* __restrict__ H
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) maxdiag = fmaxf(maxdiag, __shfl_xor_sync(0xffffffffu, maxdiag, o));
   const float floor_ = 1e-14f * maxdiag;  // numerics.cpp:38-41,55-56
-  float2 a[N], l[N];
+  // complex products in packed fp32x2: u conj(b) = b.x (u.x, u.y) + b.y (u.y, -u.x)
+  // and L x = L.x (x.x, x.y) + L.y (-x.y, x.x), with the swizzled copies kept
+  // next to each register value (lw, xw) and the shared-memory operand broadcast
+  float2 a[N], l[N], lw[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     a[k] = (k <= i) ? Ah[k * N + i] : make_float2(0.f, 0.f);
-    l[k] = make_float2(0.f, 0.f);
+    l[k] = lw[k] = make_float2(0.f, 0.f);
   }
   bool singular = false;
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     if (i == j) {  // d_j = A_jj - sum_k |L_jk|^2 ; L_jj = sqrt(d_j)   (numerics.cpp:47-52)
-      float d = a[j].x;
+      float2 e = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int k = 0; k < j; ++k) d -= l[k].x * l[k].x + l[k].y * l[k].y;
+      for (int k = 0; k < j; ++k) e = ffma2(l[k], l[k], e);
+      const float d = a[j].x - hsum(e);
       if (!(d > floor_)) singular = true;
       l[j] = make_float2(__fsqrt_rn(fmaxf(d, 1e-30f)), 0.f);
+      lw[j] = make_float2(0.f, -l[j].x);
 #pragma unroll
       for (int k = 0; k <= j; ++k) Lh[j * N + k] = l[k];
     }
     __syncwarp();
     if (i > j) {  // L_ij = (A_ij - sum_{k<j} L_ik conj(L_jk)) / L_jj   (numerics.cpp:53-56)
-      float sr = a[j].x, si = a[j].y;
+      float2 sv = a[j];
 #pragma unroll
       for (int k = 0; k < j; ++k) {
-        const float2 b = Lh[j * N + k];
-        sr -= l[k].x * b.x + l[k].y * b.y;
-        si -= l[k].y * b.x - l[k].x * b.y;
+        const float2 bk = Lh[j * N + k];
+        sv = ffma2(-bk.x, l[k], sv);
+        sv = ffma2(-bk.y, lw[k], sv);
       }
       const float inv = __frcp_rn(Lh[j * N + j].x);
-      l[j] = make_float2(sr * inv, si * inv);
+      l[j] = fmul2(inv, sv);
+      lw[j] = make_float2(l[j].y, -l[j].x);
     }
   }
   __syncwarp();
   // X = L^-1: lane (h, c) holds column c; X_ic = -(sum_{k=c}^{i-1} L_ik X_kc) / L_ii
   const int c = i;
   float tr = 0.f;
-  float2 x[N];
+  float2 x[N], xw[N];
 #pragma unroll
   for (int r = 0; r < N; ++r) {
     const float linv = __frcp_rn(Lh[r * N + r].x);
-    float sr = 0.f, si = 0.f;
+    float2 sv = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int k = 0; k < r; ++k) {
+    for (int k = 0; k < r; ++k) {  // x[k] is zero above the diagonal (k < c)
       const float2 lk = Lh[r * N + k];
-      const float2 xk = x[k];  // zero above the diagonal (k < c)
-      sr += lk.x * xk.x - lk.y * xk.y;
-      si += lk.x * xk.y + lk.y * xk.x;
+      sv = ffma2(lk.x, x[k], sv);
+      sv = ffma2(lk.y, xw[k], sv);
     }
     float2 v;
     if (c == r) v = make_float2(linv, 0.f);
-    else if (c < r) v = make_float2(-sr * linv, -si * linv);
+    else if (c < r) v = fmul2(-linv, sv);
     else v = make_float2(0.f, 0.f);
     x[r] = v;
+    xw[r] = make_float2(-v.y, v.x);
     tr = fmaf(v.x, v.x, fmaf(v.y, v.y, tr));
   }
 #pragma unroll
