@@ -152,14 +152,15 @@ def _rank_main(rank, world, port_, fmt, fusion, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fmt,fusion", [("fp32", "uniform"), ("fp16", "uniform"), ("fp32", "optimal")])
-def test_two_ranks_on_one_gpu_bitwise(engine, tmp_path, fmt, fusion):
-    """world 2 (two processes sharing cuda:0, windows mapped by CUDA IPC):
+@pytest.mark.parametrize("world,fmt,fusion", [(2, "fp32", "uniform"), (2, "fp16", "uniform"), (2, "fp32", "optimal"),
+                                              (4, "fp32", "uniform"), (4, "fp32", "optimal")])
+def test_ranks_on_one_gpu_bitwise(engine, tmp_path, world, fmt, fusion):
+    """world 2 / 4 (processes sharing cuda:0, windows mapped by CUDA IPC):
     each rank's owned subcarriers equal the single-process fusion bitwise."""
     import torch.multiprocessing as mp
 
     from paper_1902_08653_b200 import to_fp16_pairs
-    mp.spawn(_rank_main, args=(2, _free_port(), fmt, fusion, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_rank_main, args=(world, _free_port(), fmt, fusion, str(tmp_path)), nprocs=world, join=True)
     C, BC, U, S = 8, 32, 16, 64
     g = torch.Generator().manual_seed(5)
     H = torch.randn((S, C, U, BC), dtype=torch.complex64, generator=g).cuda()
@@ -167,14 +168,16 @@ def test_two_ranks_on_one_gpu_bitwise(engine, tmp_path, fmt, fusion):
     if fmt == "fp16":
         H, y = to_fp16_pairs(H), to_fp16_pairs(y)
     want = _single(engine, H, y, fusion=fusion, n0=1.6).cpu()
-    for r in range(2):
+    cl = C // world
+    for r in range(world):
         got = torch.from_numpy(np.load(tmp_path / f"r{r}.npy"))
         for step in range(got.shape[0]):
-            assert torch.equal(torch.view_as_real(got[step]), torch.view_as_real(want[r * S // 2:(r + 1) * S // 2]))
-        # bus bytes: half of this rank's x_local (C_local = 4 clusters x U x esz per subcarrier) crosses
+            assert torch.equal(torch.view_as_real(got[step]),
+                               torch.view_as_real(want[r * S // world:(r + 1) * S // world]))
+        # bus bytes: (W-1)/W of this rank's x_local (C_local clusters x U x esz per subcarrier) crosses
         esz = 8 if fmt == "fp32" else 4
-        per = S * 4 * U * esz + (S * 4 * 4 if fusion == "optimal" else 0)
-        assert int(np.load(tmp_path / f"t{r}.npy")[0]) == 3 * per // 2
+        per = S * cl * U * esz + (S * cl * 4 if fusion == "optimal" else 0)
+        assert int(np.load(tmp_path / f"t{r}.npy")[0]) == 3 * round(per * (world - 1) / world)
     if fusion == "uniform":
         g = torch.Generator().manual_seed(5)
         torch.randn((S, C, U, BC), dtype=torch.complex64, generator=g)
@@ -183,9 +186,9 @@ def test_two_ranks_on_one_gpu_bitwise(engine, tmp_path, fmt, fusion):
         syd = sy.cuda() if fmt == "fp32" else torch.view_as_real(sy).to(torch.float16).cuda().contiguous()
         want_dl = engine.dl_precode(H, syd, rho=4.0, K=3, want_gain=True)
         engine.sync()
-        for r in range(2):
+        for r in range(world):
             for xd, gain in torch.load(tmp_path / f"d{r}.pt"):
-                wx = want_dl.x[:, 4 * r:4 * (r + 1)].cpu()
+                wx = want_dl.x[:, cl * r:cl * (r + 1)].cpu()
                 assert torch.equal(torch.view_as_real(xd) if xd.is_complex() else xd,
                                    torch.view_as_real(wx) if wx.is_complex() else wx)
                 assert torch.equal(gain, want_dl.gain.cpu())
