@@ -192,4 +192,33 @@ class DeviceBatch {
   Engine& eng_;
 };
 
+/// This rank's window of the fused cross-GPU exchange (dcdg_xwin_*, one
+/// process per GPU): DeviceBatch::detect / precode with the fusion stores and
+/// the symbol broadcast done by the kernels in peer memory.
+/// Every rank sends handle() to the others over the host's own transport and
+/// opens theirs; then all ranks issue the same sequence of calls.
+class ExchangeWindow {
+ public:
+  ExchangeWindow(Engine& eng, int world, int rank, int S, int C_total, int U, int fmt);
+  ~ExchangeWindow();
+  ExchangeWindow(const ExchangeWindow&) = delete;
+  ExchangeWindow& operator=(const ExchangeWindow&) = delete;
+
+  std::vector<std::uint8_t> handle() const;
+  void open(int peer, const std::vector<std::uint8_t>& handle);
+
+  /// Uplink of the batch's C clusters [c0, c0 + C): batch.xhat receives the
+  /// fused estimates of the subcarriers this rank owns, [S/world][U].
+  void detect(DeviceBatch& batch, int c0, int C_total, int K, double n0, double ex, FusionMode fusion);
+  /// Downlink: the root's batch.s is pushed to every rank; batch.x_dl gets this
+  /// rank's beamformers and batch.gain the effective gain (every rank).
+  void precode(DeviceBatch& batch, int root, int c0, int C_total, int K, double rho);
+
+  int world, rank;
+
+ private:
+  Engine& eng_;
+  dcdg_xwin* w_ = nullptr;
+};
+
 }  // namespace dcd::gpu

@@ -4,6 +4,7 @@
 // batched device call per decentralized operation.  Host code here only moves
 // and re-lays-out data (fp64 <-> fp32/fp16 packing, H_dl <-> uplink tiles);
 // all arithmetic of the path runs in the CUDA kernels.
+#include <algorithm>
 #include "dcd_gpu.hpp"
 
 #include <cuda_fp16.h>
@@ -543,6 +544,45 @@ void DeviceBatch::download_gain(float* host) const {
 void DeviceBatch::download_sigma2(float* host) const {
   d2h(host, sigma2, static_cast<std::size_t>(S) * C * sizeof(float), eng_.stream());
   eng_.sync();
+}
+
+// ---------------------------------------------------------------------------
+// ExchangeWindow
+// ---------------------------------------------------------------------------
+ExchangeWindow::ExchangeWindow(Engine& eng, int world_, int rank_, int S, int C_total, int U, int fmt)
+    : world(world_), rank(rank_), eng_(eng) {
+  if (world_ <= 0 || S % world_) throw std::invalid_argument("dcd::gpu::ExchangeWindow: S must divide over the ranks");
+  const std::int64_t es = static_cast<std::int64_t>(esize(fmt)), s_own = S / world_;
+  const std::int64_t ul = ((s_own * C_total * U * es + 255) / 256) * 256 + s_own * C_total * 4;
+  const std::int64_t dl = ((static_cast<std::int64_t>(S) * U * es + 255) / 256) * 256 + std::int64_t{S} * C_total * 4;
+  Engine::check(dcdg_xwin_create(eng.ctx(), world_, rank_, std::max(ul, dl), &w_));
+}
+
+ExchangeWindow::~ExchangeWindow() {
+  if (w_) dcdg_xwin_destroy(w_);
+}
+
+std::vector<std::uint8_t> ExchangeWindow::handle() const {
+  std::vector<std::uint8_t> h(DCDG_XWIN_HANDLE_BYTES);
+  Engine::check(dcdg_xwin_handle(w_, h.data()));
+  return h;
+}
+
+void ExchangeWindow::open(int peer, const std::vector<std::uint8_t>& h) {
+  if (h.size() != DCDG_XWIN_HANDLE_BYTES)
+    throw std::invalid_argument("dcd::gpu::ExchangeWindow: handle has the wrong size");
+  Engine::check(dcdg_xwin_open(w_, peer, h.data()));
+}
+
+void ExchangeWindow::detect(DeviceBatch& b, int c0, int C_total, int K, double n0, double ex, FusionMode fusion) {
+  Engine::check(dcdg_ul_detect_xchg(eng_.ctx(), w_, b.H, b.y, b.S, b.C, c0, C_total, b.Bc, b.U, K, n0, ex, b.fmt,
+                                    fusion == FusionMode::optimal ? DCDG_FUSION_OPTIMAL : DCDG_FUSION_UNIFORM, b.xhat,
+                                    eng_.stream()));
+}
+
+void ExchangeWindow::precode(DeviceBatch& b, int root, int c0, int C_total, int K, double rho) {
+  Engine::check(dcdg_dl_precode_xchg(eng_.ctx(), w_, root, b.H, b.s, b.S, b.C, c0, C_total, b.Bc, b.U, K, rho, b.fmt,
+                                     b.x_dl, b.gain, eng_.stream()));
 }
 
 }  // namespace dcd::gpu

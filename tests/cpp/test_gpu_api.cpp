@@ -445,6 +445,39 @@ TEST_CASE("batched device API round trip", t_batch) {
   CHECK(rel_dist(got, want) <= kTol);
 }
 
+TEST_CASE("exchange window (world 1) reproduces the batched detector and precoder bitwise", t_xwin) {
+  dcd::gpu::Engine eng(0);
+  const int S = 4, C = 2, Bc = 32, U = 8;
+  dcd::gpu::DeviceBatch plain(eng, S, C, Bc, U, DCDG_FP32), via(eng, S, C, Bc, U, DCDG_FP32);
+  std::vector<float> h(2 * S * C * U * Bc), y(2 * S * C * Bc), sy(2 * S * U);
+  for (auto& v : h) v = static_cast<float>(randc().real());
+  for (auto& v : y) v = static_cast<float>(randc().real());
+  for (auto& v : sy) v = static_cast<float>(randc().real());
+  for (auto* b : {&plain, &via}) {
+    b->upload_h(h.data(), h.size() * 4);
+    b->upload_y(y.data(), y.size() * 4);
+    b->upload_s(sy.data(), sy.size() * 4);
+  }
+  plain.detect(C, 3, 0.2, 1.0, FusionMode::uniform);
+  plain.precode(C, 3, 2.0, true);
+  dcd::gpu::ExchangeWindow w(eng, 1, 0, S, C, U, DCDG_FP32);
+  w.open(0, w.handle());
+  w.detect(via, 0, C, 3, 0.2, 1.0, FusionMode::uniform);
+  w.precode(via, 0, 0, C, 3, 2.0);
+  std::vector<float> a(2 * S * U), b(2 * S * U), xa(2 * S * C * Bc), xb(2 * S * C * Bc), ga(S), gb(S);
+  plain.download_xhat(a.data());
+  via.download_xhat(b.data());
+  plain.download_x_dl(xa.data());
+  via.download_x_dl(xb.data());
+  plain.download_gain(ga.data());
+  via.download_gain(gb.data());
+  CHECK(std::memcmp(a.data(), b.data(), a.size() * 4) == 0);
+  CHECK(std::memcmp(xa.data(), xb.data(), xa.size() * 4) == 0);
+  CHECK(std::memcmp(ga.data(), gb.data(), ga.size() * 4) == 0);
+  CHECK(throws_with<std::invalid_argument>([&] { dcd::gpu::ExchangeWindow bad(eng, 3, 0, S, C, U, DCDG_FP32); },
+                                           "S must divide over the ranks"));
+}
+
 int main() {
   for (auto& [name, fn] : registry()) {
     g_case = name;
