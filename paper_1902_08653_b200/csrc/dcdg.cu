@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -88,6 +89,29 @@ int ensure_scratch(dcdg_ctx* ctx, size_t bytes) {
 }
 
 inline size_t esize(int fmt) { return fmt == DCDG_FP16 ? 4 : 8; }
+
+#ifndef DCDG_PDL
+#define DCDG_PDL 1
+#endif
+// Launch a stage kernel that consumes its stream predecessor's output (fusion
+// after detection, gain after precoding) as a programmatic dependent: it is
+// scheduled while the CD kernel's last CTAs drain and waits in
+// griddep_wait(), which hides the launch gap between the two.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_dependent(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                             Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = DCDG_PDL;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // launchers for the register-resident kernels
@@ -375,16 +399,16 @@ int launch_fuse(dcdg_ctx* ctx, const void* xl, const float* s2, int S, int C, in
                 bool optimal, float* xhat, float* wsum, cudaStream_t st) {
   const long long n = static_cast<long long>(S) * U;
   const int threads = 256;
-  const long long blocks = (n + threads - 1) / threads;
+  const unsigned blocks = static_cast<unsigned>((n + threads - 1) / threads);
   if (fmt == DCDG_FP16)
-    dcdg::fuse_kernel<__half2><<<blocks, threads, 0, st>>>(static_cast<const __half2*>(xl), s2, S, C, C_total, U,
-                                                            optimal, reinterpret_cast<float2*>(xhat), wsum,
-                                                            ctx->d_status);
+    CUDA_TRY(launch_dependent(dcdg::fuse_kernel<__half2>, blocks, threads, 0, st, static_cast<const __half2*>(xl), s2, S,
+                              C, C_total, U, optimal, reinterpret_cast<float2*>(xhat), wsum, ctx->d_status),
+             "fuse launch");
   else
-    dcdg::fuse_kernel<float2><<<blocks, threads, 0, st>>>(static_cast<const float2*>(xl), s2, S, C, C_total, U, optimal,
-                                                           reinterpret_cast<float2*>(xhat), wsum, ctx->d_status);
+    CUDA_TRY(launch_dependent(dcdg::fuse_kernel<float2>, blocks, threads, 0, st, static_cast<const float2*>(xl), s2, S,
+                              C, C_total, U, optimal, reinterpret_cast<float2*>(xhat), wsum, ctx->d_status),
+             "fuse launch");
   ++ctx->launches;
-  CUDA_TRY(cudaGetLastError(), "fuse launch");
   return DCDG_OK;
 }
 
@@ -761,16 +785,23 @@ int dcdg_gain_reduce(dcdg_ctx* ctx, const float* gain_part, const void* s, int S
   if (int rc = check_fmt(fmt)) return rc;
   if (S <= 0) return DCDG_OK;
   CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
-  const int threads = 256;
-  const int blocks = (S + threads - 1) / threads;
-  if (fmt == DCDG_FP16)
-    dcdg::gain_reduce_kernel<__half2><<<blocks, threads, 0, as_stream(stream)>>>(
-        gain_part, static_cast<const __half2*>(s), S, C, U, gain);
-  else
-    dcdg::gain_reduce_kernel<float2><<<blocks, threads, 0, as_stream(stream)>>>(
-        gain_part, static_cast<const float2*>(s), S, C, U, gain);
+  const unsigned blocks = static_cast<unsigned>((S + dcdg::kGainSubs - 1) / dcdg::kGainSubs);
+  const size_t smem = dcdg::gain_reduce_smem(U, C);
+  if (smem > 227 * 1024) return fail(DCDG_EINVAL, "dcdg_gain_reduce: U or C too large");
+  if (fmt == DCDG_FP16) {
+    auto k = dcdg::gain_reduce_kernel<__half2>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    CUDA_TRY(launch_dependent(k, blocks, 128, smem, as_stream(stream), gain_part, static_cast<const __half2*>(s), S, C,
+                              U, gain),
+             "gain_reduce launch");
+  } else {
+    auto k = dcdg::gain_reduce_kernel<float2>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    CUDA_TRY(launch_dependent(k, blocks, 128, smem, as_stream(stream), gain_part, static_cast<const float2*>(s), S, C,
+                              U, gain),
+             "gain_reduce launch");
+  }
   ++ctx->launches;
-  CUDA_TRY(cudaGetLastError(), "gain_reduce launch");
   return DCDG_OK;
 }
 

@@ -690,33 +690,61 @@ template <typename T>
 __global__ void fuse_kernel(const T* __restrict__ XL, const float* __restrict__ sigma2, int S, int C, int C_total, int U,
                             bool optimal, float2* __restrict__ xhat, float* __restrict__ wsum,
                             unsigned long long* __restrict__ status) {
+  griddep_wait();  // launched as a programmatic dependent of the CD kernel
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= static_cast<long long>(S) * U) return;
   const long long s = idx / U;
   const int u = static_cast<int>(idx - s * U);
   const bool full = C == C_total;
+  const T* xs = XL + static_cast<size_t>(s) * C * U + u;
+  // the estimates of a chunk of clusters are loaded together (independent
+  // loads in flight), then accumulated in ascending cluster order
+  constexpr int CH = 8;
   float2 acc = make_float2(0.f, 0.f);
   if (!optimal) {
     const float w = 1.f / static_cast<float>(C_total);
-    for (int c = 0; c < C; ++c) {
-      const float2 v = ldc(XL, (static_cast<size_t>(s) * C + c) * U + u);
-      acc.x = fmaf(w, v.x, acc.x);
-      acc.y = fmaf(w, v.y, acc.y);
+    for (int c0 = 0; c0 < C; c0 += CH) {
+      float2 v[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) v[i] = c0 + i < C ? ldc(xs, static_cast<size_t>(c0 + i) * U) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < CH; ++i)
+        if (c0 + i < C) {
+          acc.x = fmaf(w, v[i].x, acc.x);
+          acc.y = fmaf(w, v[i].y, acc.y);
+        }
     }
   } else {
+    const float* sg = sigma2 + s * C;
     float total = 0.f;
     bool bad = false;
-    for (int c = 0; c < C; ++c) {
-      const float v = sigma2[s * C + c];
-      if (!(v > 0.f) || !isfinite(v)) bad = true;
-      total += 1.f / v;
+    for (int c0 = 0; c0 < C; c0 += CH) {
+      float v[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) v[i] = c0 + i < C ? __ldg(sg + c0 + i) : 1.f;
+#pragma unroll
+      for (int i = 0; i < CH; ++i)
+        if (c0 + i < C) {
+          if (!(v[i] > 0.f) || !isfinite(v[i])) bad = true;
+          total += 1.f / v[i];
+        }
     }
     if (bad && u == 0) record_status(status, s * C, ST_BAD_VARIANCE, 0);
-    for (int c = 0; c < C; ++c) {
-      const float w = full ? (1.f / sigma2[s * C + c]) / total : 1.f / sigma2[s * C + c];
-      const float2 v = ldc(XL, (static_cast<size_t>(s) * C + c) * U + u);
-      acc.x = fmaf(w, v.x, acc.x);
-      acc.y = fmaf(w, v.y, acc.y);
+    for (int c0 = 0; c0 < C; c0 += CH) {
+      float2 v[CH];
+      float q[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        v[i] = c0 + i < C ? ldc(xs, static_cast<size_t>(c0 + i) * U) : make_float2(0.f, 0.f);
+        q[i] = c0 + i < C ? __ldg(sg + c0 + i) : 1.f;
+      }
+#pragma unroll
+      for (int i = 0; i < CH; ++i)
+        if (c0 + i < C) {
+          const float w = full ? (1.f / q[i]) / total : 1.f / q[i];
+          acc.x = fmaf(w, v[i].x, acc.x);
+          acc.y = fmaf(w, v[i].y, acc.y);
+        }
     }
     if (!full && wsum && u == 0) wsum[s] = total;
   }
@@ -870,19 +898,39 @@ __global__ void fuse_finalize_kernel(float2* __restrict__ xhat, const float* __r
   xhat[idx] = make_float2(xhat[idx].x / w, xhat[idx].y / w);
 }
 
+// Effective gain per subcarrier (precode.cpp:123-131): a block stages the
+// symbols and gain shares of kGainSubs subcarriers with coalesced loads (rows
+// padded by one complex against bank conflicts), then one thread per
+// subcarrier runs the ascending-order sums.
+constexpr int kGainSubs = 32;
+inline size_t gain_reduce_smem(int U, int C) {
+  return static_cast<size_t>(kGainSubs) * (U + 1) * sizeof(float2) + static_cast<size_t>(kGainSubs) * C * sizeof(float);
+}
+
 template <typename T>
 __global__ void gain_reduce_kernel(const float* __restrict__ part, const T* __restrict__ Sy, int S, int C, int U,
                                    float* __restrict__ gain) {
-  const long long s = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s >= S) return;
+  extern __shared__ float2 gsh[];  // [kGainSubs][U + 1] symbols, then [kGainSubs][C] shares
+  float* psh = reinterpret_cast<float*>(gsh + kGainSubs * (U + 1));
+  griddep_wait();  // launched as a programmatic dependent of the CD kernel
+  const long long s0 = static_cast<long long>(blockIdx.x) * kGainSubs;
+  const int ns = S - s0 < kGainSubs ? static_cast<int>(S - s0) : kGainSubs;
+  for (int i = threadIdx.x; i < ns * U; i += blockDim.x) {
+    const int r = i / U, u = i - r * U;
+    gsh[r * (U + 1) + u] = ldc(Sy, static_cast<size_t>(s0) * U + i);
+  }
+  for (int i = threadIdx.x; i < ns * C; i += blockDim.x) psh[i] = __ldg(part + s0 * C + i);
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t >= ns) return;
   float se = 0.f;
   for (int u = 0; u < U; ++u) {
-    const float2 v = ldc(Sy, static_cast<size_t>(s) * U + u);
+    const float2 v = gsh[t * (U + 1) + u];
     se = fmaf(v.y, v.y, fmaf(v.x, v.x, se));
   }
   float num = 0.f;
-  for (int c = 0; c < C; ++c) num += part[s * C + c];
-  gain[s] = se > 0.f ? num / se : 0.f;
+  for (int c = 0; c < C; ++c) num += psh[t * C + c];
+  gain[s0 + t] = se > 0.f ? num / se : 0.f;
 }
 
 template <typename T>

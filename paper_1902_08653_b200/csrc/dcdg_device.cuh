@@ -146,6 +146,12 @@ __device__ __forceinline__ float2 ldv(const __half2* v, int i) {
   return make_float2(__half2float(h[0]), __half2float(h[2]));
 }
 
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization starts while its
+// predecessor drains and waits here until the predecessor's results are
+// visible; without the attribute this is a no-op.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ __half2 u32_as_h2(uint32_t u) {
   __half2 h;
   memcpy(&h, &u, 4);

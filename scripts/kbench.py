@@ -1,5 +1,6 @@
 """Quick kernel timing at the north-star shape: achieved algorithmic GB/s of the
-UL/DL CD kernels (fp32, fp16).  usage: python scripts/kbench.py [S] [reps]"""
+UL/DL CD kernels (fp32, fp16), alone and with the cross-cluster stage
+(uniform fusion / effective gain).  usage: python scripts/kbench.py [S] [reps]"""
 import json
 import math
 import os
@@ -21,12 +22,16 @@ for fmt in ("fp32", "fp16"):
     Hh, yh, xh = (H, y, x) if fmt == "fp32" else (to_fp16_pairs(H), to_fp16_pairs(y), to_fp16(x))
     esz = 8 if fmt == "fp32" else 4
     nbytes = S * 8 * (32 * 16 + 32 + 16) * esz
-    for d in ("ul", "dl"):
+    for d in ("ul", "dl", "ul+fusion", "dl+gain"):
         def run():
             if d == "ul":
                 eng.ul_detect(Hh, yh, n0=n0, K=3, want_xhat=False)
-            else:
+            elif d == "dl":
                 eng.dl_precode(Hh, xh, rho=4.0, K=3, want_gain=False)
+            elif d == "ul+fusion":
+                eng.ul_detect(Hh, yh, n0=n0, K=3)
+            else:
+                eng.dl_precode(Hh, xh, rho=4.0, K=3)
         for _ in range(3):
             run()
         torch.cuda.synchronize()
