@@ -151,10 +151,13 @@ def secondary_lines(eng, dev, S, reps, hbm):
     st = torch.cuda.current_stream(dev)
     P = S * C
     rho = math.sqrt(U)
-    for fmt in ("fp32", "fp16"):
+    # fp16: the default uplink kernel is the tensor-core Gram kernel; "fp16sweep"
+    # is the half2 residual-sweep kernel (the paper's half-precision arithmetic)
+    for fmt in ("fp32", "fp16", "fp16sweep"):
         esz = 8 if fmt == "fp32" else 4
         Hh, yh, xh = (H, y, x) if fmt == "fp32" else (to_fp16_pairs(H), to_fp16_pairs(y), to_fp16(x))
-        for d in ("ul", "dl"):
+        eng.set_fp16_algorithm("sweep" if fmt == "fp16sweep" else "gram")
+        for d in (("ul",) if fmt == "fp16sweep" else ("ul", "dl")):
             if d == "ul":
                 fn = lambda: eng.ul_detect(Hh, yh, n0=n0, K=K_SWEEPS, fusion="uniform")  # noqa: E731
                 kfn = lambda: eng.ul_detect(Hh, yh, n0=n0, K=K_SWEEPS, want_xhat=False)  # noqa: E731
@@ -167,9 +170,12 @@ def secondary_lines(eng, dev, S, reps, hbm):
             ms = _time_stream(fn, st, reps)
             kms = _time_stream(kfn, st, reps)
             ach = P * alg_bytes_per_problem(BC, U, esz) / (kms * 1e-3) / 1e9
+            fcode = 0 if fmt == "fp32" else 1
             out[f"{d}_{fmt}"] = {"value": round(S * U * BITS / (ms * 1e-3) / 1e9, 4), "unit": "Gbps",
                                  "ms_per_batch": round(ms, 5), "kernel_ms": round(kms, 5),
-                                 "roofline_frac": round(ach / hbm, 4), "achieved_GBps": round(ach, 1)}
+                                 "roofline_frac": round(ach / hbm, 4), "achieved_GBps": round(ach, 1),
+                                 "kernel": eng.kernel_name(0 if d == "ul" else 1, BC, U, fcode)}
+    eng.set_fp16_algorithm("gram")
     # latency of one OFDM symbol's batch (1200 subcarriers x 8 clusters): eager vs CUDA graph
     from paper_1902_08653_b200 import GraphedUplink
     Hs, ys = H[:1200].contiguous(), y[:1200].contiguous()

@@ -227,9 +227,24 @@ int dcdg_round_fp16(dcdg_ctx* ctx, float* x, int64_t n, void* stream);
 int dcdg_convert(dcdg_ctx* ctx, const void* src, int src_fmt, void* dst, int dst_fmt,
                  int64_t n_complex, void* stream);
 
+/* fp16 uplink algorithm of a context (DCDG_FP16 batches of dcdg_ul_detect):
+ *   DCDG_ALG_SWEEP  the half2 residual sweep kernel (h_j^H r dots and rank-1
+ *                   r updates in half2 arithmetic, the paper's half-precision
+ *                   path, detect.cpp:67-110 with fp16 arithmetic);
+ *   DCDG_ALG_GRAM   fp16 storage, fp32 arithmetic: G = H^H H and z = H^H y on
+ *                   the tensor cores (mma.sync, fp32 accumulation), then the
+ *                   same sweeps in the U-dimensional space c = H^H r
+ *                   (B_c = 32, U = 16; other shapes use the sweep kernel).
+ * Both meet the fp16 tolerance against the reference; GRAM is the default. */
+#define DCDG_ALG_SWEEP 0
+#define DCDG_ALG_GRAM 1
+int dcdg_set_fp16_algorithm(dcdg_ctx* ctx, int alg);
+
 /* Which kernel variant a (direction, Bc, U, fmt) problem shape dispatches to:
  * writes a short name ("ul_f32_reg<32,16,8>", "ul_generic_f32", …). */
 int dcdg_kernel_name(int direction /*0 UL, 1 DL*/, int Bc, int U, int fmt, char* buf, int len);
+/* As dcdg_kernel_name, for the algorithm a context selects (fp16 uplink). */
+int dcdg_ctx_kernel_name(dcdg_ctx* ctx, int direction, int Bc, int U, int fmt, char* buf, int len);
 
 /* ---- fused cross-GPU exchange over peer memory (NVLink P2P) ----------------
  * Replaces "CD kernel, then an NCCL collective" for the uplink fusion of

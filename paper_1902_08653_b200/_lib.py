@@ -14,6 +14,7 @@ LIB_PATH = os.environ.get("DCDG_LIB_PATH") or os.path.join(os.path.dirname(os.pa
 DCDG_OK, DCDG_EINVAL, DCDG_ENUMERIC, DCDG_ECUDA, DCDG_ENCCL = 0, 1, 2, 3, 4
 FP32, FP16 = 0, 1
 FUSION_OPTIMAL, FUSION_UNIFORM = 0, 1
+ALG_SWEEP, ALG_GRAM = 0, 1
 
 
 class DcdgError(Exception):
@@ -80,6 +81,8 @@ SIGNATURES = {
                                    _vp]),
     "dcdg_zf_exact": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _vp, _vp]),
     "dcdg_kernel_name": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int]),
+    "dcdg_ctx_kernel_name": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int]),
+    "dcdg_set_fp16_algorithm": (C.c_int, [C.c_void_p, C.c_int]),
     "dcdg_xwin_create": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int64, C.POINTER(_vp)]),
     "dcdg_xwin_handle": (C.c_int, [_vp, _vp]),
     "dcdg_xwin_open": (C.c_int, [_vp, C.c_int, _vp]),

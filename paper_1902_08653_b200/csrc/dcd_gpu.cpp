@@ -126,7 +126,8 @@ void d2h(void* dst, const void* src, std::size_t bytes, void* st) {
 // How a reference PrecisionMode maps onto the device:
 //   fp64 / fp32          -> fp32 kernels
 //   fp16 messages_only   -> fp32 kernels + binary16 rounding of the wire payloads
-//   fp16 full_storage    -> half2 kernels (fp16 storage and arithmetic)
+//   fp16 full_storage    -> half2 sweep kernels (fp16 storage and arithmetic;
+//                           the Engine selects DCDG_ALG_SWEEP)
 struct DevPrecision {
   int fmt;
   bool round_messages;
@@ -179,6 +180,9 @@ void Engine::check(int status) {
 
 Engine::Engine(int device) : device_(device) {
   check(dcdg_init(device, &ctx_));
+  // PrecisionMode{fp16, full_storage} mirrors the reference's fp16 arithmetic
+  // emulation: the half2 sweep kernel, not the fp32-arithmetic Gram kernel
+  check(dcdg_set_fp16_algorithm(ctx_, DCDG_ALG_SWEEP));
   cudaStream_t st = nullptr;
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
     dcdg_destroy(ctx_);

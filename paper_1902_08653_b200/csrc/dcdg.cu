@@ -12,10 +12,12 @@
 #include <string>
 #include <utility>
 
+#include <cudaTypedefs.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include "dcdg.h"
 #include "dcdg_aux_kernels.cuh"
+#include "dcdg_gram_kernels.cuh"
 #include "dcdg_mw_kernels.cuh"
 #include "dcdg_sweep_kernels.cuh"
 #include "dcdg_reg_kernels.cuh"
@@ -28,6 +30,7 @@ struct dcdg_ctx {
   uint64_t launches = 0;
   void* scratch = nullptr;  // x_local / sigma2 / gain_part scratch
   size_t scratch_bytes = 0;
+  int fp16_alg = DCDG_ALG_GRAM;  // dcdg_set_fp16_algorithm
 };
 
 // Exchange window of one rank (dcdg_ul_detect_xchg): [flags][parity 0][parity 1]
@@ -379,6 +382,53 @@ const Spec kSpecs[] = {
     {64, 16, DCDG_FP16, UL_F16(64, 16, 8), DL_F16(64, 16, 8)},
 };
 
+// ---------------------------------------------------------------------------
+// Gram-space fp16 uplink (dcdg_gram_kernels.cuh): B_c = 32, U = 16.
+// ---------------------------------------------------------------------------
+#ifndef DCDG_GRAM_MINB
+#define DCDG_GRAM_MINB 16
+#endif
+constexpr int kGramNpw = 4;
+
+bool gram_shape(int bc, int u, int fmt) { return fmt == DCDG_FP16 && bc == 32 && u == 16; }
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+int launch_ul_gram(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X, cudaStream_t st) {
+  constexpr int U = 16, NPW = kGramNpw;
+  using L = dcdg::GramSmem<U, NPW>;
+  auto encode = tensor_map_encoder();
+  if (!encode) return fail(DCDG_ECUDA, "dcdg_ul_detect: cuTensorMapEncodeTiled unavailable");
+  // the tiles as rows of 128 B (one fp16 column of 32 antennas), P*U rows
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(P) * U};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(NPW * U)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(H), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DCDG_ECUDA, "dcdg_ul_detect: tensor map encode failed (" + std::to_string(r) + ")");
+  auto kern = dcdg::ul_gram_f16<U, NPW, DCDG_GRAM_MINB>;
+  static const int occ = occupancy_of(kern, L::kAlloc, 32);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int blocks = std::min(nsets, ctx->sms * occ);
+  kern<<<blocks, 32, L::kAlloc, st>>>(map, static_cast<const __half2*>(Y), P, K, kappa, static_cast<__half2*>(X));
+  CUDA_TRY(cudaGetLastError(), "ul_gram launch");
+  return DCDG_OK;
+}
+
 const Spec* find_spec(int bc, int u, int fmt) {
   for (const auto& s : kSpecs)
     if (s.bc == bc && s.u == u && s.fmt == fmt) return &s;
@@ -554,6 +604,24 @@ int dcdg_destroy(dcdg_ctx* ctx) {
 
 uint64_t dcdg_launch_count(dcdg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int dcdg_set_fp16_algorithm(dcdg_ctx* ctx, int alg) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (alg != DCDG_ALG_SWEEP && alg != DCDG_ALG_GRAM) return fail(DCDG_EINVAL, "dcdg_set_fp16_algorithm: unknown algorithm");
+  ctx->fp16_alg = alg;
+  return DCDG_OK;
+}
+
+int dcdg_ctx_kernel_name(dcdg_ctx* ctx, int direction, int Bc, int U, int fmt, char* buf, int len) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (direction == 0 && ctx->fp16_alg == DCDG_ALG_GRAM && gram_shape(Bc, U, fmt)) {
+    if (buf && len > 0) {
+      std::snprintf(buf, static_cast<size_t>(len), "ul_gram_f16<%d,%d,%d>", Bc, U, kGramNpw);
+    }
+    return DCDG_OK;
+  }
+  return dcdg_kernel_name(direction, Bc, U, fmt, buf, len);
+}
+
 int dcdg_kernel_name(int direction, int Bc, int U, int fmt, char* buf, int len) {
   const Spec* s = find_spec(Bc, U, fmt);
   char tmp[96];
@@ -658,7 +726,9 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
 
   const float kappa = static_cast<float>(n0 / ex);
   const Spec* spec = find_spec(Bc, U, fmt);
-  if (spec) {
+  if (ctx->fp16_alg == DCDG_ALG_GRAM && gram_shape(Bc, U, fmt)) {
+    if (int rc = launch_ul_gram(ctx, H, y, static_cast<int>(P), K, kappa, x_local, st)) return rc;
+  } else if (spec) {
     CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, x_local, nullptr, st), "ul_detect launch");
   } else {
     const size_t smem = 4 * (static_cast<size_t>(Bc) + 2 * U) * sizeof(float2);
@@ -1182,7 +1252,8 @@ int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* 
 
   const float kappa = static_cast<float>(n0 / ex);
   const Spec* spec = find_spec(Bc, U, fmt);
-  if (spec && spec->ulk.kind == kReg && !optimal) {
+  const bool gram = ctx->fp16_alg == DCDG_ALG_GRAM && gram_shape(Bc, U, fmt);  // no exchange epilogue
+  if (spec && spec->ulk.kind == kReg && !optimal && !gram) {
     // fused: the CD kernel stores into the owners' windows and signals
     CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, nullptr, &m, st), "ul_detect_xchg launch");
     ++ctx->launches;

@@ -137,6 +137,21 @@ class Engine:
     def launches(self) -> int:
         return int(lib().dcdg_launch_count(self._ctx))
 
+    def set_fp16_algorithm(self, alg: str) -> None:
+        """fp16 uplink kernel: "gram" (tensor-core Gram + fp32 sweeps in the
+        U-dimensional space, default) or "sweep" (half2 residual sweeps, the
+        paper's half-precision arithmetic).  See include/dcdg.h."""
+        codes = {"sweep": _lib.ALG_SWEEP, "gram": _lib.ALG_GRAM}
+        if alg not in codes:
+            raise ValueError(f"unknown fp16 algorithm {alg!r}")
+        check(lib().dcdg_set_fp16_algorithm(self._ctx, codes[alg]))
+
+    def kernel_name(self, direction: int, bc: int, u: int, fmt: int) -> str:
+        """Kernel this context dispatches a (direction, B_c, U, fmt) batch to."""
+        buf = C.create_string_buffer(96)
+        check(lib().dcdg_ctx_kernel_name(self._ctx, direction, bc, u, fmt, buf, 96))
+        return buf.value.decode()
+
     def _stream(self, stream):
         if stream is None:
             stream = torch.cuda.current_stream(self.device)

@@ -18,8 +18,10 @@ dev = torch.device("cuda", 0)
 eng = Engine(0)
 H, y, x, n0 = make_inputs(S, 8, dev, 1)
 out = {"lib": os.environ.get("DCDG_LIB_PATH", "default")}
-for fmt in ("fp32", "fp16"):
+for fmt in ("fp32", "fp16", "fp16sweep"):
     Hh, yh, xh = (H, y, x) if fmt == "fp32" else (to_fp16_pairs(H), to_fp16_pairs(y), to_fp16(x))
+    if fmt != "fp32" and hasattr(eng, "set_fp16_algorithm"):
+        eng.set_fp16_algorithm("sweep" if fmt == "fp16sweep" else "gram")
     esz = 8 if fmt == "fp32" else 4
     nbytes = S * 8 * (32 * 16 + 32 + 16) * esz
     for d in ("ul", "dl", "ul+fusion", "dl+gain"):
