@@ -151,13 +151,13 @@ def secondary_lines(eng, dev, S, reps, hbm):
     st = torch.cuda.current_stream(dev)
     P = S * C
     rho = math.sqrt(U)
-    # fp16: the default uplink kernel is the tensor-core Gram kernel; "fp16sweep"
-    # is the half2 residual-sweep kernel (the paper's half-precision arithmetic)
+    # fp16: the default kernels are the tensor-core Gram kernels; "fp16sweep"
+    # are the half2 residual-sweep kernels (the paper's half-precision arithmetic)
     for fmt in ("fp32", "fp16", "fp16sweep"):
         esz = 8 if fmt == "fp32" else 4
         Hh, yh, xh = (H, y, x) if fmt == "fp32" else (to_fp16_pairs(H), to_fp16_pairs(y), to_fp16(x))
         eng.set_fp16_algorithm("sweep" if fmt == "fp16sweep" else "gram")
-        for d in (("ul",) if fmt == "fp16sweep" else ("ul", "dl")):
+        for d in ("ul", "dl"):
             if d == "ul":
                 fn = lambda: eng.ul_detect(Hh, yh, n0=n0, K=K_SWEEPS, fusion="uniform")  # noqa: E731
                 kfn = lambda: eng.ul_detect(Hh, yh, n0=n0, K=K_SWEEPS, want_xhat=False)  # noqa: E731

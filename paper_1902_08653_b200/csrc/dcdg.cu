@@ -429,6 +429,40 @@ int launch_ul_gram(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, fl
   return DCDG_OK;
 }
 
+int launch_dl_gram(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X, float* gp,
+                   cudaStream_t st) {
+  constexpr int U = 16, NPW = kGramNpw;
+  using L = dcdg::GramSmem<U, NPW>;
+  auto encode = tensor_map_encoder();
+  if (!encode) return fail(DCDG_ECUDA, "dcdg_dl_precode: cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;  // as launch_ul_gram: P*U rows of 128 B
+  const cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(P) * U};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(NPW * U)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(H), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(DCDG_ECUDA, "dcdg_dl_precode: tensor map encode failed (" + std::to_string(r) + ")");
+  const int nsets = (P + NPW - 1) / NPW;
+#define DL_GRAM(GAIN)                                                                                              \
+  {                                                                                                                \
+    auto kern = dcdg::dl_gram_f16<U, NPW, DCDG_GRAM_MINB, GAIN>;                                                   \
+    static const int occ = occupancy_of(kern, L::kAlloc, 32);                                                      \
+    const int blocks = std::min(nsets, ctx->sms * occ);                                                           \
+    kern<<<blocks, 32, L::kAlloc, st>>>(map, static_cast<const __half2*>(H), static_cast<const __half2*>(S), P, C, K, \
+                                        rho_c, static_cast<__half2*>(X), gp, ctx->d_status);                       \
+  }
+  if (gp)
+    DL_GRAM(true)
+  else
+    DL_GRAM(false)
+#undef DL_GRAM
+  CUDA_TRY(cudaGetLastError(), "dl_gram launch");
+  return DCDG_OK;
+}
+
 const Spec* find_spec(int bc, int u, int fmt) {
   for (const auto& s : kSpecs)
     if (s.bc == bc && s.u == u && s.fmt == fmt) return &s;
@@ -613,9 +647,9 @@ int dcdg_set_fp16_algorithm(dcdg_ctx* ctx, int alg) {
 
 int dcdg_ctx_kernel_name(dcdg_ctx* ctx, int direction, int Bc, int U, int fmt, char* buf, int len) {
   if (int rc = check_ctx(ctx)) return rc;
-  if (direction == 0 && ctx->fp16_alg == DCDG_ALG_GRAM && gram_shape(Bc, U, fmt)) {
+  if (ctx->fp16_alg == DCDG_ALG_GRAM && gram_shape(Bc, U, fmt)) {
     if (buf && len > 0) {
-      std::snprintf(buf, static_cast<size_t>(len), "ul_gram_f16<%d,%d,%d>", Bc, U, kGramNpw);
+      std::snprintf(buf, static_cast<size_t>(len), "%s_gram_f16<%d,%d,%d>", direction ? "dl" : "ul", Bc, U, kGramNpw);
     }
     return DCDG_OK;
   }
@@ -784,7 +818,9 @@ int dcdg_dl_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, i
   // rho == 0: return the raw cd_precode beamformer (no power_scale)
   const float rho_c = static_cast<float>(rho / std::sqrt(static_cast<double>(C_total)));
   const Spec* spec = find_spec(Bc, U, fmt);
-  if (spec) {
+  if (ctx->fp16_alg == DCDG_ALG_GRAM && gram_shape(Bc, U, fmt)) {
+    if (int rc = launch_dl_gram(ctx, H, s, static_cast<int>(P), C, K, rho_c, x_dl, gain_part, st)) return rc;
+  } else if (spec) {
     CUDA_TRY(spec->dl(ctx, H, s, static_cast<int>(P), C, K, rho_c, x_dl, gain_part, st), "dl_precode launch");
   } else {
     const size_t smem = 4 * (static_cast<size_t>(Bc) + 2 * U) * sizeof(float2);

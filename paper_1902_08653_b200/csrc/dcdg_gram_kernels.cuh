@@ -96,6 +96,88 @@ __device__ __forceinline__ void csub_mul(float& cr, float& ci, float ar, float a
   ci = fmaf(-ar, bi, fmaf(-ai, br, ci));
 }
 
+// Tensor-core phase of a set (shared by the uplink and downlink kernels): the
+// Gram G = H^H H (and, with Z, the matched filter z = H^H y) of each of the
+// NPW problems, from the swizzled TMA slot, handed through the padded transit
+// buffer to the problem's 8 sweep lanes: lane k of problem q gets rows 2k and
+// 2k+1 of G (and z_{2k}, z_{2k+1}).
+template <int U, int NPW, bool Z>
+__device__ __forceinline__ void gram_tc_phase(unsigned char* sm, uint32_t sbase, int lane, float (&g0r)[U],
+                                              float (&g0i)[U], float (&g1r)[U], float (&g1i)[U], float (&cr)[2],
+                                              float (&ci)[2]) {
+  using L = GramSmem<U, NPW>;
+  const int g = lane >> 2, t = lane & 3;  // mma fragment coordinates
+  const int q = lane >> 3, k = lane & 7;
+  // ldmatrix row of this lane: matrix mi = lane/8 -> users (mi&1)*8 + lane%8, chunk half mi>>1
+  const int lu = ((lane >> 3) & 1) * 8 + (lane & 7), lch = lane >> 4;
+  unsigned char* gbuf = sm + L::kGOff;
+  float2* zbuf = reinterpret_cast<float2*>(sm + L::kZOff);
+#pragma unroll
+  for (int pl = 0; pl < NPW; ++pl) {
+    float gr[2][4] = {}, gi[2][4] = {}, zz[4] = {};
+    const int row = pl * U + lu;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      uint32_t a[4];
+      const int ch = 2 * ks + lch;
+      ldsm_x4(a, sbase + row * L::kRowB + ((ch ^ (row & 7)) << 4));
+      // B = W: n-tile 0 (users 0-7) = (a0, a2), n-tile 1 (users 8-15) = (a1, a3)
+      mma_f16f32(gr[0], a, a[0], a[2]);
+      mma_f16f32(gr[1], a, a[1], a[3]);
+      mma_f16f32(gi[0], a, swap_neg(a[0], t), swap_neg(a[2], t));
+      mma_f16f32(gi[1], a, swap_neg(a[1], t), swap_neg(a[3], t));
+      if (Z) {
+        // B = [Y, Y', 0 ...]: column g = 0 is y, g = 1 its swapped/negated words
+        uint32_t y0 = 0, y1 = 0;
+        if (g < 2) {
+          const uint32_t* yw = reinterpret_cast<const uint32_t*>(sm + L::kYOff + pl * 128);
+          const int w = g ? (t ^ 1) : t;
+          const uint32_t sg = (g && (t & 1)) ? 0x80008000u : 0u;
+          y0 = yw[(2 * ks) * 4 + w] ^ sg;
+          y1 = yw[(2 * ks + 1) * 4 + w] ^ sg;
+        }
+        mma_f16f32(zz, a, y0, y1);
+      }
+    }
+    __syncwarp();  // the previous problem's lanes have read the transit buffer
+    // C fragments: (row g, cols 2t, 2t+1) and (row g+8, same cols) of each n-tile
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = nt * 8 + 2 * t + h;
+        // row g -> (k = g/2, r = g%2); row g+8 -> (k = g/2 + 4, r = g%2)
+        *reinterpret_cast<float2*>(gbuf + (g >> 1) * L::kGStride + j * 16 + (g & 1) * 8) =
+            make_float2(gr[nt][h], gi[nt][h]);
+        *reinterpret_cast<float2*>(gbuf + ((g >> 1) + 4) * L::kGStride + j * 16 + (g & 1) * 8) =
+            make_float2(gr[nt][2 + h], gi[nt][2 + h]);
+      }
+    if (Z && t == 0) {
+      zbuf[g] = make_float2(zz[0], zz[1]);
+      zbuf[g + 8] = make_float2(zz[2], zz[3]);
+    }
+    __syncwarp();
+    if (q == pl) {
+      const unsigned char* mine = gbuf + k * L::kGStride;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const float4 v = *reinterpret_cast<const float4*>(mine + j * 16);
+        g0r[j] = v.x;
+        g0i[j] = v.y;
+        g1r[j] = v.z;
+        g1i[j] = v.w;
+      }
+      if (Z) {
+        const float4 zv = reinterpret_cast<const float4*>(zbuf)[k];
+        cr[0] = zv.x;
+        ci[0] = zv.y;
+        cr[1] = zv.z;
+        ci[1] = zv.w;
+      }
+    }
+  }
+}
+
 template <int U, int NPW, int MINB>
 __global__ void __launch_bounds__(32, MINB)
     ul_gram_f16(const __grid_constant__ CUtensorMap tmH, const __half2* __restrict__ Y, int P, int K, float kappa,
@@ -108,7 +190,6 @@ __global__ void __launch_bounds__(32, MINB)
   const uint32_t sbase = smem_u32(sm);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::kBarOff);
   const int lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;  // mma fragment coordinates
   const int q = lane >> 3, k = lane & 7;  // sweep: problem q of the set; lane k owns users 2k, 2k+1
   const int nsets = (P + NPW - 1) / NPW;
   int set = blockIdx.x;
@@ -128,10 +209,6 @@ __global__ void __launch_bounds__(32, MINB)
   };
   if (lane == 0 && set < nsets) issue(set);
   uint32_t phase = 0;
-  // ldmatrix row of this lane: matrix mi = lane/8 -> users (mi&1)*8 + lane%8, chunk half mi>>1
-  const int lu = ((lane >> 3) & 1) * 8 + (lane & 7), lch = lane >> 4;
-  unsigned char* gbuf = sm + L::kGOff;
-  float2* zbuf = reinterpret_cast<float2*>(sm + L::kZOff);
   for (; set < nsets; set += gridDim.x) {
     mbar_wait(bar, phase);
     phase ^= 1u;
@@ -139,66 +216,7 @@ __global__ void __launch_bounds__(32, MINB)
     float g0r[U], g0i[U], g1r[U], g1i[U];
     float cr[2], ci[2];
     // ---------------- tensor-core phase: G and z of each problem, handed to its 8 sweep lanes
-#pragma unroll
-    for (int pl = 0; pl < NPW; ++pl) {
-      float gr[2][4] = {}, gi[2][4] = {}, zz[4] = {};
-      const int row = pl * U + lu;
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        uint32_t a[4];
-        const int ch = 2 * ks + lch;
-        ldsm_x4(a, sbase + row * L::kRowB + ((ch ^ (row & 7)) << 4));
-        // B = W: n-tile 0 (users 0-7) = (a0, a2), n-tile 1 (users 8-15) = (a1, a3)
-        mma_f16f32(gr[0], a, a[0], a[2]);
-        mma_f16f32(gr[1], a, a[1], a[3]);
-        mma_f16f32(gi[0], a, swap_neg(a[0], t), swap_neg(a[2], t));
-        mma_f16f32(gi[1], a, swap_neg(a[1], t), swap_neg(a[3], t));
-        // B = [Y, Y', 0 ...]: column g = 0 is y, g = 1 its swapped/negated words
-        uint32_t y0 = 0, y1 = 0;
-        if (g < 2) {
-          const uint32_t* yw = reinterpret_cast<const uint32_t*>(sm + L::kYOff + pl * 128);
-          const int w = g ? (t ^ 1) : t;
-          const uint32_t sg = (g && (t & 1)) ? 0x80008000u : 0u;
-          y0 = yw[(2 * ks) * 4 + w] ^ sg;
-          y1 = yw[(2 * ks + 1) * 4 + w] ^ sg;
-        }
-        mma_f16f32(zz, a, y0, y1);
-      }
-      __syncwarp();  // the previous problem's lanes have read the transit buffer
-      // C fragments: (row g, cols 2t, 2t+1) and (row g+8, same cols) of each n-tile
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int j = nt * 8 + 2 * t + h;
-          // row g -> (k = g/2, r = g%2); row g+8 -> (k = g/2 + 4, r = g%2)
-          *reinterpret_cast<float2*>(gbuf + (g >> 1) * L::kGStride + j * 16 + (g & 1) * 8) =
-              make_float2(gr[nt][h], gi[nt][h]);
-          *reinterpret_cast<float2*>(gbuf + ((g >> 1) + 4) * L::kGStride + j * 16 + (g & 1) * 8) =
-              make_float2(gr[nt][2 + h], gi[nt][2 + h]);
-        }
-      if (t == 0) {
-        zbuf[g] = make_float2(zz[0], zz[1]);
-        zbuf[g + 8] = make_float2(zz[2], zz[3]);
-      }
-      __syncwarp();
-      if (q == pl) {
-        const unsigned char* mine = gbuf + k * L::kGStride;
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-          const float4 v = *reinterpret_cast<const float4*>(mine + j * 16);
-          g0r[j] = v.x;
-          g0i[j] = v.y;
-          g1r[j] = v.z;
-          g1i[j] = v.w;
-        }
-        const float4 zv = reinterpret_cast<const float4*>(zbuf)[k];
-        cr[0] = zv.x;
-        ci[0] = zv.y;
-        cr[1] = zv.z;
-        ci[1] = zv.w;
-      }
-    }
+    gram_tc_phase<U, NPW, true>(sm, sbase, lane, g0r, g0i, g1r, g1i, cr, ci);
     fence_proxy_async_all();
     __syncwarp();
     if (lane == 0 && set + static_cast<int>(gridDim.x) < nsets) issue(set + gridDim.x);
@@ -260,6 +278,184 @@ __global__ void __launch_bounds__(32, MINB)
       reinterpret_cast<uint2*>(X + static_cast<size_t>(p) * U)[k] = w;
     }
     __syncwarp();
+  }
+}
+
+__device__ __forceinline__ uint64_t l2_evict_normal_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// 16-B read-only global load, no L1 allocation, with an L2 eviction policy
+__device__ __forceinline__ uint4 ldg_nc_hint(const void* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
+// Gram-space downlink CD (Alg. 2 / Eq. 5, precode.cpp:52-99 on raw rows, as
+// dl_reg_f16): every iterate is x = H a (a in C^U), so the dual update reads
+// the channel only through w = H^H x = G a:
+//     rho_u = q_u (w_u - s_u);  a_u -= rho_u;  w_k -= rho_u G_ku  for every k,
+// with q_u = 1/||h_u||^2.  G comes from the tensor cores exactly as in the
+// uplink kernel; the sweeps keep w and a in fp32 on the problem's 8 lanes
+// (pairs of coordinates, the second corrected with G_{2k+1,2k}).  After the
+// sweeps x = H a is formed on the CUDA cores from the problem's tile re-read
+// from L2 (the TMA brought it in with evict-normal priority; the slot already
+// holds the next set), then ||x||^2 gives power_scale (precode.cpp:101-111)
+// and Re(s^H w) the effective-gain share (precode.cpp:123-131).
+template <int U, int NPW, int MINB, bool GAIN>
+__global__ void __launch_bounds__(32, MINB)
+    dl_gram_f16(const __grid_constant__ CUtensorMap tmH, const __half2* __restrict__ H, const __half2* __restrict__ Sy,
+                int P, int C, int K, float rho_c, __half2* __restrict__ X, float* __restrict__ gain_part,
+                unsigned long long* __restrict__ status) {
+  static_assert(NPW == 4, "a set is 4 problems of 8 sweep lanes");
+  constexpr int BC = 32;
+  using L = GramSmem<U, NPW>;
+  extern __shared__ unsigned char smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  unsigned char* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  const uint32_t sbase = smem_u32(sm);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::kBarOff);
+  const int lane = threadIdx.x & 31;
+  const int q = lane >> 3, k = lane & 7;  // sweep: problem q of the set; lane k owns users 2k, 2k+1
+  const int nsets = (P + NPW - 1) / NPW;
+  int set = blockIdx.x;
+  const uint64_t pol_keep = l2_evict_normal_policy(), pol_last_use = l2_evict_first_policy();
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](int s) {
+    mbar_arrive_expect_tx(bar, static_cast<uint32_t>(L::kSlotB));
+    tma_load_2d(sm, &tmH, 0, s * NPW * U, bar, pol_keep);
+  };
+  if (lane == 0 && set < nsets) issue(set);
+  uint32_t phase = 0;
+  float4* abuf = reinterpret_cast<float4*>(sm + L::kYOff);  // a of the set's problems: [q][k] (a_2k, a_2k+1)
+  for (; set < nsets; set += gridDim.x) {
+    const int p = set * NPW + q;
+    // s_{2k}, s_{2k+1} of the problem's subcarrier, in flight during the tensor-core phase
+    uint32_t sw0 = 0, sw1 = 0;
+    if (p < P) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(Sy + static_cast<size_t>(p / C) * U) + k);
+      sw0 = v.x;
+      sw1 = v.y;
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    float g0r[U], g0i[U], g1r[U], g1i[U];
+    float unused_r[2], unused_i[2];
+    gram_tc_phase<U, NPW, false>(sm, sbase, lane, g0r, g0i, g1r, g1i, unused_r, unused_i);
+    fence_proxy_async_all();
+    __syncwarp();
+    if (lane == 0 && set + static_cast<int>(gridDim.x) < nsets) issue(set + gridDim.x);
+
+    // ---------------- sweep phase (dual coordinates in fp32)
+    float e[2];
+#pragma unroll
+    for (int jp = 0; jp < U / 2; ++jp)
+      if (k == jp) {
+        e[0] = g0r[2 * jp];      // ||h_2k||^2
+        e[1] = g1r[2 * jp + 1];  // ||h_2k+1||^2
+      }
+    float qv[2], sqr[2], sqi[2];
+    {
+      const float2 s0 = __half22float2(u32_as_h2(sw0)), s1 = __half22float2(u32_as_h2(sw1));
+      qv[0] = __frcp_rn(e[0]);
+      qv[1] = __frcp_rn(e[1]);
+      sqr[0] = qv[0] * s0.x;  // q_u s_u: the normalised symbol scaled by 1/||h_u|| (precode.cpp:80-87)
+      sqi[0] = qv[0] * s0.y;
+      sqr[1] = qv[1] * s1.x;
+      sqi[1] = qv[1] * s1.y;
+    }
+    float ar[2] = {0.f, 0.f}, ai[2] = {0.f, 0.f}, wr[2] = {0.f, 0.f}, wi[2] = {0.f, 0.f};
+    const int base = lane & ~7;
+    for (int sw = 0; sw < K; ++sw) {
+#pragma unroll
+      for (int jp = 0; jp < U / 2; ++jp) {
+        const int j0 = 2 * jp, j1 = 2 * jp + 1;
+        // rho_u = q_u h_u^H x - q_u s_u  (precode.cpp:89-94, raw rows); the owner's (lane jp) is the update
+        const float r0r = fmaf(qv[0], wr[0], -sqr[0]), r0i = fmaf(qv[0], wi[0], -sqi[0]);
+        float f1r = wr[1], f1i = wi[1];
+        csub_mul(f1r, f1i, r0r, r0i, g1r[j0], g1i[j0]);  // w_{j+1} after x -= rho_j h_j
+        const float r1r = fmaf(qv[1], f1r, -sqr[1]), r1i = fmaf(qv[1], f1i, -sqi[1]);
+        const float b0r = __shfl_sync(0xffffffffu, r0r, base + jp);
+        const float b0i = __shfl_sync(0xffffffffu, r0i, base + jp);
+        const float b1r = __shfl_sync(0xffffffffu, r1r, base + jp);
+        const float b1i = __shfl_sync(0xffffffffu, r1i, base + jp);
+        if (k == jp) {
+          ar[0] -= r0r;
+          ai[0] -= r0i;
+          ar[1] -= r1r;
+          ai[1] -= r1i;
+        }
+        // x -= rho_j h_j + rho_{j+1} h_{j+1}  <=>  w_k -= rho_j G_kj + rho_{j+1} G_k,j+1
+        csub_mul(wr[0], wi[0], b0r, b0i, g0r[j0], g0i[j0]);
+        csub_mul(wr[0], wi[0], b1r, b1i, g0r[j1], g0i[j1]);
+        csub_mul(wr[1], wi[1], b0r, b0i, g1r[j0], g1i[j0]);
+        csub_mul(wr[1], wi[1], b1r, b1i, g1r[j1], g1i[j1]);
+      }
+    }
+    // ---------------- x = H a: lane k forms antennas 4k..4k+3 (its 16-B chunk of every column)
+    abuf[q * (U / 2) + k] = make_float4(ar[0], ai[0], ar[1], ai[1]);
+    __syncwarp();
+    float xr[4] = {0.f, 0.f, 0.f, 0.f}, xi[4] = {0.f, 0.f, 0.f, 0.f};
+    if (p < P) {
+      const unsigned char* hp = reinterpret_cast<const unsigned char*>(H) + static_cast<size_t>(p) * U * BC * 4 + k * 16;
+      uint4 hv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) hv[u] = ldg_nc_hint(hp + u * BC * 4, pol_last_use);
+#pragma unroll
+      for (int u2 = 0; u2 < U / 2; ++u2) {
+        const float4 av = abuf[q * (U / 2) + u2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint4 v = hv[2 * u2 + h];
+          const float aR = h ? av.z : av.x, aI = h ? av.w : av.y;
+          const float2 re01 = __half22float2(u32_as_h2(v.x)), im01 = __half22float2(u32_as_h2(v.y));
+          const float2 re23 = __half22float2(u32_as_h2(v.z)), im23 = __half22float2(u32_as_h2(v.w));
+          const float hr[4] = {re01.x, re01.y, re23.x, re23.y}, hi[4] = {im01.x, im01.y, im23.x, im23.y};
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            xr[b] = fmaf(hr[b], aR, fmaf(-hi[b], aI, xr[b]));
+            xi[b] = fmaf(hr[b], aI, fmaf(hi[b], aR, xi[b]));
+          }
+        }
+      }
+    }
+    float en = 0.f;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) en = fmaf(xr[b], xr[b], fmaf(xi[b], xi[b], en));
+    const float nrm = gsum<8>(en);
+    const float gsc = rho_c > 0.f ? rho_c / __fsqrt_rn(nrm) : 1.f;  // power_scale, rho_c = rho/sqrt(C)
+    float gq = 0.f;
+    if (GAIN) {
+      const float2 s0 = __half22float2(u32_as_h2(sw0)), s1 = __half22float2(u32_as_h2(sw1));
+      // Re(s^H H^H x) = Re(s^H w), w = G a tracked through the sweeps
+      gq = gsc * gsum<8>(fmaf(s0.x, wr[0], fmaf(s0.y, wi[0], fmaf(s1.x, wr[1], s1.y * wi[1]))));
+    }
+    if (p < P) {
+      if (e[0] == 0.f)
+        record_status(status, p, ST_ZERO_ROW, 2 * k);
+      else if (e[1] == 0.f)
+        record_status(status, p, ST_ZERO_ROW, 2 * k + 1);
+      if (k == 0) {
+        if (nrm == 0.f && rho_c > 0.f) record_status(status, p, ST_ZERO_BEAMFORMER, 0);
+        if (GAIN) gain_part[p] = gq;
+      }
+      uint4 v;  // the precoder is interleaved complex (re, im) per antenna, antennas 4k..4k+3
+      v.x = h2_as_u32(__floats2half2_rn(gsc * xr[0], gsc * xi[0]));
+      v.y = h2_as_u32(__floats2half2_rn(gsc * xr[1], gsc * xi[1]));
+      v.z = h2_as_u32(__floats2half2_rn(gsc * xr[2], gsc * xi[2]));
+      v.w = h2_as_u32(__floats2half2_rn(gsc * xr[3], gsc * xi[3]));
+      reinterpret_cast<uint4*>(X + static_cast<size_t>(p) * BC)[k] = v;
+    }
+    __syncwarp();  // abuf is rewritten by the next set
   }
 }
 
