@@ -227,14 +227,18 @@ int dcdg_round_fp16(dcdg_ctx* ctx, float* x, int64_t n, void* stream);
 int dcdg_convert(dcdg_ctx* ctx, const void* src, int src_fmt, void* dst, int dst_fmt,
                  int64_t n_complex, void* stream);
 
-/* fp16 uplink algorithm of a context (DCDG_FP16 batches of dcdg_ul_detect):
- *   DCDG_ALG_SWEEP  the half2 residual sweep kernel (h_j^H r dots and rank-1
- *                   r updates in half2 arithmetic, the paper's half-precision
- *                   path, detect.cpp:67-110 with fp16 arithmetic);
- *   DCDG_ALG_GRAM   fp16 storage, fp32 arithmetic: G = H^H H and z = H^H y on
- *                   the tensor cores (mma.sync, fp32 accumulation), then the
- *                   same sweeps in the U-dimensional space c = H^H r
- *                   (B_c = 32, U = 16; other shapes use the sweep kernel).
+/* fp16 algorithm of a context (DCDG_FP16 batches of dcdg_ul_detect and
+ * dcdg_dl_precode):
+ *   DCDG_ALG_SWEEP  the half2 residual sweep kernels (h_j^H r dots and rank-1
+ *                   r / x updates in half2 arithmetic, the paper's
+ *                   half-precision path: detect.cpp:67-110 and
+ *                   precode.cpp:52-99 with fp16 arithmetic);
+ *   DCDG_ALG_GRAM   fp16 storage, fp32 arithmetic: G = H^H H (and z = H^H y)
+ *                   on the tensor cores (mma.sync, fp32 accumulation), then
+ *                   the same sweeps in the U-dimensional spaces c = H^H r
+ *                   (uplink) and w = H^H x = G a (downlink, x = H a formed at
+ *                   the end) (B_c = 32, U = 16; other shapes use the sweep
+ *                   kernels).
  * Both meet the fp16 tolerance against the reference; GRAM is the default. */
 #define DCDG_ALG_SWEEP 0
 #define DCDG_ALG_GRAM 1
@@ -243,7 +247,7 @@ int dcdg_set_fp16_algorithm(dcdg_ctx* ctx, int alg);
 /* Which kernel variant a (direction, Bc, U, fmt) problem shape dispatches to:
  * writes a short name ("ul_f32_reg<32,16,8>", "ul_generic_f32", …). */
 int dcdg_kernel_name(int direction /*0 UL, 1 DL*/, int Bc, int U, int fmt, char* buf, int len);
-/* As dcdg_kernel_name, for the algorithm a context selects (fp16 uplink). */
+/* As dcdg_kernel_name, for the fp16 algorithm a context selects. */
 int dcdg_ctx_kernel_name(dcdg_ctx* ctx, int direction, int Bc, int U, int fmt, char* buf, int len);
 
 /* ---- fused cross-GPU exchange over peer memory (NVLink P2P) ----------------
