@@ -86,9 +86,31 @@ struct GramSmem {
   static constexpr int kGOff = kYOff + NPW * 128;
   static constexpr int kZOff = kGOff + (U / 2) * kGStride;  // z: [j] float2
   static constexpr int kBarOff = kZOff + U * 8;
-  static constexpr int kBytes = kBarOff + 16;
+  static constexpr int kBcOff = kBarOff + 16;       // sweep broadcast slots: [NPW][2] float4
+  static constexpr int kBytes = kBcOff + NPW * 32;
   static constexpr int kAlloc = kBytes + 1024;      // slack to align the swizzled slot to 1024 B
 };
+
+#ifndef DCDG_GRAM_SMEM_BCAST
+#define DCDG_GRAM_SMEM_BCAST 1
+#endif
+// The pair's two updates from its owner lane (base + jp) to the problem's 8
+// lanes: one 16-B store by the owner into an alternating shared-memory slot
+// and one 16-B broadcast load (default; 0.8-1.2% faster than the four
+// shuffles of DCDG_GRAM_SMEM_BCAST=0, profiles/lab/README.md).
+__device__ __forceinline__ float4 pair_bcast(float4 v, int JP, int k, int base, float4* slots) {
+#if DCDG_GRAM_SMEM_BCAST
+  float4* sl = slots + (JP & 1);
+  if (k == JP) *sl = v;
+  __syncwarp();
+  return *sl;
+#else
+  (void)k;
+  (void)slots;
+  return make_float4(__shfl_sync(0xffffffffu, v.x, base + JP), __shfl_sync(0xffffffffu, v.y, base + JP),
+                     __shfl_sync(0xffffffffu, v.z, base + JP), __shfl_sync(0xffffffffu, v.w, base + JP));
+#endif
+}
 
 // complex c -= a * b
 __device__ __forceinline__ void csub_mul(float& cr, float& ci, float ar, float ai, float br, float bi) {
@@ -241,6 +263,7 @@ __global__ void __launch_bounds__(32, MINB)
       }
     }
     const int base = lane & ~7;
+    float4* bslots = reinterpret_cast<float4*>(sm + L::kBcOff) + 2 * q;
     for (int sw = 0; sw < K; ++sw) {
 #pragma unroll
       for (int jp = 0; jp < U / 2; ++jp) {
@@ -253,10 +276,8 @@ __global__ void __launch_bounds__(32, MINB)
         csub_mul(c1r, c1i, d0r, d0i, g1r[j0], g1i[j0]);  // d_{j+1} = c_{j+1} - dx_j G_{j+1,j}
         const float n1r = fmaf(mm[1], c1r, nn[1] * xr[1]), n1i = fmaf(mm[1], c1i, nn[1] * xi[1]);
         const float d1r = n1r - xr[1], d1i = n1i - xi[1];
-        const float a0r = __shfl_sync(0xffffffffu, d0r, base + jp);
-        const float a0i = __shfl_sync(0xffffffffu, d0i, base + jp);
-        const float a1r = __shfl_sync(0xffffffffu, d1r, base + jp);
-        const float a1i = __shfl_sync(0xffffffffu, d1i, base + jp);
+        const float4 bv = pair_bcast(make_float4(d0r, d0i, d1r, d1i), jp, k, base, bslots);
+        const float a0r = bv.x, a0i = bv.y, a1r = bv.z, a1i = bv.w;
         if (k == jp) {
           xr[0] = n0r;
           xi[0] = n0i;
@@ -375,6 +396,7 @@ __global__ void __launch_bounds__(32, MINB)
     }
     float ar[2] = {0.f, 0.f}, ai[2] = {0.f, 0.f}, wr[2] = {0.f, 0.f}, wi[2] = {0.f, 0.f};
     const int base = lane & ~7;
+    float4* bslots = reinterpret_cast<float4*>(sm + L::kBcOff) + 2 * q;
     for (int sw = 0; sw < K; ++sw) {
 #pragma unroll
       for (int jp = 0; jp < U / 2; ++jp) {
@@ -384,10 +406,8 @@ __global__ void __launch_bounds__(32, MINB)
         float f1r = wr[1], f1i = wi[1];
         csub_mul(f1r, f1i, r0r, r0i, g1r[j0], g1i[j0]);  // w_{j+1} after x -= rho_j h_j
         const float r1r = fmaf(qv[1], f1r, -sqr[1]), r1i = fmaf(qv[1], f1i, -sqi[1]);
-        const float b0r = __shfl_sync(0xffffffffu, r0r, base + jp);
-        const float b0i = __shfl_sync(0xffffffffu, r0i, base + jp);
-        const float b1r = __shfl_sync(0xffffffffu, r1r, base + jp);
-        const float b1i = __shfl_sync(0xffffffffu, r1i, base + jp);
+        const float4 bv = pair_bcast(make_float4(r0r, r0i, r1r, r1i), jp, k, base, bslots);
+        const float b0r = bv.x, b0i = bv.y, b1r = bv.z, b1i = bv.w;
         if (k == jp) {
           ar[0] -= r0r;
           ai[0] -= r0i;
