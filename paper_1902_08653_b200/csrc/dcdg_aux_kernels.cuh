@@ -507,6 +507,9 @@ __global__ void __launch_bounds__(128) gram_chol(const T* __restrict__ H, int P,
 // half).  gram_chol's factorisation keeps half the warp idle at U = 16; here
 // every lane works, so the scalar Cholesky/inverse stream serves two problems.
 // ===========================================================================
+#ifndef DCDG_PEV_TRI  // lower-triangle-only Gram (lab switch: measured slower for fp32, see below)
+#define DCDG_PEV_TRI 0
+#endif
 template <typename T, int BT>
 __global__ void __launch_bounds__(128) pev16_pair_kernel(const T* __restrict__ H, int P, float gam, float scale,
                                                          bool round_fp16, float* __restrict__ out,
@@ -560,6 +563,85 @@ __global__ void __launch_bounds__(128) pev16_pair_kernel(const T* __restrict__ H
     }
   }
   __syncwarp();
+#if DCDG_PEV_TRI
+  // ---- Grams, lower triangles only (detect.cpp:118-121 reads i >= j): both
+  // problems at once.  Lanes 0-23: half of an off-diagonal 4x4 block (4x2,
+  // 6 blocks per problem); lanes 24-31: the left 4x2 of a diagonal 4x4 block;
+  // lanes 0-7 also the bottom-right 2x2 of a diagonal block.  24 FFMA2 per
+  // staged row on the busiest lanes instead of 2 x 16 for two full Grams.
+  // Bitwise-identical variances, but 0.452 vs 0.428 ms (fp32) and 0.421 vs
+  // 0.427 ms (fp16) per 134 400 problems: the factorisation chain, not the
+  // Gram, bounds this kernel, and the mixed-problem loads conflict in banks.
+  {
+    constexpr int kOffI[6] = {1, 2, 2, 3, 3, 3}, kOffJ[6] = {0, 0, 1, 0, 1, 2};
+    int t1, i1, j1;
+    if (lane < 24) {
+      const int idx = lane % 12, bp = idx >> 1;
+      t1 = lane / 12;
+      i1 = 4 * kOffI[bp];
+      j1 = 4 * kOffJ[bp] + 2 * (idx & 1);
+    } else {
+      t1 = (lane - 24) >> 2;
+      i1 = j1 = 4 * ((lane - 24) & 3);
+    }
+    const int t2 = (lane & 7) >> 2, d2 = 4 * (lane & 3) + 2;  // 2x2 unit (rows/cols d2, d2+1) of problem t2
+    const float2* h1 = Hs + t1 * N * (PR + 1);
+    const float2* h2 = Hs + t2 * N * (PR + 1);
+    float2 pa[4][2], qa[4][2], pb[2][2], qb[2][2];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) pa[r][q] = qa[r][q] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) pb[r][q] = qb[r][q] = make_float2(0.f, 0.f);
+#pragma unroll 8
+    for (int b = 0; b < PR; ++b) {
+      float2 a[4], c[2], a2[2];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = h1[(i1 + r) * (PR + 1) + b];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) c[q] = h1[(j1 + q) * (PR + 1) + b];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) a2[r] = h2[(d2 + r) * (PR + 1) + b];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          pa[r][q] = ffma2(a[r].x, c[q], pa[r][q]);
+          qa[r][q] = ffma2(a[r].y, c[q], qa[r][q]);
+        }
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          pb[r][q] = ffma2(a2[r].x, a2[q], pb[r][q]);
+          qb[r][q] = ffma2(a2[r].y, a2[q], qb[r][q]);
+        }
+    }
+    float2* A1 = A + t1 * N * N;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int i = i1 + r, j = j1 + q;
+        const float gr = pa[r][q].x + qa[r][q].y, gi = pa[r][q].y - qa[r][q].x;
+        if (i >= j) A1[j * N + i] = make_float2((i == j ? 1.f : 0.f) + gam * gr, gam * gi);
+      }
+    if (lane < 8) {
+      float2* A2 = A + t2 * N * N;
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int q = 0; q <= r; ++q) {
+          const int i = d2 + r, j = d2 + q;
+          const float gr = pb[r][q].x + qb[r][q].y, gi = pb[r][q].y - qb[r][q].x;
+          A2[j * N + i] = make_float2((i == j ? 1.f : 0.f) + gam * gr, gam * gi);
+        }
+    }
+  }
+#else
   // ---- Grams: lane -> 4x2 block (rows 4*ib.., columns 2*jb..) of G_t; A_t = I + gam G_t
   const int i0 = 4 * (lane >> 3), j0 = 2 * (lane & 7);
 #pragma unroll
@@ -598,6 +680,7 @@ __global__ void __launch_bounds__(128) pev16_pair_kernel(const T* __restrict__ H
           At[j * N + i] = make_float2((i == j ? 1.f : 0.f) + gam * gr, gam * gi);
       }
   }
+#endif
   __syncwarp();  // the staged tiles are dead from here: Lr reuses their space
   // ---- factorisation, half-warp h = problem p0 + h, lane i = row i
   const int hf = lane >> 4, i = lane & 15;
