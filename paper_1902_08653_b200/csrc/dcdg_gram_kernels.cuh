@@ -317,6 +317,17 @@ __device__ __forceinline__ uint4 ldg_nc_hint(const void* p, uint64_t pol) {
   return v;
 }
 
+#ifndef DCDG_DL_GRAM_PREFETCH
+#define DCDG_DL_GRAM_PREFETCH 0  // lab switch, measured slower (profiles/lab/README.md)
+#endif
+__device__ __forceinline__ uint4 ldg_nc_l1(const void* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
 // Gram-space downlink CD (Alg. 2 / Eq. 5, precode.cpp:52-99 on raw rows, as
 // dl_reg_f16): every iterate is x = H a (a in C^U), so the dual update reads
 // the channel only through w = H^H x = G a:
@@ -398,6 +409,13 @@ __global__ void __launch_bounds__(32, MINB)
     const int base = lane & ~7;
     float4* bslots = reinterpret_cast<float4*>(sm + L::kBcOff) + 2 * q;
     for (int sw = 0; sw < K; ++sw) {
+#if DCDG_DL_GRAM_PREFETCH
+      if (sw == K - 1 && p < P) {  // the tile's columns 2k, 2k+1 (one 128-B line each) into L1 for x = H a
+        const char* hl = reinterpret_cast<const char*>(H) + static_cast<size_t>(p) * U * BC * 4 + (2 * k) * BC * 4;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(hl));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(hl + BC * 4));
+      }
+#endif
 #pragma unroll
       for (int jp = 0; jp < U / 2; ++jp) {
         const int j0 = 2 * jp, j1 = 2 * jp + 1;
@@ -429,7 +447,8 @@ __global__ void __launch_bounds__(32, MINB)
       const unsigned char* hp = reinterpret_cast<const unsigned char*>(H) + static_cast<size_t>(p) * U * BC * 4 + k * 16;
       uint4 hv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) hv[u] = ldg_nc_hint(hp + u * BC * 4, pol_last_use);
+      for (int u = 0; u < U; ++u)
+        hv[u] = DCDG_DL_GRAM_PREFETCH ? ldg_nc_l1(hp + u * BC * 4, pol_last_use) : ldg_nc_hint(hp + u * BC * 4, pol_last_use);
 #pragma unroll
       for (int u2 = 0; u2 < U / 2; ++u2) {
         const float4 av = abuf[q * (U / 2) + u2];
