@@ -197,6 +197,14 @@ def secondary_lines(eng, dev, S, reps, hbm):
     out["ul_fp32_optimal_fusion"] = {"value": round(S * U * BITS / (ms * 1e-3) / 1e9, 4), "unit": "Gbps",
                                      "ms_per_batch": round(ms, 5),
                                      "note": "CD kernel + post-equalization variance (Gram+Cholesky) + fusion"}
+    H16, y16 = to_fp16_pairs(H), to_fp16_pairs(y)
+    fn = lambda: eng.ul_detect(H16, y16, n0=n0, K=K_SWEEPS, fusion="optimal")  # noqa: E731
+    fn()
+    ms = _time_stream(fn, st, reps)
+    out["ul_fp16_optimal_fusion"] = {"value": round(S * U * BITS / (ms * 1e-3) / 1e9, 4), "unit": "Gbps",
+                                     "ms_per_batch": round(ms, 5),
+                                     "kernel": eng.kernel_name(0, BC, U, 1),
+                                     "note": "Gram kernel with the variance fused (sweep operator on its Gram) + fusion"}
     eng.sync()
     return out
 

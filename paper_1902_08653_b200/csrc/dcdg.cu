@@ -388,6 +388,9 @@ const Spec kSpecs[] = {
 #ifndef DCDG_GRAM_MINB
 #define DCDG_GRAM_MINB 16
 #endif
+#ifndef DCDG_GRAM_SIG_MINB  // the variance-fused instance (optimal fusion)
+#define DCDG_GRAM_SIG_MINB 12  // 168 registers: no spills, 0.283 vs 0.289 ms at 16 warps (profiles/lab/README.md)
+#endif
 constexpr int kGramNpw = 4;
 
 bool gram_shape(int bc, int u, int fmt) { return fmt == DCDG_FP16 && bc == 32 && u == 16; }
@@ -405,7 +408,10 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-int launch_ul_gram(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X, cudaStream_t st) {
+// sigma2 != NULL: optimal fusion, post_eq_variance fused into the same kernel
+// (gam = E_x/N0, scale = E_x/U) from the Gram it already holds
+int launch_ul_gram(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X, cudaStream_t st,
+                   float* sigma2 = nullptr, float gam = 0.f, float scale = 0.f) {
   constexpr int U = 16, NPW = kGramNpw;
   using L = dcdg::GramSmem<U, NPW>;
   auto encode = tensor_map_encoder();
@@ -420,11 +426,20 @@ int launch_ul_gram(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, fl
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DCDG_ECUDA, "dcdg_ul_detect: tensor map encode failed (" + std::to_string(r) + ")");
-  auto kern = dcdg::ul_gram_f16<U, NPW, DCDG_GRAM_MINB>;
-  static const int occ = occupancy_of(kern, L::kAlloc, 32);
   const int nsets = (P + NPW - 1) / NPW;
-  const int blocks = std::min(nsets, ctx->sms * occ);
-  kern<<<blocks, 32, L::kAlloc, st>>>(map, static_cast<const __half2*>(Y), P, K, kappa, static_cast<__half2*>(X));
+  if (sigma2) {
+    auto kern = dcdg::ul_gram_f16<U, NPW, DCDG_GRAM_SIG_MINB, true>;
+    static const int occ = occupancy_of(kern, L::kAlloc, 32);
+    const int blocks = std::min(nsets, ctx->sms * occ);
+    kern<<<blocks, 32, L::kAlloc, st>>>(map, static_cast<const __half2*>(Y), P, K, kappa, static_cast<__half2*>(X),
+                                        sigma2, gam, scale, ctx->d_status);
+  } else {
+    auto kern = dcdg::ul_gram_f16<U, NPW, DCDG_GRAM_MINB, false>;
+    static const int occ = occupancy_of(kern, L::kAlloc, 32);
+    const int blocks = std::min(nsets, ctx->sms * occ);
+    kern<<<blocks, 32, L::kAlloc, st>>>(map, static_cast<const __half2*>(Y), P, K, kappa, static_cast<__half2*>(X),
+                                        nullptr, 0.f, 0.f, nullptr);
+  }
   CUDA_TRY(cudaGetLastError(), "ul_gram launch");
   return DCDG_OK;
 }
@@ -760,8 +775,11 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
 
   const float kappa = static_cast<float>(n0 / ex);
   const Spec* spec = find_spec(Bc, U, fmt);
-  if (ctx->fp16_alg == DCDG_ALG_GRAM && gram_shape(Bc, U, fmt)) {
-    if (int rc = launch_ul_gram(ctx, H, y, static_cast<int>(P), K, kappa, x_local, st)) return rc;
+  const bool gram = ctx->fp16_alg == DCDG_ALG_GRAM && gram_shape(Bc, U, fmt);
+  if (gram) {
+    if (int rc = launch_ul_gram(ctx, H, y, static_cast<int>(P), K, kappa, x_local, st, optimal ? sigma2 : nullptr,
+                                static_cast<float>(ex / n0), static_cast<float>(ex / U)))
+      return rc;
   } else if (spec) {
     CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, x_local, nullptr, st), "ul_detect launch");
   } else {
@@ -781,7 +799,7 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
     CUDA_TRY(cudaGetLastError(), "ul_generic launch");
   }
   ++ctx->launches;
-  if (optimal)
+  if (optimal && !gram)  // the Gram kernel computed sigma^2 itself
     if (int rc = launch_post_eq(ctx, H, static_cast<int>(P), Bc, U, n0, ex, fmt, sigma2, st)) return rc;
   if (xhat)
     if (int rc = launch_fuse(ctx, x_local, sigma2, S, C, C_total, U, fmt, optimal, xhat, wsum, st)) return rc;

@@ -200,10 +200,84 @@ __device__ __forceinline__ void gram_tc_phase(unsigned char* sm, uint32_t sbase,
   }
 }
 
-template <int U, int NPW, int MINB>
+// post_eq_variance of a problem from the Gram rows its 8 lanes hold
+// (detect.cpp:112-130): sigma^2 = (E_x/U) tr (I + (E_x/N0) G)^-1.  The
+// inverse's trace comes from the sweep operator in place on the lanes' rows
+// (lane k: rows 2k, 2k+1 of A = I + gam G): pivot kk in ascending order, its
+// row broadcast through shared memory,
+//     d = a_kk,kk;  a_ij -= (a_i,kk / d) a_kk,j  (i, j != kk);
+//     a_i,kk <- a_i,kk / d;  a_kk,j <- a_kk,j / d;  a_kk,kk <- -1/d,
+// after which A holds -A^-1.  The pivots are the Cholesky pivots of the
+// reference's hermitian_solve, so its singularity test (d > 1e-14 max A_jj,
+// numerics.cpp:38-41,55-56) applies unchanged.  Returns tr A^-1 (on every lane
+// of the problem); `singular` is set on the lanes that saw a failing pivot.
+template <int U>
+__device__ __forceinline__ float gram_trace_inverse(float (&ar0)[U], float (&ai0)[U], float (&ar1)[U],
+                                                    float (&ai1)[U], int k, float gam, float4* prow,
+                                                    bool& singular) {
+  // A = I + gam G in place over the Gram rows (they are dead after the sweeps)
+#pragma unroll
+  for (int j = 0; j < U; ++j) {
+    ar0[j] = fmaf(gam, ar0[j], j == 2 * k ? 1.f : 0.f);
+    ai0[j] *= gam;
+    ar1[j] = fmaf(gam, ar1[j], j == 2 * k + 1 ? 1.f : 0.f);
+    ai1[j] *= gam;
+  }
+  float dmax = 0.f;
+#pragma unroll
+  for (int jp = 0; jp < U / 2; ++jp)
+    if (k == jp) dmax = fmaxf(ar0[2 * jp], ar1[2 * jp + 1]);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  const float floor_ = 1e-14f * dmax;
+#pragma unroll
+  for (int kk = 0; kk < U; ++kk) {
+    float4* slot = prow + (kk & 1) * (U / 2);  // alternating [U/2] float4 rows (pairs of entries)
+    if (k == kk / 2) {
+      const float* rr = (kk & 1) ? ar1 : ar0;
+      const float* ri = (kk & 1) ? ai1 : ai0;
+#pragma unroll
+      for (int j = 0; j < U / 2; ++j) slot[j] = make_float4(rr[2 * j], ri[2 * j], rr[2 * j + 1], ri[2 * j + 1]);
+    }
+    __syncwarp();
+    const float d = reinterpret_cast<const float*>(slot)[2 * kk];
+    if (!(d > floor_)) singular = true;
+    const float inv = __frcp_rn(d);
+    const bool piv0 = (2 * k == kk), piv1 = (2 * k + 1 == kk);
+    // pivot row: a_kk,j - (1 - 1/d) a_kk,j = a_kk,j / d with the same update
+    const float f0r = piv0 ? 1.f - inv : ar0[kk] * inv, f0i = piv0 ? 0.f : ai0[kk] * inv;
+    const float f1r = piv1 ? 1.f - inv : ar1[kk] * inv, f1i = piv1 ? 0.f : ai1[kk] * inv;
+#pragma unroll
+    for (int jq = 0; jq < U / 2; ++jq) {
+      const float4 v = slot[jq];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 2 * jq + h;
+        if (j == kk) continue;
+        const float br = h ? v.z : v.x, bi = h ? v.w : v.y;
+        csub_mul(ar0[j], ai0[j], f0r, f0i, br, bi);
+        csub_mul(ar1[j], ai1[j], f1r, f1i, br, bi);
+      }
+    }
+    ar0[kk] = piv0 ? -inv : f0r;
+    ai0[kk] = piv0 ? 0.f : f0i;
+    ar1[kk] = piv1 ? -inv : f1r;
+    ai1[kk] = piv1 ? 0.f : f1i;
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int jp = 0; jp < U / 2; ++jp)
+    if (k == jp) t = -(ar0[2 * jp] + ar1[2 * jp + 1]);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+template <int U, int NPW, int MINB, bool SIG = false>
 __global__ void __launch_bounds__(32, MINB)
     ul_gram_f16(const __grid_constant__ CUtensorMap tmH, const __half2* __restrict__ Y, int P, int K, float kappa,
-                __half2* __restrict__ X) {
+                __half2* __restrict__ X, float* __restrict__ sigma2, float gam, float scale,
+                unsigned long long* __restrict__ status) {
   static_assert(NPW == 4, "a set is 4 problems of 8 sweep lanes");
   using L = GramSmem<U, NPW>;
   extern __shared__ unsigned char smem_raw[];
@@ -297,6 +371,19 @@ __global__ void __launch_bounds__(32, MINB)
       w.x = h2_as_u32(__floats2half2_rn(xr[0], xi[0]));
       w.y = h2_as_u32(__floats2half2_rn(xr[1], xi[1]));
       reinterpret_cast<uint2*>(X + static_cast<size_t>(p) * U)[k] = w;
+    }
+    if constexpr (SIG) {
+      // optimal fusion: sigma^2 from the same Gram (the transit buffer is free
+      // until the next set's tensor-core phase); rounded to the fp16 wire
+      // format as the reference rounds the messages (detect.cpp:170-173)
+      bool singular = false;
+      float4* prow = reinterpret_cast<float4*>(sm + L::kGOff) + q * U;
+      const float tr = gram_trace_inverse<U>(g0r, g0i, g1r, g1i, k, gam, prow, singular);
+      const unsigned sing = __ballot_sync(0xffffffffu, singular);
+      if (p < P && k == 0) {
+        sigma2[p] = __half2float(__float2half_rn(scale * tr));
+        if ((sing >> (8 * q)) & 0xffu) record_status(status, p, ST_SINGULAR, 0);
+      }
     }
     __syncwarp();
   }

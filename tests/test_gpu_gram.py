@@ -8,7 +8,7 @@ convergence against the exact L-MMSE solution of the stored fp16 inputs."""
 import numpy as np
 import pytest
 
-from helpers import FP16, FULL_STORAGE, TOL_FP16, UNIFORM, batch, qam_symbols, rel_err, to_dev, to_host
+from helpers import FP16, FULL_STORAGE, OPTIMAL, TOL_FP16, UNIFORM, batch, qam_symbols, rel_err, to_dev, to_host
 
 pytestmark = pytest.mark.gpu
 
@@ -189,3 +189,27 @@ def test_dl_gram_zero_beamformer(engine):
         _run_dl(engine, b, sym, "gram", 4.0)
     assert ei.value.problem == 1 * C
     engine.sync()
+
+
+@pytest.mark.parametrize("C,S", [(8, 48), (3, 7), (8, 1200)], ids=lambda v: str(v))
+def test_gram_optimal_fusion_fused_variance(engine, port, C, S):
+    """Optimal fusion on the Gram kernel: post_eq_variance (detect.cpp:112-130)
+    from the kernel's own Gram by the in-place sweep operator, fp16 wire
+    rounding of sigma^2, then the weighted fusion; against the fp64 reference,
+    its fp16 full-storage emulation, and the standalone variance kernel."""
+    U = 16
+    b = batch(C, 32, U, S=S, seed=31 + S)
+    xhat, local, s2 = port.ul_detect_batch(b["h_tiles"], b["y"], b["n0"], 1.0, 3, OPTIMAL)
+    xhat16, _, s216 = port.ul_detect_batch(b["h_tiles"], b["y"], b["n0"], 1.0, 3, OPTIMAL, FP16, FULL_STORAGE)
+    H16 = to_dev(b["h_tiles"], "fp16", True)
+    r = engine.ul_detect(H16, to_dev(b["y"], "fp16", True), n0=b["n0"], K=3, fusion="optimal")
+    engine.sync()
+    assert engine.kernel_name(0, 32, 16, 1).startswith("ul_gram_f16")
+    got = r.sigma2.cpu().numpy()
+    assert np.max(np.abs(got - s2) / s2) <= TOL_FP16
+    assert np.max(np.abs(got - s216) / s216) <= TOL_FP16
+    standalone = engine.post_eq_variance(H16, n0=b["n0"]).cpu().numpy()
+    assert np.max(np.abs(got - standalone) / standalone) <= 2e-3  # both on the fp16 grid
+    assert rel_err(to_host(r.xhat), xhat) <= TOL_FP16
+    assert rel_err(to_host(r.xhat), xhat16) <= TOL_FP16
+    assert rel_err(to_host(r.x_local), local) <= TOL_FP16

@@ -31,6 +31,7 @@ def _single(engine, H, y, *, fusion, n0):
     ((8, 32, 16), "fp32", "uniform"),   # fused epilogue (ul_reg_f32)
     ((8, 32, 16), "fp16", "uniform"),   # fused epilogue (ul_reg_f16)
     ((8, 32, 16), "fp32", "optimal"),   # CD + variances, then xchg_put_kernel
+    ((8, 32, 16), "fp16", "optimal"),   # Gram kernel with fused variances, then xchg_put_kernel
     ((2, 256, 16), "fp32", "uniform"),  # multi-warp kernel: xchg_put_kernel path
     ((3, 24, 6), "fp32", "uniform"),    # generic kernel
 ])
