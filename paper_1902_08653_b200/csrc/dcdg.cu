@@ -389,7 +389,7 @@ const Spec kSpecs[] = {
 #define DCDG_GRAM_MINB 16
 #endif
 #ifndef DCDG_GRAM_SIG_MINB  // the variance-fused instance (optimal fusion)
-#define DCDG_GRAM_SIG_MINB 12  // 168 registers: no spills, 0.283 vs 0.289 ms at 16 warps (profiles/lab/README.md)
+#define DCDG_GRAM_SIG_MINB 12  // 168 registers (30 spilled loop invariants), 0.283 vs 0.289 ms at 16 warps (profiles/lab/README.md)
 #endif
 constexpr int kGramNpw = 4;
 

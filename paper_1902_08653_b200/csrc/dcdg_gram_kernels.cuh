@@ -234,10 +234,10 @@ __device__ __forceinline__ float gram_trace_inverse(float (&ar0)[U], float (&ai0
   for (int kk = 0; kk < U; ++kk) {
     float4* slot = prow + (kk & 1) * (U / 2);  // alternating [U/2] float4 rows (pairs of entries)
     if (k == kk / 2) {
-      const float* rr = (kk & 1) ? ar1 : ar0;
-      const float* ri = (kk & 1) ? ai1 : ai0;
 #pragma unroll
-      for (int j = 0; j < U / 2; ++j) slot[j] = make_float4(rr[2 * j], ri[2 * j], rr[2 * j + 1], ri[2 * j + 1]);
+      for (int j = 0; j < U / 2; ++j)
+        slot[j] = (kk & 1) ? make_float4(ar1[2 * j], ai1[2 * j], ar1[2 * j + 1], ai1[2 * j + 1])
+                           : make_float4(ar0[2 * j], ai0[2 * j], ar0[2 * j + 1], ai0[2 * j + 1]);
     }
     __syncwarp();
     const float d = reinterpret_cast<const float*>(slot)[2 * kk];
