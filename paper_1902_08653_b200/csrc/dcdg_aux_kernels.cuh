@@ -507,6 +507,9 @@ __global__ void __launch_bounds__(128) gram_chol(const T* __restrict__ H, int P,
 // half).  gram_chol's factorisation keeps half the warp idle at U = 16; here
 // every lane works, so the scalar Cholesky/inverse stream serves two problems.
 // ===========================================================================
+#ifndef DCDG_PEV_SWEEP  // factorisation: 1 = sweep operator, 0 = Cholesky + triangular inverse
+#define DCDG_PEV_SWEEP 0  // lab switch: the sweep operator measured slower here (profiles/lab/README.md)
+#endif
 #ifndef DCDG_PEV_TRI  // lower-triangle-only Gram (lab switch: measured slower for fp32, see below)
 #define DCDG_PEV_TRI 0
 #endif
@@ -682,6 +685,63 @@ __global__ void __launch_bounds__(128) pev16_pair_kernel(const T* __restrict__ H
   }
 #endif
   __syncwarp();  // the staged tiles are dead from here: Lr reuses their space
+#if DCDG_PEV_SWEEP
+  // ---- tr A^-1 by the sweep operator, half-warp h = problem p0 + h, lane i =
+  // row i of A (full Hermitian row, upper part conj of the stored lower part).
+  // Pivot kk in ascending order, its row broadcast through shared memory as
+  // (a_kk,j, i a_kk,j) pairs:  d = a_kk,kk;  a_ij -= (a_i,kk / d) a_kk,j;
+  // a_i,kk <- a_i,kk / d;  a_kk,j <- a_kk,j / d;  a_kk,kk <- -1/d.  After the
+  // 16 pivots the rows hold -A^-1.  The pivots are the Cholesky pivots of
+  // hermitian_solve, so the reference's singularity test applies unchanged
+  // (numerics.cpp:38-41,55-56); every update is independent (no dot-product
+  // chains), two FFMA2 per complex update.
+  const int hf = lane >> 4, i = lane & 15;
+  const float2* Ah = A + hf * N * N;
+  float4* prow = reinterpret_cast<float4*>(Lr) + hf * 2 * N;  // 2 alternating rows of N (a, i a) pairs
+  float2 a[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const float2 v = (j <= i) ? Ah[j * N + i] : Ah[i * N + j];
+    a[j] = (j <= i) ? v : make_float2(v.x, -v.y);
+  }
+  float maxdiag = 0.f;
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+    if (i == j) maxdiag = fabsf(a[j].x);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) maxdiag = fmaxf(maxdiag, __shfl_xor_sync(0xffffffffu, maxdiag, o));
+  const float floor_ = 1e-14f * maxdiag;  // numerics.cpp:38-41,55-56
+  bool singular = false;
+  __syncwarp();  // every lane has its row: the staged tiles' space now carries the pivot rows
+#pragma unroll
+  for (int kk = 0; kk < N; ++kk) {
+    float4* slot = prow + (kk & 1) * N;
+    if (i == kk) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) slot[j] = make_float4(a[j].x, a[j].y, -a[j].y, a[j].x);
+    }
+    __syncwarp();
+    const float d = slot[kk].x;
+    if (!(d > floor_)) singular = true;
+    const float inv = __frcp_rn(d);
+    const bool piv = (i == kk);
+    const float2 f = piv ? make_float2(1.f - inv, 0.f) : fmul2(inv, a[kk]);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      if (j == kk) continue;
+      const float4 v = slot[j];
+      a[j] = ffma2(-f.x, make_float2(v.x, v.y), a[j]);
+      a[j] = ffma2(-f.y, make_float2(v.z, v.w), a[j]);
+    }
+    a[kk] = piv ? make_float2(-inv, 0.f) : f;
+  }
+  float tr = 0.f;
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+    if (i == j) tr = -a[j].x;
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+#else
   // ---- factorisation, half-warp h = problem p0 + h, lane i = row i
   const int hf = lane >> 4, i = lane & 15;
   const float2* Ah = A + hf * N * N;
@@ -752,6 +812,7 @@ __global__ void __launch_bounds__(128) pev16_pair_kernel(const T* __restrict__ H
   }
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+#endif
   const unsigned sing = __ballot_sync(0xffffffffu, singular);
   const long long p = p0 + hf;
   if (i == 0 && p < P) {
