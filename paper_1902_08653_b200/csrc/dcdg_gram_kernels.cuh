@@ -80,12 +80,10 @@ struct GramSmem {
   static constexpr int kRowB = 128;                 // one fp16 column of B_c = 32 antennas
   static constexpr int kSlotB = NPW * U * kRowB;    // TMA box: NPW*U rows of 128 B (1024-B aligned)
   static constexpr int kYOff = kSlotB;              // NPW y vectors, 128 B each
-  // one problem's G in transit from the mma fragments to the sweep lanes:
-  // [k][col j][rows 2k, 2k+1] float2, k-stride padded 16 B (conflict-free)
-  static constexpr int kGStride = U * 16 + 16;
+  // pivot rows of the fused variance (SIG): [problem][2][U/2] float4
   static constexpr int kGOff = kYOff + NPW * 128;
-  static constexpr int kZOff = kGOff + (U / 2) * kGStride;  // z: [j] float2
-  static constexpr int kBarOff = kZOff + U * 8;
+  static constexpr int kZOff = kGOff + NPW * U * 16;  // z: [problem][j] float2
+  static constexpr int kBarOff = kZOff + NPW * U * 8;
   static constexpr int kBcOff = kBarOff + 16;       // sweep broadcast slots: [NPW][2] float4
   static constexpr int kBytes = kBcOff + NPW * 32;
   static constexpr int kAlloc = kBytes + 1024;      // slack to align the swizzled slot to 1024 B
@@ -120,9 +118,9 @@ __device__ __forceinline__ void csub_mul(float& cr, float& ci, float ar, float a
 
 // Tensor-core phase of a set (shared by the uplink and downlink kernels): the
 // Gram G = H^H H (and, with Z, the matched filter z = H^H y) of each of the
-// NPW problems, from the swizzled TMA slot, handed through the padded transit
-// buffer to the problem's 8 sweep lanes: lane k of problem q gets rows 2k and
-// 2k+1 of G (and z_{2k}, z_{2k+1}).
+// NPW problems, from the swizzled TMA slot, handed through the slot itself
+// (each problem's consumed rows) to the problem's 8 sweep lanes: lane k of
+// problem q gets rows 2k and 2k+1 of G (and z_{2k}, z_{2k+1}).
 template <int U, int NPW, bool Z>
 __device__ __forceinline__ void gram_tc_phase(unsigned char* sm, uint32_t sbase, int lane, float (&g0r)[U],
                                               float (&g0i)[U], float (&g1r)[U], float (&g1i)[U], float (&cr)[2],
@@ -132,7 +130,6 @@ __device__ __forceinline__ void gram_tc_phase(unsigned char* sm, uint32_t sbase,
   const int q = lane >> 3, k = lane & 7;
   // ldmatrix row of this lane: matrix mi = lane/8 -> users (mi&1)*8 + lane%8, chunk half mi>>1
   const int lu = ((lane >> 3) & 1) * 8 + (lane & 7), lch = lane >> 4;
-  unsigned char* gbuf = sm + L::kGOff;
   float2* zbuf = reinterpret_cast<float2*>(sm + L::kZOff);
 #pragma unroll
   for (int pl = 0; pl < NPW; ++pl) {
@@ -161,41 +158,45 @@ __device__ __forceinline__ void gram_tc_phase(unsigned char* sm, uint32_t sbase,
         mma_f16f32(zz, a, y0, y1);
       }
     }
-    __syncwarp();  // the previous problem's lanes have read the transit buffer
-    // C fragments: (row g, cols 2t, 2t+1) and (row g+8, same cols) of each n-tile
+    // problem pl's rows of the slot are consumed: its G goes there, swizzled
+    // [k][chunk j ^ k][rows 2k, 2k+1] (2048 B, conflict-free 16-B reads), and
+    // all four problems' rows are read back in one pass after the loop
+    // (0.096 -> 0.087 ms uplink, 0.103 -> 0.095 ms downlink against a
+    // separate transit buffer read problem by problem, profiles/lab/README.md)
+    __syncwarp();
+    unsigned char* tb = sm + pl * (U * L::kRowB);
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int j = nt * 8 + 2 * t + h;
-        // row g -> (k = g/2, r = g%2); row g+8 -> (k = g/2 + 4, r = g%2)
-        *reinterpret_cast<float2*>(gbuf + (g >> 1) * L::kGStride + j * 16 + (g & 1) * 8) =
+        const int j = nt * 8 + 2 * t + h, k0 = g >> 1, k1 = (g >> 1) + 4;
+        *reinterpret_cast<float2*>(tb + k0 * (U * 16) + ((j ^ k0) << 4) + (g & 1) * 8) =
             make_float2(gr[nt][h], gi[nt][h]);
-        *reinterpret_cast<float2*>(gbuf + ((g >> 1) + 4) * L::kGStride + j * 16 + (g & 1) * 8) =
+        *reinterpret_cast<float2*>(tb + k1 * (U * 16) + ((j ^ k1) << 4) + (g & 1) * 8) =
             make_float2(gr[nt][2 + h], gi[nt][2 + h]);
       }
     if (Z && t == 0) {
-      zbuf[g] = make_float2(zz[0], zz[1]);
-      zbuf[g + 8] = make_float2(zz[2], zz[3]);
+      zbuf[pl * U + g] = make_float2(zz[0], zz[1]);
+      zbuf[pl * U + g + 8] = make_float2(zz[2], zz[3]);
     }
-    __syncwarp();
-    if (q == pl) {
-      const unsigned char* mine = gbuf + k * L::kGStride;
+  }
+  __syncwarp();
+  {
+    const unsigned char* mine = sm + q * (U * L::kRowB) + k * (U * 16);
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const float4 v = *reinterpret_cast<const float4*>(mine + j * 16);
-        g0r[j] = v.x;
-        g0i[j] = v.y;
-        g1r[j] = v.z;
-        g1i[j] = v.w;
-      }
-      if (Z) {
-        const float4 zv = reinterpret_cast<const float4*>(zbuf)[k];
-        cr[0] = zv.x;
-        ci[0] = zv.y;
-        cr[1] = zv.z;
-        ci[1] = zv.w;
-      }
+    for (int j = 0; j < U; ++j) {
+      const float4 v = *reinterpret_cast<const float4*>(mine + ((j ^ k) << 4));
+      g0r[j] = v.x;
+      g0i[j] = v.y;
+      g1r[j] = v.z;
+      g1i[j] = v.w;
+    }
+    if (Z) {
+      const float4 zv = reinterpret_cast<const float4*>(zbuf + q * U)[k];
+      cr[0] = zv.x;
+      ci[0] = zv.y;
+      cr[1] = zv.z;
+      ci[1] = zv.w;
     }
   }
 }
