@@ -530,7 +530,9 @@ __global__ void __launch_bounds__(32, MINB)
     // ---------------- x = H a: lane k forms antennas 4k..4k+3 (its 16-B chunk of every column)
     abuf[q * (U / 2) + k] = make_float4(ar[0], ai[0], ar[1], ai[1]);
     __syncwarp();
-    float xr[4] = {0.f, 0.f, 0.f, 0.f}, xi[4] = {0.f, 0.f, 0.f, 0.f};
+    // antenna pairs (4k, 4k+1) and (4k+2, 4k+3) as packed fp32x2: the row-pair
+    // planar tile words convert straight into FFMA2 operands
+    float2 xr2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}, xi2[2] = {xr2[0], xr2[0]};
     if (p < P) {
       const unsigned char* hp = reinterpret_cast<const unsigned char*>(H) + static_cast<size_t>(p) * U * BC * 4 + k * 16;
       uint4 hv[U];
@@ -544,17 +546,17 @@ __global__ void __launch_bounds__(32, MINB)
         for (int h = 0; h < 2; ++h) {
           const uint4 v = hv[2 * u2 + h];
           const float aR = h ? av.z : av.x, aI = h ? av.w : av.y;
-          const float2 re01 = __half22float2(u32_as_h2(v.x)), im01 = __half22float2(u32_as_h2(v.y));
-          const float2 re23 = __half22float2(u32_as_h2(v.z)), im23 = __half22float2(u32_as_h2(v.w));
-          const float hr[4] = {re01.x, re01.y, re23.x, re23.y}, hi[4] = {im01.x, im01.y, im23.x, im23.y};
+          const float2 hr[2] = {__half22float2(u32_as_h2(v.x)), __half22float2(u32_as_h2(v.z))};
+          const float2 hi[2] = {__half22float2(u32_as_h2(v.y)), __half22float2(u32_as_h2(v.w))};
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            xr[b] = fmaf(hr[b], aR, fmaf(-hi[b], aI, xr[b]));
-            xi[b] = fmaf(hr[b], aI, fmaf(hi[b], aR, xi[b]));
+          for (int b = 0; b < 2; ++b) {  // x += h a: (hr ar - hi ai, hr ai + hi ar)
+            xr2[b] = ffma2(aR, hr[b], ffma2(-aI, hi[b], xr2[b]));
+            xi2[b] = ffma2(aI, hr[b], ffma2(aR, hi[b], xi2[b]));
           }
         }
       }
     }
+    const float xr[4] = {xr2[0].x, xr2[0].y, xr2[1].x, xr2[1].y}, xi[4] = {xi2[0].x, xi2[0].y, xi2[1].x, xi2[1].y};
     float en = 0.f;
 #pragma unroll
     for (int b = 0; b < 4; ++b) en = fmaf(xr[b], xr[b], fmaf(xi[b], xi[b], en));
