@@ -90,12 +90,14 @@ struct GramSmem {
 };
 
 #ifndef DCDG_GRAM_SMEM_BCAST
-#define DCDG_GRAM_SMEM_BCAST 1
+#define DCDG_GRAM_SMEM_BCAST 0
 #endif
 // The pair's two updates from its owner lane (base + jp) to the problem's 8
-// lanes: one 16-B store by the owner into an alternating shared-memory slot
-// and one 16-B broadcast load (default; 0.8-1.2% faster than the four
-// shuffles of DCDG_GRAM_SMEM_BCAST=0, profiles/lab/README.md).
+// lanes: four shuffles (default), or (DCDG_GRAM_SMEM_BCAST=1) one 16-B store
+// by the owner into an alternating shared-memory slot and one 16-B broadcast
+// load.  The slot won by ~1% while the Gram rows went through a separate
+// transit buffer; with the slot transit the shuffles win by 1-2%
+// (profiles/lab/README.md).
 __device__ __forceinline__ float4 pair_bcast(float4 v, int JP, int k, int base, float4* slots) {
 #if DCDG_GRAM_SMEM_BCAST
   float4* sl = slots + (JP & 1);
