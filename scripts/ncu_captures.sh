@@ -1,11 +1,11 @@
 #!/bin/bash
 # Full ncu captures of the hot kernels at the north-star shape, summarised on the
 # box (gpurun_out/ncu_summary.json + the variance kernel stall page).
-mkdir -p /tmp/reps
+rm -rf /tmp/reps; mkdir -p /tmp/reps  # a reused box keeps /tmp: never summarise a stale report
 args=""
 for k in "ul fp32 4480" "dl fp32 4480" "ul fp16 2240" "dl fp16 2240" "pev fp32 4096"; do
   set -- $k
-  timeout 300 ncu --set full --clock-control none --import-source on -k regex:"reg_f|gram_f16|gram_chol|pev16" -s 2 -c 1 \
+  timeout 300 ncu -f --set full --clock-control none --import-source on -k regex:"reg_f|gram_f16|gram_chol|pev16" -s 2 -c 1 \
     -o /tmp/reps/full_$1_$2 python scripts/prof_kernel.py $1 $2 4 > /dev/null 2>&1
   args="$args ${1}_${2}_32_16=/tmp/reps/full_$1_$2.ncu-rep:134400:$3"
 done

@@ -1,6 +1,6 @@
-mkdir -p /tmp/reps
+rm -rf /tmp/reps; mkdir -p /tmp/reps  # a reused box keeps /tmp: never summarise a stale report
 for d in ul dl; do
-  timeout 300 ncu --set full --clock-control none --import-source on -k regex:"gram_f16" -s 2 -c 1 \
+  timeout 300 ncu -f --set full --clock-control none --import-source on -k regex:"gram_f16" -s 2 -c 1 \
     -o /tmp/reps/full_${d}_gram python scripts/prof_kernel.py $d fp16 4 > /dev/null 2>&1
   ncu -i /tmp/reps/full_${d}_gram.ncu-rep --page source --csv --print-source sass > /tmp/reps/${d}.csv 2>/dev/null
   python scripts/stall_summary.py /tmp/reps/${d}.csv > gpurun_out/stalls_${d}_gram.txt 2>&1
