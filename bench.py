@@ -108,16 +108,16 @@ class ClockSampler:
 # synthetic inputs (device-side, torch RNG; same distribution as the
 # reference's make_batch: H ~ CN(0,1), Gray 16-QAM at unit energy, AWGN N0)
 # ---------------------------------------------------------------------------
-def make_inputs(S, c_local, device, seed):
+def make_inputs(S, c_local, device, seed, u=U, bc=BC):
     import torch
     g = torch.Generator(device=device)
     g.manual_seed(seed)
-    n0 = U * 1.0 / 10 ** (SNR_DB / 10)
-    H = torch.randn((S, c_local, U, BC), dtype=torch.complex64, device=device, generator=g)  # CN(0,1)
+    n0 = u * 1.0 / 10 ** (SNR_DB / 10)
+    H = torch.randn((S, c_local, u, bc), dtype=torch.complex64, device=device, generator=g)  # CN(0,1)
     lv = torch.tensor([-3.0, -1.0, 1.0, 3.0], device=device) / math.sqrt(10.0)
-    idx = torch.randint(0, 4, (S, U, 2), device=device, generator=g)
+    idx = torch.randint(0, 4, (S, u, 2), device=device, generator=g)
     x = torch.complex(lv[idx[..., 0]], lv[idx[..., 1]])
-    noise = torch.randn((S, c_local, BC), dtype=torch.complex64, device=device, generator=g) * math.sqrt(n0)
+    noise = torch.randn((S, c_local, bc), dtype=torch.complex64, device=device, generator=g) * math.sqrt(n0)
     y = torch.einsum("scub,su->scb", H, x) + noise
     return H.contiguous(), y.contiguous(), x.contiguous(), n0
 
@@ -209,6 +209,141 @@ def secondary_lines(eng, dev, S, reps, hbm):
     return out
 
 
+def measure_e2e(eng, dcd, part, H, y, n0, fusion, world, dev, n_e2e, barrier):
+    """The metric end to end through the public API (Engine.ul_detect -> C ABI
+    dcdg_ul_detect, or DistributedCD.uplink at N>1): pinned host H, y -> device
+    in chunks on a copy stream overlapped with detection on a compute stream ->
+    host fused estimates, every step; plus the copy-only time of the same bytes
+    (the PCIe bound of the step)."""
+    import torch
+    import torch.distributed as dist
+    Hh = H.cpu().pin_memory()
+    yh = y.cpu().pin_memory()
+    Hd, yd = torch.empty_like(H), torch.empty_like(y)
+    n_chunks = 8 if (world == 1 and part.S_local % 8 == 0) else 1
+    cs = part.S_local // n_chunks
+    copy_st, comp_st = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    own = part.own_hi - part.own_lo
+    xh_host = torch.empty((own, U), dtype=torch.complex64).pin_memory()
+
+    def copies():
+        evs = []
+        for i in range(n_chunks):
+            with torch.cuda.stream(copy_st):
+                Hd[i * cs:(i + 1) * cs].copy_(Hh[i * cs:(i + 1) * cs], non_blocking=True)
+                yd[i * cs:(i + 1) * cs].copy_(yh[i * cs:(i + 1) * cs], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_st)
+                evs.append(ev)
+        return evs
+
+    def e2e_step():
+        evs = copies()
+        with torch.cuda.stream(comp_st):
+            if world == 1:
+                for i in range(n_chunks):
+                    comp_st.wait_event(evs[i])
+                    r = eng.ul_detect(Hd[i * cs:(i + 1) * cs], yd[i * cs:(i + 1) * cs], n0=n0, K=K_SWEEPS,
+                                      fusion=fusion, want_local=False, stream=comp_st)
+                    xh_host[i * cs:(i + 1) * cs].copy_(r.xhat, non_blocking=True)
+            else:
+                comp_st.wait_event(evs[-1])
+                out = dcd.uplink(Hd, yd, n0=n0, K=K_SWEEPS, fusion=fusion)
+                xh_host.copy_(out, non_blocking=True)
+
+    e2e_step()
+    barrier()
+    t0, t1 = _ev(), _ev()
+    torch.cuda.synchronize(dev)
+    t0.record(copy_st)
+    for _ in range(n_e2e):
+        e2e_step()
+        comp_st.synchronize()  # the host consumes this step's estimates
+    t1.record(comp_st)
+    barrier()
+    e_ms = t0.elapsed_time(t1) / n_e2e
+    if world > 1:
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    h2d = H.numel() * H.element_size() + y.numel() * y.element_size()
+    copies()
+    torch.cuda.synchronize(dev)
+    c0, c1 = _ev(), _ev()
+    c0.record(copy_st)
+    for _ in range(n_e2e):
+        copies()
+    c1.record(copy_st)
+    torch.cuda.synchronize(dev)
+    c_ms = c0.elapsed_time(c1) / n_e2e
+    S_total = part.S
+    return {"value": round(S_total * U * BITS / (e_ms * 1e-3) / 1e9, 5), "unit": "Gbps", "ms_per_step": round(e_ms, 4),
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(own * U * 8),
+            "h2d_copy_only_ms": round(c_ms, 4), "h2d_GBps": round(h2d / (c_ms * 1e-3) / 1e9, 2),
+            "frac_of_copy_bound": round(c_ms / e_ms, 4),
+            "path": "Engine.ul_detect (C ABI dcdg_ul_detect): pinned host H,y -> device in %d chunks on a copy "
+                    "stream overlapped with detection -> host fused estimates" % n_chunks}
+
+
+PARITY_S = 96  # subcarriers of the bench batch re-checked against the reference after timing
+
+
+def parity_check(eng, H, y, n0, fusion):
+    """Outside every timed region: the fused estimates of the first PARITY_S
+    subcarriers of the bench's own batch against the reference's
+    decentralized_cd_detect (oracle/_ref, fp64) on the same values — the
+    checker, never the measured path.  north_star tolerance 1e-5 (fp32)."""
+    S = min(PARITY_S, H.shape[0])
+    if _ref_lib() is None:
+        return {"checked_subcarriers": 0, "note": "oracle/_ref/libdcdref.so missing"}
+    r = eng.ul_detect(H[:S].contiguous(), y[:S].contiguous(), n0=n0, K=K_SWEEPS, fusion=fusion, want_local=False)
+    got = r.xhat.cpu().numpy().astype(np.complex128)
+    Hn = H[:S].cpu().numpy().astype(np.complex128)
+    yn = y[:S].cpu().numpy().astype(np.complex128)
+    c, u, bc = Hn.shape[1], Hn.shape[2], Hn.shape[3]
+    ref = RefCPU(S, arrays=(Hn, yn, n0), c=c, u=u, bc=bc)
+    want = np.zeros((S, u), np.complex128)
+    try:
+        ref.run(S, os.cpu_count() or 1, fusion=fusion, out=want)
+    finally:
+        ref.close()
+    err = np.linalg.norm(got - want, axis=1) / np.maximum(np.linalg.norm(want, axis=1), 1e-300)
+    worst = float(err.max())
+    return {"checked_subcarriers": S, "max_rel_err": worst, "tol": 1e-5, "ok": bool(worst <= 1e-5),
+            "against": "the reference's decentralized_cd_detect (oracle/_ref, fp64) on the bench's own first "
+                       f"{S} subcarriers ({fusion} fusion), run after the timed regions"}
+
+
+def configs0_line(eng, dev, hbm, reps):
+    """BASELINE.json configs[0] (the reference's CPU-runnable case): uplink
+    B=64, U=8, C=2 (B_c=32), 16-QAM, K=3, 1200x14 subcarrier-symbols; the GPU
+    kernels next to the reference's decentralized_cd_detect on this host."""
+    import torch
+    u0, c0, bc0, S = 8, 2, 32, S_PER_GPU
+    H, y, _, n0 = make_inputs(S, c0, dev, 77, u=u0, bc=bc0)
+    st = torch.cuda.current_stream(dev)
+    fn = lambda: eng.ul_detect(H, y, n0=n0, K=K_SWEEPS, fusion="uniform")  # noqa: E731
+    kfn = lambda: eng.ul_detect(H, y, n0=n0, K=K_SWEEPS, want_xhat=False)  # noqa: E731
+    for _ in range(3):
+        fn()
+        kfn()
+    ms = _time_stream(fn, st, reps)
+    kms = _time_stream(kfn, st, reps)
+    ach = S * c0 * alg_bytes_per_problem(bc0, u0, 8) / (kms * 1e-3) / 1e9
+    out = {"workload": "configs[0]: uplink CD B=64 U=8 C=2 (B_c=32), 16-QAM, K=3, 16,800 subcarrier-symbols, fp32, "
+                       "uniform fusion", "value": round(S * u0 * BITS / (ms * 1e-3) / 1e9, 4), "unit": "Gbps",
+           "ms_per_batch": round(ms, 5), "kernel_ms": round(kms, 5), "roofline_frac": round(ach / hbm, 4),
+           "kernel": eng.kernel_name(0, bc0, u0, 0)}
+    if _ref_lib() is not None:
+        threads = os.cpu_count() or 1
+        ref = RefCPU(2400, c=c0, u=u0, bc=bc0)
+        try:
+            out["reference_cpu"] = dict(_timed_mode(ref, threads, 2.0), kind="reference", cpu_model=cpu_model())
+        finally:
+            ref.close()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -224,6 +359,9 @@ def run_ours(args):
     one_gpu = os.environ.get("BENCH_ONE_GPU") == "1"
     if one_gpu:
         local_rank = 0
+    elif world > torch.cuda.device_count():
+        raise SystemExit(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPU(s); one rank per GPU "
+                         f"(BENCH_ONE_GPU=1 runs every rank on cuda:0 as a harness self-test only)")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
@@ -378,81 +516,22 @@ def run_ours(args):
     alg = P * alg_bytes_per_problem(BC, U, esz)
     achieved = alg / (k_ms * 1e-3) / 1e9
 
-    # e2e through the public API: pinned host H, y -> device (copy stream,
-    # chunked) overlapped with detection (compute stream) -> host estimates
-    Hh = H.cpu().pin_memory()
-    yh = y.cpu().pin_memory()
-    Hd, yd = torch.empty_like(H), torch.empty_like(y)
-    n_chunks = 8 if (world == 1 and part.S_local % 8 == 0) else 1
-    cs = part.S_local // n_chunks
-    copy_st, comp_st = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    own = part.own_hi - part.own_lo
-    xh_host = torch.empty((own, U), dtype=torch.complex64).pin_memory()
-
-    def e2e_step():
-        evs = []
-        for i in range(n_chunks):
-            with torch.cuda.stream(copy_st):
-                Hd[i * cs:(i + 1) * cs].copy_(Hh[i * cs:(i + 1) * cs], non_blocking=True)
-                yd[i * cs:(i + 1) * cs].copy_(yh[i * cs:(i + 1) * cs], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy_st)
-                evs.append(ev)
-        with torch.cuda.stream(comp_st):
-            if world == 1:
-                for i in range(n_chunks):
-                    comp_st.wait_event(evs[i])
-                    r = eng.ul_detect(Hd[i * cs:(i + 1) * cs], yd[i * cs:(i + 1) * cs], n0=n0, K=K_SWEEPS,
-                                      fusion=args.fusion, want_local=False, stream=comp_st)
-                    xh_host[i * cs:(i + 1) * cs].copy_(r.xhat, non_blocking=True)
-            else:
-                comp_st.wait_event(evs[-1])
-                out = dcd.uplink(Hd, yd, n0=n0, K=K_SWEEPS, fusion=args.fusion)
-                xh_host.copy_(out, non_blocking=True)
-
-    e2e_step()
-    barrier()
     n_e2e = max(2, min(args.steps, 5))
-    t0, t1 = _ev(), _ev()
-    torch.cuda.synchronize(dev)
-    t0.record(copy_st)
-    for _ in range(n_e2e):
-        e2e_step()
-        comp_st.synchronize()  # the host consumes this step's estimates
-    t1.record(comp_st)
-    barrier()
-    e_ms = t0.elapsed_time(t1) / n_e2e
-    if world > 1:
-        t = torch.tensor([e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t.item())
-    h2d = H.numel() * H.element_size() + y.numel() * y.element_size()
-
-    # the same host->device bytes with no compute: the PCIe bound of the e2e step
-    def copy_only():
-        for i in range(n_chunks):
-            with torch.cuda.stream(copy_st):
-                Hd[i * cs:(i + 1) * cs].copy_(Hh[i * cs:(i + 1) * cs], non_blocking=True)
-                yd[i * cs:(i + 1) * cs].copy_(yh[i * cs:(i + 1) * cs], non_blocking=True)
-    copy_only()
-    torch.cuda.synchronize(dev)
-    c0, c1 = _ev(), _ev()
-    c0.record(copy_st)
-    for _ in range(n_e2e):
-        copy_only()
-    c1.record(copy_st)
-    torch.cuda.synchronize(dev)
-    c_ms = c0.elapsed_time(c1) / n_e2e
-    e2e = {"value": round(S_total * U * BITS / (e_ms * 1e-3) / 1e9, 5), "unit": "Gbps", "ms_per_step": round(e_ms, 4),
-           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(own * U * 8),
-           "h2d_copy_only_ms": round(c_ms, 4), "h2d_GBps": round(h2d / (c_ms * 1e-3) / 1e9, 2),
-           "frac_of_copy_bound": round(c_ms / e_ms, 4),
-           "path": "Engine.ul_detect (C ABI dcdg_ul_detect): pinned host H,y -> device in %d chunks on a copy "
-                   "stream overlapped with detection -> host fused estimates" % n_chunks}
+    e2e = measure_e2e(eng, dcd, part, H, y, n0, args.fusion, world, dev, n_e2e, barrier)
+    h2d = e2e["h2d_bytes_per_step"]
 
     extra = None
     if rank == 0 and world == 1 and not args.fast:
         extra = secondary_lines(eng, dev, args.S, max(5, args.steps // 2), hbm)
+        if fmt == "fp32":
+            # the same e2e step with binary16 host buffers (half the PCIe bytes),
+            # through the default fp16 kernel
+            eng.set_fp16_algorithm("gram")
+            e16 = measure_e2e(eng, None, part, to_fp16_pairs(H), to_fp16_pairs(y), n0, args.fusion, world, dev,
+                              n_e2e, barrier)
+            e16["kernel"] = kernel_name("ul", BC, U, "fp16")
+            extra["e2e_fp16"] = e16
+        extra["configs0"] = configs0_line(eng, dev, hbm, max(5, args.steps // 2))
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -497,6 +576,12 @@ def run_ours(args):
         "clocks": clk.summary(),
         "interconnect": interconnect,
     }
+    if world > 1:
+        # False: the fused peer-memory exchange could not run and the line was
+        # measured with the NCCL reduce-scatter exchange instead
+        line["p2p_ok"] = p2p_error is None and mode_used == "p2p"
+        if one_gpu:
+            line["harness_self_test"] = "BENCH_ONE_GPU=1: all ranks share cuda:0; not scaling data"
     if p2p_error:
         line["p2p_error"] = p2p_error
     if compare:
@@ -507,6 +592,8 @@ def run_ours(args):
         line["extra"] = extra
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    if rank == 0 and fmt == "fp32":
+        line["parity"] = parity_check(eng, H, y, n0, args.fusion)
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
@@ -522,54 +609,133 @@ def _ref_lib():
     return Oracle("reference")
 
 
-def cpu_inputs(S, seed=5):
-    rng = np.random.default_rng(seed)
-    n0 = U * 1.0 / 10 ** (SNR_DB / 10)
-    H = (rng.standard_normal((S, C, U, BC)) + 1j * rng.standard_normal((S, C, U, BC))) / math.sqrt(2)
-    lv = np.array([-3.0, -1.0, 1.0, 3.0]) / math.sqrt(10.0)
-    x = lv[rng.integers(0, 4, (S, U))] + 1j * lv[rng.integers(0, 4, (S, U))]
-    y = np.einsum("scub,su->scb", H, x) + math.sqrt(n0 / 2) * (
-        rng.standard_normal((S, C, BC)) + 1j * rng.standard_normal((S, C, BC)))
-    return np.ascontiguousarray(H), np.ascontiguousarray(y), n0
-
-
-def cpu_time_ref(S, threads, reps=1):
-    import ctypes as Ct
-    o = _ref_lib()
-    H, y, n0 = cpu_inputs(S)
-    L = o.lib
-    dp = Ct.POINTER(Ct.c_double)
-    h = L.dcdref_ul_batch_create(S, C, BC, U, H.ctypes.data_as(dp), y.ctypes.data_as(dp))
+def cpu_model() -> str:
     try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_inputs(S, seed=5, c=C, u=U, bc=BC):
+    """Host batch of the bench workload (configs[1]): H [S][C][U][B_c], y, and
+    downlink symbols [S][U] (numpy, fp64 as the reference computes)."""
+    rng = np.random.default_rng(seed)
+    n0 = u * 1.0 / 10 ** (SNR_DB / 10)
+    H = np.empty((S, c, u, bc), np.complex128)
+    H.real = rng.standard_normal(H.shape)
+    H.imag = rng.standard_normal(H.shape)
+    H *= 1 / math.sqrt(2)
+    lv = np.array([-3.0, -1.0, 1.0, 3.0]) / math.sqrt(10.0)
+    x = lv[rng.integers(0, 4, (S, u))] + 1j * lv[rng.integers(0, 4, (S, u))]
+    y = np.einsum("scub,su->scb", H, x) + math.sqrt(n0 / 2) * (
+        rng.standard_normal((S, c, bc)) + 1j * rng.standard_normal((S, c, bc)))
+    sym = lv[rng.integers(0, 4, (S, u))] + 1j * lv[rng.integers(0, 4, (S, u))]
+    return np.ascontiguousarray(H), np.ascontiguousarray(y), np.ascontiguousarray(sym), n0
+
+
+class RefCPU:
+    """The reference's own decentralized_cd_detect / decentralized_cd_precode
+    (oracle/_ref, compiled from the reference sources) over a host batch of S
+    subcarriers, timed by the shim with contiguous subcarrier slices on
+    `threads` std::threads (oracle/ref_shim.cpp dcdref_*_batch_run)."""
+
+    def __init__(self, S, *, downlink=False, seed=5, c=C, u=U, bc=BC, arrays=None):
+        import ctypes as Ct
+        self.o = _ref_lib()
+        self.L = self.o.lib
+        if arrays is None:
+            H, y, sym, self.n0 = cpu_inputs(S, seed, c, u, bc)
+        else:  # (H [S][c][u][bc], y [S][c][bc], n0) from the caller
+            H, y, self.n0 = (np.ascontiguousarray(arrays[0], np.complex128), np.ascontiguousarray(arrays[1], np.complex128),
+                             arrays[2])
+            sym = np.zeros((S, u), np.complex128)
+        dp = Ct.POINTER(Ct.c_double)
+        self.S, self.u = S, u
+        self.ul = self.L.dcdref_ul_batch_create(S, c, bc, u, H.ctypes.data_as(dp), y.ctypes.data_as(dp))
+        self.dl = (self.L.dcdref_dl_batch_create(S, c, bc, u, H.ctypes.data_as(dp), sym.ctypes.data_as(dp))
+                   if downlink else None)
+        self.backend = self.o.backend()
+
+    def run(self, count, threads, *, direction="ul", fusion="uniform", concurrent=False, reps=1, first=0, out=None):
+        import ctypes as Ct
+        L = self.L
+        L.dcdref_set_concurrent(1 if concurrent else 0)
         ts = []
-        for _ in range(reps):
-            t = L.dcdref_ul_batch_run(h, n0, 1.0, K_SWEEPS, 1, 0, 0, threads, 0, S, None)
-            if t < 0:
-                raise RuntimeError(L.dcdref_last_error().decode())
-            ts.append(t)
-        return ts, o.backend()
-    finally:
-        L.dcdref_ul_batch_destroy(h)
+        optr = out.ctypes.data_as(Ct.POINTER(Ct.c_double)) if out is not None else None
+        try:
+            for _ in range(reps):
+                if direction == "ul":
+                    t = L.dcdref_ul_batch_run(self.ul, self.n0, 1.0, K_SWEEPS, 1 if fusion == "uniform" else 0, 0, 0,
+                                              threads, first, count, optr)
+                else:
+                    t = L.dcdref_dl_batch_run(self.dl, math.sqrt(self.u), K_SWEEPS, 0, 0, threads, first, count, None,
+                                              None)
+                if t < 0:
+                    raise RuntimeError(L.dcdref_last_error().decode())
+                ts.append(t)
+        finally:
+            L.dcdref_set_concurrent(0)
+        return ts
+
+    def close(self):
+        self.L.dcdref_ul_batch_destroy(self.ul)
+        if self.dl:
+            self.L.dcdref_dl_batch_destroy(self.dl)
 
 
-CPU_SAMPLE_S = 2400  # subcarrier-symbols per timed CPU run (x C = 19,200 cluster-problems, ~150 MB fp64)
+CPU_SAMPLE_S = 2400  # subcarrier-symbols of the CPU sample (x C = 19,200 cluster-problems, ~150 MB fp64)
+
+
+def _timed_mode(ref, threads, target_s, **kw):
+    """Gbps of one reference mode on a sample sized to ~target_s seconds."""
+    u = ref.u
+    probe = min(ref.S, max(threads * 2, 16))
+    t0 = ref.run(probe, threads, **kw)[0]
+    per_sc = max(t0 / probe, 1e-7)
+    count = int(min(ref.S, max(probe, target_s / per_sc)))
+    reps = max(1, int(target_s / (per_sc * count)))
+    sec = sum(ref.run(count, threads, reps=reps, **kw))
+    return {"value": round(count * reps * u * BITS / sec / 1e9, 6), "unit": "Gbps", "threads": threads,
+            "subcarriers": count * reps, "seconds": round(sec, 3),
+            "us_per_subcarrier_per_thread": round(sec * threads / (count * reps) * 1e6, 2)}
 
 
 def cpu_baseline(target_s=10.0):
+    """The reference's CPU path on this host: the headline (uplink, uniform
+    fusion, all host threads, like the GPU arm) plus the SURVEY §8(d) matrix:
+    1 thread, the reference's own concurrent=true mode, optimal fusion and the
+    downlink decentralized_cd_precode."""
     threads = os.cpu_count() or 1
     if _ref_lib() is None:
         return {"value": None, "unit": "Gbps", "cores": threads, "kind": "reference",
                 "sample": "oracle/_ref/libdcdref.so missing"}
-    t, _ = cpu_time_ref(CPU_SAMPLE_S, threads)
-    reps = int(min(max(target_s / max(t[0], 1e-3), 1), 5000))
-    ts, backend = cpu_time_ref(CPU_SAMPLE_S, threads, reps=reps)
-    sec = sum(ts)
-    return {"value": round(CPU_SAMPLE_S * reps * U * BITS / sec / 1e9, 6), "unit": "Gbps", "cores": threads,
-            "kind": "reference",
-            "sample": f"{reps} x {CPU_SAMPLE_S} subcarrier-symbols (C={C} clusters each) through the reference's "
-                      f"decentralized_cd_detect (uniform fusion, K=3) on {threads} std::threads, {sec:.2f} s, "
-                      f"reference kernels backend={backend}",
-            "seconds": round(sec, 3)}
+    ref = RefCPU(CPU_SAMPLE_S, downlink=True)
+    try:
+        head = _timed_mode(ref, threads, target_s)
+        side = max(1.0, target_s / 6)
+        modes = {
+            "ul_uniform_1thread": _timed_mode(ref, 1, side),
+            "ul_uniform_concurrent_true": dict(_timed_mode(ref, 1, side, concurrent=True),
+                                               note="one caller thread, the reference's concurrent=true "
+                                                    "(a std::thread per cluster per call, detect.cpp:32-52)"),
+            "ul_optimal_all_threads": _timed_mode(ref, threads, side, fusion="optimal"),
+            "ul_optimal_1thread": _timed_mode(ref, 1, side, fusion="optimal"),
+            "dl_all_threads": _timed_mode(ref, threads, side, direction="dl"),
+            "dl_1thread": _timed_mode(ref, 1, side, direction="dl"),
+        }
+    finally:
+        ref.close()
+    return {"value": head["value"], "unit": "Gbps", "cores": threads, "kind": "reference",
+            "cpu_model": cpu_model(),
+            "sample": f"{head['subcarriers']} subcarrier-symbols (C={C} clusters each) through the reference's "
+                      f"decentralized_cd_detect (uniform fusion, K=3, fp64) on {threads} std::threads, "
+                      f"{head['seconds']:.2f} s, reference kernels backend={ref.backend}",
+            "seconds": head["seconds"], "modes": modes}
 
 
 def run_reference(args):
@@ -581,13 +747,15 @@ def run_reference(args):
     if _ref_lib() is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdcdref.so not built"}))
         return
-    # each step: a bounded sample of the workload through the reference's own
-    # decentralized_cd_detect, all host threads, sized to fit the time budget
-    t, _ = cpu_time_ref(CPU_SAMPLE_S, threads)
-    per_sc = t[0] / CPU_SAMPLE_S
-    budget = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.2)
-    S = int(min(max(budget / per_sc, 240), 4 * CPU_SAMPLE_S))
-    ts, backend = cpu_time_ref(S, threads, reps=args.warmup + args.steps)
+    # the GPU arm's exact workload: S = 16,800 subcarrier-symbols per GPU (x N
+    # GPUs, weak scaling), each through the reference's own
+    # decentralized_cd_detect on all host threads
+    S = args.S * world
+    ref = RefCPU(S)
+    try:
+        ts = ref.run(S, threads, reps=args.warmup + args.steps)
+    finally:
+        ref.close()
     timed = ts[args.warmup:]
     sec = sum(timed) / len(timed)
     value = S * U * BITS / sec / 1e9
@@ -596,14 +764,32 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic CN(0,1) H / 16-QAM / AWGN (numpy), host-resident",
         "config": {"workload": "uplink CD L-MMSE detection + uniform fusion (configs[1])", "B": B, "U": U, "C": C,
-                   "B_c": BC, "K": K_SWEEPS, "qam": QAM, "subcarrier_symbols_per_step": S},
+                   "B_c": BC, "K": K_SWEEPS, "qam": QAM, "fmt": "fp64", "subcarrier_symbols_per_step": S},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 6), "unit": "Gbps", "cores": threads, "kind": "reference",
-                         "sample": f"{S} subcarrier-symbols per step through decentralized_cd_detect on {threads} "
-                                   f"std::threads, backend={backend}"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"the full step: {S} subcarrier-symbols (the GPU arm's per-step batch) through "
+                                   f"decentralized_cd_detect on {threads} std::threads, backend={ref.backend}"},
         "e2e": {"value": round(value, 6), "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _relaunch_torchrun(n: int) -> int:
+    """`python bench.py --gpus N` without a torchrun environment: start N ranks
+    (one per GPU) on this node with the same arguments; rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.run(cmd, env=env).returncode
 
 
 def main():
@@ -624,6 +810,15 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        raise SystemExit(f"bench.py: --gpus must be >= 1 (got {args.gpus})")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torchrun
+        sys.exit(_relaunch_torchrun(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+                         f"(torchrun --nproc-per-node {args.gpus}) or drop WORLD_SIZE from the environment")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -30,6 +30,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <span>
 #include <vector>
 
@@ -117,8 +118,10 @@ struct PrecodeResult {  // precode.hpp:33-37
   double effective_gain = 0.0;
 };
 
-/// One CUDA device context (dcdg_ctx) plus a stream.  Reentrant per Engine;
-/// use one Engine per host thread for concurrent calls.
+/// One CUDA device context (dcdg_ctx), its own stream, and the buffers every
+/// call reuses: grow-only device scratch and pinned host staging (no
+/// allocation, free or device-wide synchronisation per call once warm).
+/// Calls on one Engine serialise on its mutex; Engines run concurrently.
 class Engine {
  public:
   explicit Engine(int device = 0);
@@ -132,30 +135,75 @@ class Engine {
   static void check(int status);
   /// Waits for the stream and rethrows any recorded numerical error.
   void sync();
+  /// Device scratch of at least `bytes` (grow-only; valid until the next call
+  /// that needs more).  Callers hold mutex().
+  void* device_scratch(std::size_t bytes);
+  /// Pinned host staging of at least `bytes` (grow-only).  Callers hold mutex().
+  void* host_staging(std::size_t bytes);
+  std::mutex& mutex() { return *mu_; }
 
  private:
   dcdg_ctx* ctx_ = nullptr;
   void* stream_ = nullptr;
   int device_ = 0;
+  void* dscratch_ = nullptr;
+  std::size_t dscratch_bytes_ = 0;
+  void* hstage_ = nullptr;
+  std::size_t hstage_bytes_ = 0;
+  std::unique_ptr<std::mutex> mu_;
 };
 
-/// Process-wide engine on device 0 used by the reference-signature functions.
+/// The calling thread's engine on device 0 (thread_local): the
+/// reference-signature functions below use it, so concurrent host threads
+/// never serialise on a shared engine.
 Engine& default_engine();
 
 // ---- reference-signature API (one subcarrier per call) --------------------
+// `concurrent` is accepted for signature compatibility: every cluster of the
+// call already runs in one batched launch.  Each function also has an
+// overload taking the Engine explicitly (last argument).
 ComplexVector cd_detect(const ComplexMatrix& h, const ComplexVector& y, double n0, double ex,
                         unsigned t_max, const PrecisionMode& prec = {},
                         SweepObserver* observer = nullptr);
+ComplexVector cd_detect(const ComplexMatrix& h, const ComplexVector& y, double n0, double ex,
+                        unsigned t_max, const PrecisionMode& prec, SweepObserver* observer,
+                        Engine& eng);
 double post_eq_variance(const ComplexMatrix& hc, double n0, double ex);
+double post_eq_variance(const ComplexMatrix& hc, double n0, double ex, Engine& eng);
 std::vector<double> fusion_weights(std::span<const double> sigma2);
+std::vector<double> fusion_weights(std::span<const double> sigma2, Engine& eng);
 DetectionResult decentralized_cd_detect(std::span<const ClusterData> clusters,
                                         const DetectorConfig& cfg, bool concurrent = false);
+DetectionResult decentralized_cd_detect(std::span<const ClusterData> clusters,
+                                        const DetectorConfig& cfg, bool concurrent, Engine& eng);
 ComplexVector cd_precode(const ComplexMatrix& h_dl, const ComplexVector& s, unsigned t_max,
                          const PrecisionMode& prec = {}, SweepObserver* observer = nullptr);
+ComplexVector cd_precode(const ComplexMatrix& h_dl, const ComplexVector& s, unsigned t_max,
+                         const PrecisionMode& prec, SweepObserver* observer, Engine& eng);
 void power_scale(ComplexVector& x, double rho);
+void power_scale(ComplexVector& x, double rho, Engine& eng);
 PrecodeResult decentralized_cd_precode(std::span<const ComplexMatrix> h_dl_blocks,
                                        const ComplexVector& s, const PrecoderConfig& cfg,
                                        bool concurrent = false);
+PrecodeResult decentralized_cd_precode(std::span<const ComplexMatrix> h_dl_blocks,
+                                       const ComplexVector& s, const PrecoderConfig& cfg,
+                                       bool concurrent, Engine& eng);
+
+// ---- batched round API (what the reference's per-subcarrier round loops,
+// src/cluster.cpp:138-152 and :239-254, become) ------------------------------
+/// decentralized_cd_detect for every subcarrier in ONE device call: the same
+/// checks (in the reference's order, per subcarrier) and the same results as
+/// calling decentralized_cd_detect per subcarrier.  Subcarriers whose clusters
+/// all have the same antenna count (the round's partition_rows case) share one
+/// launch; otherwise each subcarrier is its own launch sequence.
+std::vector<DetectionResult> decentralized_cd_detect_batch(
+    std::span<const std::vector<ClusterData>> subcarriers, const DetectorConfig& cfg,
+    Engine& eng = default_engine());
+/// decentralized_cd_precode for every subcarrier (blocks[s], symbols[s]) in ONE
+/// device call, with the reference's per-subcarrier checks and results.
+std::vector<PrecodeResult> decentralized_cd_precode_batch(
+    std::span<const std::vector<ComplexMatrix>> h_dl_blocks, std::span<const ComplexVector> s,
+    const PrecoderConfig& cfg, Engine& eng = default_engine());
 
 // ---- batched device API (the hot path) --------------------------------------
 /// Device-resident batch of S subcarriers x C local clusters in the dcdg.h

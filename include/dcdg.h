@@ -94,6 +94,8 @@ const char* dcdg_last_error(void);
  *   x_local   optional [P][U] in `fmt` (NULL = not returned).
  *   sigma2    optional [P] fp32: optimal-fusion variances (post_eq_variance);
  *             required scratch when fusion == OPTIMAL (NULL = internal).
+ *             Optimal fusion supports U <= 32 (DCDG_EINVAL otherwise, as
+ *             dcdg_post_eq_variance); uniform fusion takes any U.
  *   xhat      optional [S][U] fp32 complex.  With C == C_total it is the
  *             reference's fused estimate (ascending-cluster order).  With
  *             C < C_total it is this GPU's partial: uniform: sum_c x_c/C_total;
@@ -131,6 +133,13 @@ int dcdg_fuse(dcdg_ctx* ctx, const void* x_local, const float* sigma2, int S, in
 /* gain[s] = (sum_c gain_part[s][c]) / ||s_s||^2  (precode.cpp:123-131). */
 int dcdg_gain_reduce(dcdg_ctx* ctx, const float* gain_part, const void* s, int S, int C, int U,
                      int fmt, float* gain, void* stream);
+
+/* gain_part[p] = Re(s^H H_dl,c x_c) of finished beamformers x_dl [P][Bc]
+ * (assemble_blocks' per-cluster share, precode.cpp:123-131); feeds
+ * dcdg_gain_reduce when the gain must use a different s than the precoder saw
+ * (fp16 messages_only: the clusters precode the rounded broadcast). */
+int dcdg_gain_part(dcdg_ctx* ctx, const void* H, const void* x_dl, const void* s, int S, int C, int Bc,
+                   int U, int fmt, float* gain_part, void* stream);
 
 /* Finalize a cross-GPU optimal-fusion reduction: xhat[s] /= wsum[s]. */
 int dcdg_fuse_finalize(dcdg_ctx* ctx, float* xhat, const float* wsum, int S, int U, void* stream);

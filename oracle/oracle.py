@@ -105,6 +105,7 @@ class Oracle:
             L.dcdref_dl_batch_create.argtypes = [C.c_int] * 4 + [_dp, _dp]
             L.dcdref_ul_batch_destroy.argtypes = [C.c_void_p]
             L.dcdref_dl_batch_destroy.argtypes = [C.c_void_p]
+            L.dcdref_set_concurrent.argtypes = [C.c_int]
             L.dcdref_ul_batch_run.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_uint, C.c_int,
                                               C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
             L.dcdref_dl_batch_run.argtypes = [C.c_void_p, C.c_double, C.c_uint, C.c_int, C.c_int,

@@ -334,6 +334,15 @@ int dcdref_uplink_observe(const double* h, int b, int u, const uint8_t* bits, un
 double dcdref_snr_to_n0(double snr_db, int users, double ex) { return dcd::snr_to_n0(snr_db, users, ex); }
 
 // ---- batched CPU baseline --------------------------------------------------
+// The reference's own `concurrent` argument of decentralized_cd_detect /
+// decentralized_cd_precode (one std::thread per cluster per call,
+// detect.cpp:32-52) for the batch runners below; off by default.
+static bool g_concurrent = false;
+int dcdref_set_concurrent(int on) {
+  g_concurrent = on != 0;
+  return 0;
+}
+
 // h_tiles: [S][C] tiles of B_c x U (column-major); y: [S][C][B_c].
 void* dcdref_ul_batch_create(int s, int nc, int bc, int u, const double* h_tiles, const double* y) {
   auto* b = new UlBatch;
@@ -375,7 +384,7 @@ double dcdref_ul_batch_run(void* p, double n0, double ex, unsigned t_max, int fu
     const int hi = first + static_cast<int>(static_cast<long long>(count) * (t + 1) / threads);
     try {
       for (int i = lo; i < hi; ++i) {
-        const auto r = dcd::decentralized_cd_detect(b->sub[i], cfg, false);
+        const auto r = dcd::decentralized_cd_detect(b->sub[i], cfg, g_concurrent);
         if (xhat) vec_out(r.xhat, xhat + 2 * static_cast<std::size_t>(i - first) * b->u);
       }
     } catch (...) {
@@ -438,7 +447,7 @@ double dcdref_dl_batch_run(void* p, double rho, unsigned t_max, int fmt, int sco
     const int hi = first + static_cast<int>(static_cast<long long>(count) * (t + 1) / threads);
     try {
       for (int i = lo; i < hi; ++i) {
-        const auto r = dcd::decentralized_cd_precode(b->hdl[i], b->sym[i], cfg, false);
+        const auto r = dcd::decentralized_cd_precode(b->hdl[i], b->sym[i], cfg, g_concurrent);
         if (x) vec_out(r.x, x + 2 * static_cast<std::size_t>(i - first) * r.x.size());
         if (gain) gain[i - first] = r.effective_gain;
       }

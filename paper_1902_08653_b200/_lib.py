@@ -61,6 +61,7 @@ SIGNATURES = {
     "dcdg_fuse": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp]),
     "dcdg_gain_reduce": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp]),
     "dcdg_fuse_finalize": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _vp]),
+    "dcdg_gain_part": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp]),
     "dcdg_power_scale": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_double, C.c_int, _vp]),
     "dcdg_fusion_weights": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp]),
     "dcdg_sync_status": (C.c_int, [_vp, _vp]),

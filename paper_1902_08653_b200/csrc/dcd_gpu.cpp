@@ -97,20 +97,6 @@ void unpack(const unsigned char* in, std::size_t n, int fmt, cf64* out) {
   }
 }
 
-struct DevMem {
-  void* p = nullptr;
-  explicit DevMem(std::size_t bytes) {
-    if (bytes && cudaMalloc(&p, bytes) != cudaSuccess) throw std::runtime_error("dcd::gpu: device allocation failed");
-  }
-  ~DevMem() {
-    if (p) cudaFree(p);
-  }
-  template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
-
 void h2d(void* dst, const void* src, std::size_t bytes, void* st) {
   if (!bytes) return;
   if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(st)) != cudaSuccess)
@@ -142,6 +128,35 @@ DevPrecision map_precision(const PrecisionMode& p) {
 constexpr std::size_t kAlign = 256;
 std::size_t align_up(std::size_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
 
+// One call's buffers, laid out identically in the engine's pinned staging and
+// device scratch: inputs [0, in_end) go over in one H2D copy, outputs
+// [in_end, end) come back in one D2H copy.
+struct Layout {
+  std::size_t end = 0, in_end = 0;
+  std::size_t take(std::size_t bytes) {
+    const std::size_t off = end;
+    end = align_up(end + bytes);
+    return off;
+  }
+  void close_inputs() { in_end = end; }
+};
+
+struct Call {
+  Engine& eng;
+  unsigned char* host;
+  unsigned char* dev;
+  Call(Engine& e, const Layout& l)
+      : eng(e),
+        host(static_cast<unsigned char*>(e.host_staging(l.end))),
+        dev(static_cast<unsigned char*>(e.device_scratch(l.end))) {}
+  template <class T = unsigned char>
+  T* h(std::size_t off) const { return reinterpret_cast<T*>(host + off); }
+  template <class T = unsigned char>
+  T* d(std::size_t off) const { return reinterpret_cast<T*>(dev + off); }
+  void upload(const Layout& l) const { h2d(dev, host, l.in_end, eng.stream()); }
+  void download(const Layout& l) const { d2h(host + l.in_end, dev + l.in_end, l.end - l.in_end, eng.stream()); }
+};
+
 // detect.cpp:12-19
 void check_system(const ComplexMatrix& h, std::size_t ylen, double n0, double ex) {
   if (h.rows() == 0 || h.cols() == 0) throw std::invalid_argument("detector: empty channel matrix");
@@ -168,246 +183,24 @@ void uplink_tile_of(const ComplexMatrix& h_dl, cf64* out) {
     for (std::size_t i = 0; i < b; ++i) out[j * b + i] = std::conj(h_dl(j, i));
 }
 
-}  // namespace
-
-// ---------------------------------------------------------------------------
-// Engine
-// ---------------------------------------------------------------------------
-void Engine::check(int status) {
-  if (status == DCDG_OK) return;
-  throw_status(status, dcdg_last_error());
-}
-
-Engine::Engine(int device) : device_(device) {
-  check(dcdg_init(device, &ctx_));
-  // PrecisionMode{fp16, full_storage} mirrors the reference's fp16 arithmetic
-  // emulation: the half2 sweep kernel, not the fp32-arithmetic Gram kernel
-  check(dcdg_set_fp16_algorithm(ctx_, DCDG_ALG_SWEEP));
-  cudaStream_t st = nullptr;
-  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
-    dcdg_destroy(ctx_);
-    throw std::runtime_error("dcd::gpu: stream creation failed");
-  }
-  stream_ = st;
-}
-
-Engine::~Engine() {
-  if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
-  dcdg_destroy(ctx_);
-}
-
-void Engine::sync() { check(dcdg_sync_status(ctx_, stream_)); }
-
-Engine& default_engine() {
-  static Engine eng(0);
-  return eng;
-}
-
-namespace {
-std::mutex g_default_mu;  // the reference-signature calls share default_engine()
-}
-
-// ---------------------------------------------------------------------------
-// uplink
-// ---------------------------------------------------------------------------
-ComplexVector cd_detect(const ComplexMatrix& h, const ComplexVector& y, double n0, double ex, unsigned t_max,
-                        const PrecisionMode& prec, SweepObserver* observer) {
-  check_system(h, y.size(), n0, ex);
-  if (t_max == 0) throw std::invalid_argument("cd_detect: need at least one sweep");
-  reject_observer(observer);
-  std::lock_guard<std::mutex> lk(g_default_mu);
-  Engine& eng = default_engine();
-  const DevPrecision dp = map_precision(prec);
-  const std::size_t b = h.rows(), u = h.cols(), es = esize(dp.fmt), bd = dev_rows(b, dp.fmt);
-  std::vector<unsigned char> hb(bd * u * es), yb(bd * es), xb(u * es);
-  pack_tile(h.flat().data(), b, u, dp.fmt, hb.data());
-  pack_tile(y.data(), b, 1, dp.fmt, yb.data());
-  DevMem dh(hb.size()), dy(yb.size()), dx(xb.size());
-  h2d(dh.p, hb.data(), hb.size(), eng.stream());
-  h2d(dy.p, yb.data(), yb.size(), eng.stream());
-  Engine::check(dcdg_ul_detect(eng.ctx(), dh.p, dy.p, 1, 1, 1, static_cast<int>(bd), static_cast<int>(u),
-                               static_cast<int>(t_max), n0, ex, dp.fmt, DCDG_FUSION_UNIFORM, dx.p, nullptr, nullptr,
-                               nullptr, eng.stream()));
-  d2h(xb.data(), dx.p, xb.size(), eng.stream());
-  eng.sync();
-  ComplexVector x(u);
-  unpack(xb.data(), u, dp.fmt, x.data());
-  return x;
-}
-
-double post_eq_variance(const ComplexMatrix& hc, double n0, double ex) {
-  if (hc.rows() == 0 || hc.cols() == 0) throw std::invalid_argument("post_eq_variance: empty channel block");
-  if (!(n0 > 0.0) || !(ex > 0.0)) throw std::invalid_argument("post_eq_variance: need N0 > 0 and E_x > 0");
-  std::lock_guard<std::mutex> lk(g_default_mu);
-  Engine& eng = default_engine();
-  const std::size_t b = hc.rows(), u = hc.cols();
-  std::vector<unsigned char> hb(b * u * 8);
-  pack(hc.flat().data(), b * u, DCDG_FP32, hb.data());
-  DevMem dh(hb.size()), ds(sizeof(float));
-  h2d(dh.p, hb.data(), hb.size(), eng.stream());
-  Engine::check(dcdg_post_eq_variance(eng.ctx(), dh.p, 1, static_cast<int>(b), static_cast<int>(u), n0, ex, DCDG_FP32,
-                                      ds.as<float>(), eng.stream()));
-  float s2 = 0.f;
-  d2h(&s2, ds.p, sizeof s2, eng.stream());
-  eng.sync();
-  return s2;
-}
-
-std::vector<double> fusion_weights(std::span<const double> sigma2) {
-  if (sigma2.empty()) throw std::invalid_argument("fusion_weights: no clusters");
-  for (double v : sigma2)
-    if (!(v > 0.0) || !std::isfinite(v))
-      throw std::invalid_argument("fusion_weights: variances must be positive and finite");
-  std::lock_guard<std::mutex> lk(g_default_mu);
-  Engine& eng = default_engine();
-  const int c = static_cast<int>(sigma2.size());
-  std::vector<float> s2(sigma2.begin(), sigma2.end()), w(c);
-  DevMem ds(c * sizeof(float)), dw(c * sizeof(float));
-  h2d(ds.p, s2.data(), c * sizeof(float), eng.stream());
-  Engine::check(dcdg_fusion_weights(eng.ctx(), ds.as<float>(), 1, c, dw.as<float>(), eng.stream()));
-  d2h(w.data(), dw.p, c * sizeof(float), eng.stream());
-  eng.sync();
-  return {w.begin(), w.end()};
-}
-
-DetectionResult decentralized_cd_detect(std::span<const ClusterData> clusters, const DetectorConfig& cfg,
-                                        bool /*concurrent*/) {
-  // detect.cpp:150-155
+// ---- the reference's per-call checks, in its order -------------------------
+// detect.cpp:150-155 then each worker's cd_detect / post_eq_variance checks
+std::size_t check_detect_call(std::span<const ClusterData> clusters, const DetectorConfig& cfg) {
   if (clusters.empty()) throw std::invalid_argument("decentralized_cd_detect: no clusters");
   const std::size_t u = clusters[0].h.cols();
   for (const auto& c : clusters)
     if (c.h.cols() != u) throw std::invalid_argument("decentralized_cd_detect: clusters disagree on user count");
-  // per-cluster checks in worker order (cd_detect then post_eq_variance)
   const bool optimal = cfg.fusion == FusionMode::optimal;
   for (const auto& c : clusters) {
     check_system(c.h, c.y.size(), cfg.n0, cfg.ex);
     if (cfg.t_max == 0) throw std::invalid_argument("cd_detect: need at least one sweep");
     if (optimal && !(cfg.n0 > 0.0)) throw std::invalid_argument("post_eq_variance: need N0 > 0 and E_x > 0");
   }
-  std::lock_guard<std::mutex> lk(g_default_mu);
-  Engine& eng = default_engine();
-  const DevPrecision dp = map_precision(cfg.precision);
-  const std::size_t nc = clusters.size(), es = esize(dp.fmt);
-  bool uniform_bc = true;
-  for (const auto& c : clusters) uniform_bc &= c.h.rows() == clusters[0].h.rows();
-
-  // one device buffer each for tiles, observations and per-cluster outputs
-  std::vector<std::size_t> hoff(nc), yoff(nc);
-  std::size_t hbytes = 0, ybytes = 0;
-  for (std::size_t c = 0; c < nc; ++c) {
-    hoff[c] = hbytes;
-    yoff[c] = ybytes;
-    const std::size_t b = dev_rows(clusters[c].h.rows(), dp.fmt);
-    hbytes += uniform_bc ? b * u * es : align_up(b * u * es);
-    ybytes += uniform_bc ? b * es : align_up(b * es);
-  }
-  std::vector<unsigned char> hb(hbytes), yb(ybytes);
-  for (std::size_t c = 0; c < nc; ++c) {
-    pack_tile(clusters[c].h.flat().data(), clusters[c].h.rows(), u, dp.fmt, hb.data() + hoff[c]);
-    pack_tile(clusters[c].y.data(), clusters[c].y.size(), 1, dp.fmt, yb.data() + yoff[c]);
-  }
-  const std::size_t xl_bytes = nc * u * es;
-  DevMem dh(hbytes), dy(ybytes), dxl(xl_bytes), ds2(nc * sizeof(float)), dxh(u * 8), dw(nc * sizeof(float));
-  h2d(dh.p, hb.data(), hbytes, eng.stream());
-  h2d(dy.p, yb.data(), ybytes, eng.stream());
-  const int fusion = optimal ? DCDG_FUSION_OPTIMAL : DCDG_FUSION_UNIFORM;
-  const int ui = static_cast<int>(u), K = static_cast<int>(cfg.t_max);
-  if (uniform_bc) {
-    Engine::check(dcdg_ul_detect(eng.ctx(), dh.p, dy.p, 1, static_cast<int>(nc), static_cast<int>(nc),
-                                 static_cast<int>(dev_rows(clusters[0].h.rows(), dp.fmt)), ui, K, cfg.n0, cfg.ex, dp.fmt, fusion, dxl.p,
-                                 optimal ? ds2.as<float>() : nullptr, nullptr, nullptr, eng.stream()));
-  } else {
-    for (std::size_t c = 0; c < nc; ++c)
-      Engine::check(dcdg_ul_detect(eng.ctx(), static_cast<unsigned char*>(dh.p) + hoff[c],
-                                   static_cast<unsigned char*>(dy.p) + yoff[c], 1, 1, 1,
-                                   static_cast<int>(dev_rows(clusters[c].h.rows(), dp.fmt)), ui, K, cfg.n0, cfg.ex, dp.fmt, fusion,
-                                   static_cast<unsigned char*>(dxl.p) + c * u * es,
-                                   optimal ? ds2.as<float>() + c : nullptr, nullptr, nullptr, eng.stream()));
-  }
-  // message boundary: payloads leave the cluster in the wire precision (detect.cpp:169-173)
-  if (dp.round_messages) {
-    Engine::check(dcdg_round_fp16(eng.ctx(), dxl.as<float>(), static_cast<int64_t>(2 * nc * u), eng.stream()));
-    if (optimal) Engine::check(dcdg_round_fp16(eng.ctx(), ds2.as<float>(), static_cast<int64_t>(nc), eng.stream()));
-  }
-  Engine::check(dcdg_fuse(eng.ctx(), dxl.p, optimal ? ds2.as<float>() : nullptr, 1, static_cast<int>(nc),
-                          static_cast<int>(nc), ui, dp.fmt, fusion, dxh.as<float>(), nullptr, eng.stream()));
-  if (optimal)
-    Engine::check(dcdg_fusion_weights(eng.ctx(), ds2.as<float>(), 1, static_cast<int>(nc), dw.as<float>(), eng.stream()));
-  std::vector<unsigned char> xl(xl_bytes);
-  std::vector<float> xh(2 * u), s2(nc), w(nc);
-  d2h(xl.data(), dxl.p, xl_bytes, eng.stream());
-  d2h(xh.data(), dxh.p, u * 8, eng.stream());
-  if (optimal) {
-    d2h(s2.data(), ds2.p, nc * sizeof(float), eng.stream());
-    d2h(w.data(), dw.p, nc * sizeof(float), eng.stream());
-  }
-  eng.sync();
-
-  DetectionResult res;
-  res.local.resize(nc);
-  for (std::size_t c = 0; c < nc; ++c) {
-    res.local[c].resize(u);
-    unpack(xl.data() + c * u * es, u, dp.fmt, res.local[c].data());
-  }
-  res.xhat.resize(u);
-  for (std::size_t j = 0; j < u; ++j) res.xhat[j] = cf64{xh[2 * j], xh[2 * j + 1]};
-  if (optimal) {
-    res.sigma2.assign(s2.begin(), s2.end());
-    res.weights.assign(w.begin(), w.end());
-  } else {
-    res.weights.assign(nc, 1.0 / static_cast<double>(nc));  // detect.cpp:181
-  }
-  return res;
+  return u;
 }
 
-// ---------------------------------------------------------------------------
-// downlink
-// ---------------------------------------------------------------------------
-ComplexVector cd_precode(const ComplexMatrix& h_dl, const ComplexVector& s, unsigned t_max,
-                         const PrecisionMode& prec, SweepObserver* observer) {
-  check_downlink(h_dl, s);
-  if (t_max == 0) throw std::invalid_argument("cd_precode: need at least one sweep");
-  reject_observer(observer);
-  std::lock_guard<std::mutex> lk(g_default_mu);
-  Engine& eng = default_engine();
-  const DevPrecision dp = map_precision(prec);
-  const std::size_t u = h_dl.rows(), b = h_dl.cols(), es = esize(dp.fmt), bd = dev_rows(b, dp.fmt);
-  std::vector<cf64> tile(b * u);
-  uplink_tile_of(h_dl, tile.data());
-  std::vector<unsigned char> hb(bd * u * es), sb(u * es), xb(bd * es);
-  pack_tile(tile.data(), b, u, dp.fmt, hb.data());
-  pack(s.data(), u, dp.fmt, sb.data());
-  DevMem dh(hb.size()), ds(sb.size()), dx(xb.size());
-  h2d(dh.p, hb.data(), hb.size(), eng.stream());
-  h2d(ds.p, sb.data(), sb.size(), eng.stream());
-  // rho == 0: unnormalised beamformer, exactly what cd_precode returns
-  Engine::check(dcdg_dl_precode(eng.ctx(), dh.p, ds.p, 1, 1, 1, static_cast<int>(bd), static_cast<int>(u),
-                                static_cast<int>(t_max), 0.0, dp.fmt, dx.p, nullptr, nullptr, eng.stream()));
-  d2h(xb.data(), dx.p, xb.size(), eng.stream());
-  eng.sync();
-  ComplexVector x(b);
-  unpack(xb.data(), b, dp.fmt, x.data());
-  return x;
-}
-
-void power_scale(ComplexVector& x, double rho) {
-  if (!(rho > 0.0)) throw std::invalid_argument("power_scale: amplitude must be positive");
-  if (x.empty()) throw std::invalid_argument("power_scale: empty beamformer");
-  std::lock_guard<std::mutex> lk(g_default_mu);
-  Engine& eng = default_engine();
-  std::vector<unsigned char> xb(x.size() * 8);
-  pack(x.data(), x.size(), DCDG_FP32, xb.data());
-  DevMem dx(xb.size());
-  h2d(dx.p, xb.data(), xb.size(), eng.stream());
-  Engine::check(dcdg_power_scale(eng.ctx(), dx.p, 1, static_cast<int>(x.size()), rho, DCDG_FP32, eng.stream()));
-  d2h(xb.data(), dx.p, xb.size(), eng.stream());
-  eng.sync();
-  unpack(xb.data(), x.size(), DCDG_FP32, x.data());
-}
-
-PrecodeResult decentralized_cd_precode(std::span<const ComplexMatrix> h_dl_blocks, const ComplexVector& s,
-                                       const PrecoderConfig& cfg, bool /*concurrent*/) {
-  // precode.cpp:138-152
+// precode.cpp:138-152, then cd_precode / power_scale
+void check_precode_call(std::span<const ComplexMatrix> h_dl_blocks, const ComplexVector& s, const PrecoderConfig& cfg) {
   if (h_dl_blocks.empty()) throw std::invalid_argument("decentralized_cd_precode: no clusters");
   const std::size_t u = s.size();
   for (std::size_t c = 0; c < h_dl_blocks.size(); ++c) {
@@ -421,65 +214,473 @@ PrecodeResult decentralized_cd_precode(std::span<const ComplexMatrix> h_dl_block
   }
   if (cfg.t_max == 0) throw std::invalid_argument("cd_precode: need at least one sweep");
   if (!(cfg.rho > 0.0)) throw std::invalid_argument("power_scale: amplitude must be positive");
-  std::lock_guard<std::mutex> lk(g_default_mu);
-  Engine& eng = default_engine();
+}
+
+bool uniform_rows(std::span<const ClusterData> cl) {
+  for (const auto& c : cl)
+    if (c.h.rows() != cl[0].h.rows()) return false;
+  return true;
+}
+bool uniform_cols(std::span<const ComplexMatrix> bl) {
+  for (const auto& b : bl)
+    if (b.cols() != bl[0].cols()) return false;
+  return true;
+}
+
+// ---- uplink: S subcarriers with identical cluster shapes in one launch -----
+// (uniform B_c, the layout of include/dcdg.h), or one subcarrier with
+// per-cluster launches (non-uniform B_c).
+using ClusterSpan = std::span<const ClusterData>;
+using BlockSpan = std::span<const ComplexMatrix>;
+
+std::vector<DetectionResult> detect_impl(std::span<const ClusterSpan> subs, std::size_t u,
+                                         const DetectorConfig& cfg, Engine& eng) {
   const DevPrecision dp = map_precision(cfg.precision);
-  const std::size_t nc = h_dl_blocks.size(), es = esize(dp.fmt);
-  bool uniform_bc = true;
-  for (const auto& h : h_dl_blocks) uniform_bc &= h.cols() == h_dl_blocks[0].cols();
-  std::vector<std::size_t> hoff(nc), xoff(nc);
-  std::size_t hbytes = 0, xbytes = 0, btot = 0;
+  const bool optimal = cfg.fusion == FusionMode::optimal;
+  const std::size_t S = subs.size(), nc = subs[0].size(), es = esize(dp.fmt);
+  const bool uniform = S > 1 || uniform_rows(subs[0]);  // S > 1: shapes checked equal by the caller
+  // per-cluster byte offsets inside one subcarrier's tile / vector block
+  std::vector<std::size_t> hoff(nc), yoff(nc);
+  std::size_t hsub = 0, ysub = 0;
   for (std::size_t c = 0; c < nc; ++c) {
-    const std::size_t b = dev_rows(h_dl_blocks[c].cols(), dp.fmt);
-    hoff[c] = hbytes;
-    xoff[c] = xbytes;
-    hbytes += uniform_bc ? b * u * es : align_up(b * u * es);
-    xbytes += uniform_bc ? b * es : align_up(b * es);
-    btot += h_dl_blocks[c].cols();
+    hoff[c] = hsub;
+    yoff[c] = ysub;
+    const std::size_t b = dev_rows(subs[0][c].h.rows(), dp.fmt);
+    hsub += uniform ? b * u * es : align_up(b * u * es);
+    ysub += uniform ? b * es : align_up(b * es);
   }
-  std::vector<unsigned char> hb(hbytes), sb(u * es), xb(xbytes);
-  for (std::size_t c = 0; c < nc; ++c) {
-    std::vector<cf64> tile(h_dl_blocks[c].cols() * u);
-    uplink_tile_of(h_dl_blocks[c], tile.data());
-    pack_tile(tile.data(), h_dl_blocks[c].cols(), u, dp.fmt, hb.data() + hoff[c]);
-  }
-  pack(s.data(), u, dp.fmt, sb.data());
-  DevMem dh(hbytes), ds(sb.size()), dx(xbytes), dgp(nc * sizeof(float)), dg(sizeof(float));
-  h2d(dh.p, hb.data(), hbytes, eng.stream());
-  h2d(ds.p, sb.data(), sb.size(), eng.stream());
-  // broadcast boundary: every cluster receives s in the wire precision (precode.cpp:157-160)
-  if (dp.round_messages)
-    Engine::check(dcdg_round_fp16(eng.ctx(), ds.as<float>(), static_cast<int64_t>(2 * u), eng.stream()));
+  Layout L;
+  const std::size_t oH = L.take(S * hsub), oY = L.take(S * ysub);
+  L.close_inputs();
+  const std::size_t oXL = L.take(S * nc * u * es), oS2 = L.take(optimal ? S * nc * sizeof(float) : 0),
+                    oXH = L.take(S * u * 8), oW = L.take(optimal ? S * nc * sizeof(float) : 0);
+  Call k(eng, L);
+  for (std::size_t s = 0; s < S; ++s)
+    for (std::size_t c = 0; c < nc; ++c) {
+      const auto& cl = subs[s][c];
+      pack_tile(cl.h.flat().data(), cl.h.rows(), u, dp.fmt, k.h(oH + s * hsub + hoff[c]));
+      pack_tile(cl.y.data(), cl.y.size(), 1, dp.fmt, k.h(oY + s * ysub + yoff[c]));
+    }
+  k.upload(L);
+  const int fusion = optimal ? DCDG_FUSION_OPTIMAL : DCDG_FUSION_UNIFORM;
   const int ui = static_cast<int>(u), K = static_cast<int>(cfg.t_max), nci = static_cast<int>(nc);
-  if (uniform_bc) {
-    Engine::check(dcdg_dl_precode(eng.ctx(), dh.p, ds.p, 1, nci, nci,
-                                  static_cast<int>(dev_rows(h_dl_blocks[0].cols(), dp.fmt)), ui, K,
-                                  cfg.rho, dp.fmt, dx.p, dgp.as<float>(), nullptr, eng.stream()));
+  const int Si = static_cast<int>(S);
+  float* s2 = optimal ? k.d<float>(oS2) : nullptr;
+  if (uniform) {
+    Engine::check(dcdg_ul_detect(eng.ctx(), k.d(oH), k.d(oY), Si, nci, nci,
+                                 static_cast<int>(dev_rows(subs[0][0].h.rows(), dp.fmt)), ui, K, cfg.n0, cfg.ex,
+                                 dp.fmt, fusion, k.d(oXL), s2, nullptr, nullptr, eng.stream()));
+  } else {
+    for (std::size_t c = 0; c < nc; ++c)
+      Engine::check(dcdg_ul_detect(eng.ctx(), k.d(oH + hoff[c]), k.d(oY + yoff[c]), 1, 1, 1,
+                                   static_cast<int>(dev_rows(subs[0][c].h.rows(), dp.fmt)), ui, K, cfg.n0, cfg.ex,
+                                   dp.fmt, fusion, k.d(oXL + c * u * es), optimal ? s2 + c : nullptr, nullptr,
+                                   nullptr, eng.stream()));
+  }
+  // message boundary: payloads leave the cluster in the wire precision (detect.cpp:169-173)
+  if (dp.round_messages) {
+    Engine::check(dcdg_round_fp16(eng.ctx(), k.d<float>(oXL), static_cast<int64_t>(2 * S * nc * u), eng.stream()));
+    if (optimal) Engine::check(dcdg_round_fp16(eng.ctx(), s2, static_cast<int64_t>(S * nc), eng.stream()));
+  }
+  Engine::check(dcdg_fuse(eng.ctx(), k.d(oXL), s2, Si, nci, nci, ui, dp.fmt, fusion, k.d<float>(oXH), nullptr,
+                          eng.stream()));
+  if (optimal) Engine::check(dcdg_fusion_weights(eng.ctx(), s2, Si, nci, k.d<float>(oW), eng.stream()));
+  k.download(L);
+  eng.sync();
+
+  std::vector<DetectionResult> out(S);
+  for (std::size_t s = 0; s < S; ++s) {
+    DetectionResult& res = out[s];
+    res.local.resize(nc);
+    for (std::size_t c = 0; c < nc; ++c) {
+      res.local[c].resize(u);
+      unpack(k.h(oXL + (s * nc + c) * u * es), u, dp.fmt, res.local[c].data());
+    }
+    const float* xh = k.h<float>(oXH) + 2 * s * u;
+    res.xhat.resize(u);
+    for (std::size_t j = 0; j < u; ++j) res.xhat[j] = cf64{xh[2 * j], xh[2 * j + 1]};
+    if (optimal) {
+      const float* sv = k.h<float>(oS2) + s * nc;
+      const float* wv = k.h<float>(oW) + s * nc;
+      res.sigma2.assign(sv, sv + nc);
+      res.weights.assign(wv, wv + nc);
+    } else {
+      res.weights.assign(nc, 1.0 / static_cast<double>(nc));  // detect.cpp:181
+    }
+  }
+  return out;
+}
+
+// ---- downlink ---------------------------------------------------------------
+std::vector<PrecodeResult> precode_impl(std::span<const BlockSpan> blocks,
+                                        std::span<const ComplexVector> syms, const PrecoderConfig& cfg,
+                                        Engine& eng) {
+  const DevPrecision dp = map_precision(cfg.precision);
+  const std::size_t S = blocks.size(), nc = blocks[0].size(), u = syms[0].size(), es = esize(dp.fmt);
+  const bool uniform = S > 1 || uniform_cols(blocks[0]);
+  std::vector<std::size_t> hoff(nc), xoff(nc);
+  std::size_t hsub = 0, xsub = 0, btot = 0;
+  for (std::size_t c = 0; c < nc; ++c) {
+    const std::size_t b = dev_rows(blocks[0][c].cols(), dp.fmt);
+    hoff[c] = hsub;
+    xoff[c] = xsub;
+    hsub += uniform ? b * u * es : align_up(b * u * es);
+    xsub += uniform ? b * es : align_up(b * es);
+    btot += blocks[0][c].cols();
+  }
+  Layout L;
+  const std::size_t oH = L.take(S * hsub), oS = L.take(S * u * es);
+  // fp16 messages_only: the clusters precode the rounded broadcast, the gain
+  // uses the centre's own s (assemble_blocks, precode.cpp:157-168)
+  const std::size_t oSw = L.take(dp.round_messages ? S * u * es : 0);
+  L.close_inputs();
+  const std::size_t oX = L.take(S * xsub), oGP = L.take(S * nc * sizeof(float)), oG = L.take(S * sizeof(float));
+  Call k(eng, L);
+  std::vector<cf64> tile;
+  for (std::size_t s = 0; s < S; ++s) {
+    for (std::size_t c = 0; c < nc; ++c) {
+      tile.resize(blocks[s][c].cols() * u);
+      uplink_tile_of(blocks[s][c], tile.data());
+      pack_tile(tile.data(), blocks[s][c].cols(), u, dp.fmt, k.h(oH + s * hsub + hoff[c]));
+    }
+    pack(syms[s].data(), u, dp.fmt, k.h(oS + s * u * es));
+    if (dp.round_messages) pack(syms[s].data(), u, dp.fmt, k.h(oSw + s * u * es));
+  }
+  k.upload(L);
+  const void* s_in = k.d(oS);
+  if (dp.round_messages) {  // broadcast boundary (precode.cpp:157-160)
+    Engine::check(dcdg_round_fp16(eng.ctx(), k.d<float>(oSw), static_cast<int64_t>(2 * S * u), eng.stream()));
+    s_in = k.d(oSw);
+  }
+  const int ui = static_cast<int>(u), K = static_cast<int>(cfg.t_max), nci = static_cast<int>(nc);
+  const int Si = static_cast<int>(S);
+  float* gp = k.d<float>(oGP);
+  if (uniform) {
+    Engine::check(dcdg_dl_precode(eng.ctx(), k.d(oH), s_in, Si, nci, nci,
+                                  static_cast<int>(dev_rows(blocks[0][0].cols(), dp.fmt)), ui, K, cfg.rho, dp.fmt,
+                                  k.d(oX), dp.round_messages ? nullptr : gp, nullptr, eng.stream()));
+    if (dp.round_messages)
+      Engine::check(dcdg_gain_part(eng.ctx(), k.d(oH), k.d(oX), k.d(oS), Si, nci,
+                                   static_cast<int>(dev_rows(blocks[0][0].cols(), dp.fmt)), ui, dp.fmt, gp,
+                                   eng.stream()));
   } else {
     // each cluster is its own launch; rho/sqrt(C) is applied with C = nc
     const double rho_1 = cfg.rho / std::sqrt(static_cast<double>(nc));
-    for (std::size_t c = 0; c < nc; ++c)
-      Engine::check(dcdg_dl_precode(eng.ctx(), static_cast<unsigned char*>(dh.p) + hoff[c], ds.p, 1, 1, 1,
-                                    static_cast<int>(dev_rows(h_dl_blocks[c].cols(), dp.fmt)), ui, K, rho_1, dp.fmt,
-                                    static_cast<unsigned char*>(dx.p) + xoff[c], dgp.as<float>() + c, nullptr,
-                                    eng.stream()));
+    for (std::size_t c = 0; c < nc; ++c) {
+      const int bc = static_cast<int>(dev_rows(blocks[0][c].cols(), dp.fmt));
+      Engine::check(dcdg_dl_precode(eng.ctx(), k.d(oH + hoff[c]), s_in, 1, 1, 1, bc, ui, K, rho_1, dp.fmt,
+                                    k.d(oX + xoff[c]), dp.round_messages ? nullptr : gp + c, nullptr, eng.stream()));
+      if (dp.round_messages)
+        Engine::check(dcdg_gain_part(eng.ctx(), k.d(oH + hoff[c]), k.d(oX + xoff[c]), k.d(oS), 1, 1, bc, ui, dp.fmt,
+                                     gp + c, eng.stream()));
+    }
   }
-  Engine::check(dcdg_gain_reduce(eng.ctx(), dgp.as<float>(), ds.p, 1, nci, ui, dp.fmt, dg.as<float>(), eng.stream()));
-  float gain = 0.f;
-  d2h(xb.data(), dx.p, xbytes, eng.stream());
-  d2h(&gain, dg.p, sizeof gain, eng.stream());
+  Engine::check(dcdg_gain_reduce(eng.ctx(), gp, k.d(oS), Si, nci, ui, dp.fmt, k.d<float>(oG), eng.stream()));
+  k.download(L);
   eng.sync();
 
-  PrecodeResult res;
-  res.blocks.resize(nc);
-  res.x.reserve(btot);
-  for (std::size_t c = 0; c < nc; ++c) {
-    res.blocks[c].resize(h_dl_blocks[c].cols());
-    unpack(xb.data() + xoff[c], res.blocks[c].size(), dp.fmt, res.blocks[c].data());
-    res.x.insert(res.x.end(), res.blocks[c].begin(), res.blocks[c].end());
+  std::vector<PrecodeResult> out(S);
+  for (std::size_t s = 0; s < S; ++s) {
+    PrecodeResult& res = out[s];
+    res.blocks.resize(nc);
+    res.x.reserve(btot);
+    for (std::size_t c = 0; c < nc; ++c) {
+      res.blocks[c].resize(blocks[s][c].cols());
+      unpack(k.h(oX + s * xsub + xoff[c]), res.blocks[c].size(), dp.fmt, res.blocks[c].data());
+      res.x.insert(res.x.end(), res.blocks[c].begin(), res.blocks[c].end());
+    }
+    res.effective_gain = k.h<float>(oG)[s];
   }
-  res.effective_gain = gain;
-  return res;
+  return out;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Engine
+// ---------------------------------------------------------------------------
+void Engine::check(int status) {
+  if (status == DCDG_OK) return;
+  throw_status(status, dcdg_last_error());
+}
+
+Engine::Engine(int device) : device_(device), mu_(std::make_unique<std::mutex>()) {
+  check(dcdg_init(device, &ctx_));
+  // PrecisionMode{fp16, full_storage} mirrors the reference's fp16 arithmetic
+  // emulation: the half2 sweep kernel, not the fp32-arithmetic Gram kernel
+  check(dcdg_set_fp16_algorithm(ctx_, DCDG_ALG_SWEEP));
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    dcdg_destroy(ctx_);
+    throw std::runtime_error("dcd::gpu: stream creation failed");
+  }
+  stream_ = st;
+}
+
+Engine::~Engine() {
+  if (stream_) cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
+  if (dscratch_) cudaFree(dscratch_);
+  if (hstage_) cudaFreeHost(hstage_);
+  if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+  dcdg_destroy(ctx_);
+}
+
+void Engine::sync() { check(dcdg_sync_status(ctx_, stream_)); }
+
+namespace {
+std::size_t grow_to(std::size_t have, std::size_t need) {
+  std::size_t n = std::max<std::size_t>(have, 1 << 16);
+  while (n < need) n += n / 2;
+  return n;
+}
+}  // namespace
+
+void* Engine::device_scratch(std::size_t bytes) {
+  if (bytes <= dscratch_bytes_) return dscratch_;
+  const std::size_t n = grow_to(dscratch_bytes_, bytes);
+  cudaSetDevice(device_);
+  if (dscratch_) {
+    cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));  // the old buffer may still be in use
+    cudaFree(dscratch_);
+    dscratch_ = nullptr;
+    dscratch_bytes_ = 0;
+  }
+  if (cudaMalloc(&dscratch_, n) != cudaSuccess) {
+    dscratch_ = nullptr;
+    throw std::runtime_error("dcd::gpu: device allocation failed");
+  }
+  dscratch_bytes_ = n;
+  return dscratch_;
+}
+
+void* Engine::host_staging(std::size_t bytes) {
+  if (bytes <= hstage_bytes_) return hstage_;
+  const std::size_t n = grow_to(hstage_bytes_, bytes);
+  if (hstage_) {
+    cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
+    cudaFreeHost(hstage_);
+    hstage_ = nullptr;
+    hstage_bytes_ = 0;
+  }
+  if (cudaMallocHost(&hstage_, n) != cudaSuccess) {
+    hstage_ = nullptr;
+    throw std::runtime_error("dcd::gpu: pinned host allocation failed");
+  }
+  hstage_bytes_ = n;
+  return hstage_;
+}
+
+Engine& default_engine() {
+  thread_local Engine eng(0);
+  return eng;
+}
+
+// ---------------------------------------------------------------------------
+// uplink
+// ---------------------------------------------------------------------------
+ComplexVector cd_detect(const ComplexMatrix& h, const ComplexVector& y, double n0, double ex, unsigned t_max,
+                        const PrecisionMode& prec, SweepObserver* observer) {
+  return cd_detect(h, y, n0, ex, t_max, prec, observer, default_engine());
+}
+
+ComplexVector cd_detect(const ComplexMatrix& h, const ComplexVector& y, double n0, double ex, unsigned t_max,
+                        const PrecisionMode& prec, SweepObserver* observer, Engine& eng) {
+  check_system(h, y.size(), n0, ex);
+  if (t_max == 0) throw std::invalid_argument("cd_detect: need at least one sweep");
+  reject_observer(observer);
+  std::lock_guard<std::mutex> lk(eng.mutex());
+  const DevPrecision dp = map_precision(prec);
+  const std::size_t b = h.rows(), u = h.cols(), es = esize(dp.fmt), bd = dev_rows(b, dp.fmt);
+  Layout L;
+  const std::size_t oH = L.take(bd * u * es), oY = L.take(bd * es);
+  L.close_inputs();
+  const std::size_t oX = L.take(u * es);
+  Call k(eng, L);
+  pack_tile(h.flat().data(), b, u, dp.fmt, k.h(oH));
+  pack_tile(y.data(), b, 1, dp.fmt, k.h(oY));
+  k.upload(L);
+  Engine::check(dcdg_ul_detect(eng.ctx(), k.d(oH), k.d(oY), 1, 1, 1, static_cast<int>(bd), static_cast<int>(u),
+                               static_cast<int>(t_max), n0, ex, dp.fmt, DCDG_FUSION_UNIFORM, k.d(oX), nullptr, nullptr,
+                               nullptr, eng.stream()));
+  k.download(L);
+  eng.sync();
+  ComplexVector x(u);
+  unpack(k.h(oX), u, dp.fmt, x.data());
+  return x;
+}
+
+double post_eq_variance(const ComplexMatrix& hc, double n0, double ex) {
+  return post_eq_variance(hc, n0, ex, default_engine());
+}
+
+double post_eq_variance(const ComplexMatrix& hc, double n0, double ex, Engine& eng) {
+  if (hc.rows() == 0 || hc.cols() == 0) throw std::invalid_argument("post_eq_variance: empty channel block");
+  if (!(n0 > 0.0) || !(ex > 0.0)) throw std::invalid_argument("post_eq_variance: need N0 > 0 and E_x > 0");
+  std::lock_guard<std::mutex> lk(eng.mutex());
+  const std::size_t b = hc.rows(), u = hc.cols();
+  Layout L;
+  const std::size_t oH = L.take(b * u * 8);
+  L.close_inputs();
+  const std::size_t oS = L.take(sizeof(float));
+  Call k(eng, L);
+  pack(hc.flat().data(), b * u, DCDG_FP32, k.h(oH));
+  k.upload(L);
+  Engine::check(dcdg_post_eq_variance(eng.ctx(), k.d(oH), 1, static_cast<int>(b), static_cast<int>(u), n0, ex,
+                                      DCDG_FP32, k.d<float>(oS), eng.stream()));
+  k.download(L);
+  eng.sync();
+  return *k.h<float>(oS);
+}
+
+std::vector<double> fusion_weights(std::span<const double> sigma2) { return fusion_weights(sigma2, default_engine()); }
+
+std::vector<double> fusion_weights(std::span<const double> sigma2, Engine& eng) {
+  if (sigma2.empty()) throw std::invalid_argument("fusion_weights: no clusters");
+  for (double v : sigma2)
+    if (!(v > 0.0) || !std::isfinite(v))
+      throw std::invalid_argument("fusion_weights: variances must be positive and finite");
+  std::lock_guard<std::mutex> lk(eng.mutex());
+  const int c = static_cast<int>(sigma2.size());
+  Layout L;
+  const std::size_t oS = L.take(c * sizeof(float));
+  L.close_inputs();
+  const std::size_t oW = L.take(c * sizeof(float));
+  Call k(eng, L);
+  std::copy(sigma2.begin(), sigma2.end(), k.h<float>(oS));
+  k.upload(L);
+  Engine::check(dcdg_fusion_weights(eng.ctx(), k.d<float>(oS), 1, c, k.d<float>(oW), eng.stream()));
+  k.download(L);
+  eng.sync();
+  return {k.h<float>(oW), k.h<float>(oW) + c};
+}
+
+DetectionResult decentralized_cd_detect(std::span<const ClusterData> clusters, const DetectorConfig& cfg,
+                                        bool concurrent) {
+  return decentralized_cd_detect(clusters, cfg, concurrent, default_engine());
+}
+
+DetectionResult decentralized_cd_detect(std::span<const ClusterData> clusters, const DetectorConfig& cfg,
+                                        bool /*concurrent: all clusters run in one launch*/, Engine& eng) {
+  const std::size_t u = check_detect_call(clusters, cfg);
+  std::lock_guard<std::mutex> lk(eng.mutex());
+  const ClusterSpan one[1] = {clusters};
+  return std::move(detect_impl(one, u, cfg, eng)[0]);
+}
+
+std::vector<DetectionResult> decentralized_cd_detect_batch(std::span<const std::vector<ClusterData>> subcarriers,
+                                                           const DetectorConfig& cfg, Engine& eng) {
+  if (subcarriers.empty()) return {};
+  std::size_t u = 0;
+  for (const auto& sc : subcarriers) u = check_detect_call(sc, cfg);
+  // one launch when every subcarrier has the first one's cluster shapes and
+  // those are uniform; otherwise subcarrier by subcarrier
+  const auto& first = subcarriers[0];
+  bool same = uniform_rows(first);
+  for (const auto& sc : subcarriers) {
+    if (!same) break;
+    same = sc.size() == first.size() && sc[0].h.cols() == first[0].h.cols();
+    for (std::size_t c = 0; same && c < sc.size(); ++c) same = sc[c].h.rows() == first[c].h.rows();
+  }
+  const std::vector<ClusterSpan> subs(subcarriers.begin(), subcarriers.end());
+  std::lock_guard<std::mutex> lk(eng.mutex());
+  if (same) return detect_impl(subs, u, cfg, eng);
+  std::vector<DetectionResult> out;
+  out.reserve(subs.size());
+  for (std::size_t s = 0; s < subs.size(); ++s)
+    out.push_back(std::move(detect_impl(std::span<const ClusterSpan>(subs).subspan(s, 1), subs[s][0].h.cols(), cfg,
+                                        eng)[0]));
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// downlink
+// ---------------------------------------------------------------------------
+ComplexVector cd_precode(const ComplexMatrix& h_dl, const ComplexVector& s, unsigned t_max,
+                         const PrecisionMode& prec, SweepObserver* observer) {
+  return cd_precode(h_dl, s, t_max, prec, observer, default_engine());
+}
+
+ComplexVector cd_precode(const ComplexMatrix& h_dl, const ComplexVector& s, unsigned t_max,
+                         const PrecisionMode& prec, SweepObserver* observer, Engine& eng) {
+  check_downlink(h_dl, s);
+  if (t_max == 0) throw std::invalid_argument("cd_precode: need at least one sweep");
+  reject_observer(observer);
+  std::lock_guard<std::mutex> lk(eng.mutex());
+  const DevPrecision dp = map_precision(prec);
+  const std::size_t u = h_dl.rows(), b = h_dl.cols(), es = esize(dp.fmt), bd = dev_rows(b, dp.fmt);
+  Layout L;
+  const std::size_t oH = L.take(bd * u * es), oS = L.take(u * es);
+  L.close_inputs();
+  const std::size_t oX = L.take(bd * es);
+  Call k(eng, L);
+  std::vector<cf64> tile(b * u);
+  uplink_tile_of(h_dl, tile.data());
+  pack_tile(tile.data(), b, u, dp.fmt, k.h(oH));
+  pack(s.data(), u, dp.fmt, k.h(oS));
+  k.upload(L);
+  // rho == 0: unnormalised beamformer, exactly what cd_precode returns
+  Engine::check(dcdg_dl_precode(eng.ctx(), k.d(oH), k.d(oS), 1, 1, 1, static_cast<int>(bd), static_cast<int>(u),
+                                static_cast<int>(t_max), 0.0, dp.fmt, k.d(oX), nullptr, nullptr, eng.stream()));
+  k.download(L);
+  eng.sync();
+  ComplexVector x(b);
+  unpack(k.h(oX), b, dp.fmt, x.data());
+  return x;
+}
+
+void power_scale(ComplexVector& x, double rho) { power_scale(x, rho, default_engine()); }
+
+void power_scale(ComplexVector& x, double rho, Engine& eng) {
+  if (!(rho > 0.0)) throw std::invalid_argument("power_scale: amplitude must be positive");
+  if (x.empty()) throw std::invalid_argument("power_scale: empty beamformer");
+  std::lock_guard<std::mutex> lk(eng.mutex());
+  Layout L;
+  const std::size_t oX = L.take(x.size() * 8);
+  L.close_inputs();
+  Call k(eng, L);
+  pack(x.data(), x.size(), DCDG_FP32, k.h(oX));
+  k.upload(L);
+  Engine::check(dcdg_power_scale(eng.ctx(), k.d(oX), 1, static_cast<int>(x.size()), rho, DCDG_FP32, eng.stream()));
+  d2h(k.h(oX), k.d(oX), x.size() * 8, eng.stream());  // in place: the result comes back over the input
+  eng.sync();
+  unpack(k.h(oX), x.size(), DCDG_FP32, x.data());
+}
+
+PrecodeResult decentralized_cd_precode(std::span<const ComplexMatrix> h_dl_blocks, const ComplexVector& s,
+                                       const PrecoderConfig& cfg, bool concurrent) {
+  return decentralized_cd_precode(h_dl_blocks, s, cfg, concurrent, default_engine());
+}
+
+PrecodeResult decentralized_cd_precode(std::span<const ComplexMatrix> h_dl_blocks, const ComplexVector& s,
+                                       const PrecoderConfig& cfg, bool /*concurrent*/, Engine& eng) {
+  check_precode_call(h_dl_blocks, s, cfg);
+  std::lock_guard<std::mutex> lk(eng.mutex());
+  const BlockSpan one[1] = {h_dl_blocks};
+  return std::move(precode_impl(one, std::span<const ComplexVector>(&s, 1), cfg, eng)[0]);
+}
+
+std::vector<PrecodeResult> decentralized_cd_precode_batch(std::span<const std::vector<ComplexMatrix>> h_dl_blocks,
+                                                          std::span<const ComplexVector> s, const PrecoderConfig& cfg,
+                                                          Engine& eng) {
+  if (h_dl_blocks.size() != s.size())
+    throw std::invalid_argument("decentralized_cd_precode_batch: one symbol vector per subcarrier");
+  if (h_dl_blocks.empty()) return {};
+  for (std::size_t i = 0; i < s.size(); ++i) check_precode_call(h_dl_blocks[i], s[i], cfg);
+  const auto& first = h_dl_blocks[0];
+  bool same = uniform_cols(first);
+  for (std::size_t i = 0; same && i < s.size(); ++i) {
+    same = h_dl_blocks[i].size() == first.size() && s[i].size() == s[0].size();
+    for (std::size_t c = 0; same && c < first.size(); ++c) same = h_dl_blocks[i][c].cols() == first[c].cols();
+  }
+  const std::vector<BlockSpan> blocks(h_dl_blocks.begin(), h_dl_blocks.end());
+  std::lock_guard<std::mutex> lk(eng.mutex());
+  if (same) return precode_impl(blocks, s, cfg, eng);
+  std::vector<PrecodeResult> out;
+  out.reserve(s.size());
+  for (std::size_t i = 0; i < s.size(); ++i)
+    out.push_back(std::move(precode_impl(std::span<const BlockSpan>(blocks).subspan(i, 1), s.subspan(i, 1), cfg,
+                                         eng)[0]));
+  return out;
 }
 
 // ---------------------------------------------------------------------------

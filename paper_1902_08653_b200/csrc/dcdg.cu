@@ -9,6 +9,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 #include <utility>
 
@@ -44,8 +47,11 @@ struct dcdg_xwin {
   unsigned char* peer[dcdg::kXchgMaxRanks] = {};
   bool opened[dcdg::kXchgMaxRanks] = {};
   unsigned int* counter = nullptr;
-  unsigned long long epoch = 0;     // uplink calls
-  unsigned long long dl_epoch = 0;  // downlink calls
+  // One epoch sequence for BOTH directions: parity = epoch & 1 alternates over
+  // the window's calls in issue order, so an uplink and a downlink call never
+  // reuse a parity buffer before every peer's wait of the call in between
+  // (which implies all consumers of the older call are done) — DESIGN §6.1.
+  unsigned long long epoch = 0;
   long long timeout_ns = 20000000000LL;  // 20 s: a missing peer becomes ST_XCHG_TIMEOUT, not a hang
 };
 
@@ -127,12 +133,26 @@ cudaError_t launch_dependent(void (*kern)(KArgs...), unsigned grid, unsigned blo
 // one-warp CTAs let occupancy follow the register budget exactly.
 constexpr int kWarps = DCDG_CTA_WARPS;
 
-template <typename Kern>
-int occupancy_of(Kern kern, size_t smem, int threads = 32 * kWarps) {
+// Resident CTAs per SM of a kernel on the context's device.  Function
+// attributes (the dynamic shared-memory opt-in) and occupancy are per device,
+// so both are cached per (device, kernel, smem, threads), never process-wide.
+int occupancy_cached(dcdg_ctx* ctx, const void* kern, size_t smem, int threads) {
+  using Key = std::tuple<int, const void*, size_t, int>;
+  static std::mutex mu;
+  static std::map<Key, int> cache;
+  const Key key{ctx->device, kern, smem, threads};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+  cache.emplace(key, occ);
   return occ;
+}
+template <typename Kern>
+int occupancy_of(dcdg_ctx* ctx, Kern kern, size_t smem, int threads = 32 * kWarps) {
+  return occupancy_cached(ctx, reinterpret_cast<const void*>(kern), smem, threads);
 }
 
 using UlLaunch = cudaError_t (*)(dcdg_ctx*, const void*, const void*, int, int, float, void*, const dcdg::XMap*,
@@ -163,8 +183,8 @@ cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, in
       dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U, LB), NPW, kWarps>::kBytes;
   auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps, MINB, LB, false>;
   auto kx = dcdg::ul_reg_f32<BC, U, G, kWarps, MINB, LB, true>;
-  static const int occ = occupancy_of(kern, smem);
-  static const int occx = occupancy_of(kx, smem);
+  const int occ = occupancy_of(ctx, kern, smem);
+  const int occx = occupancy_of(ctx, kx, smem);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * (xm ? occx : occ));
   (xm ? kx : kern)<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P,
@@ -180,8 +200,8 @@ cudaError_t launch_ul_f16(dcdg_ctx* ctx, const void* H, const void* Y, int P, in
       dcdg::CtaSmem<NPW*(BC * U * 4 + BC * 4), dcdg::ul_scal_bytes(U), NPW, kWarps>::kBytes;
   auto kern = dcdg::ul_reg_f16<BC, U, G, kWarps, MINB, false>;
   auto kx = dcdg::ul_reg_f16<BC, U, G, kWarps, MINB, true>;
-  static const int occ = occupancy_of(kern, smem);
-  static const int occx = occupancy_of(kx, smem);
+  const int occ = occupancy_of(ctx, kern, smem);
+  const int occx = occupancy_of(ctx, kx, smem);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * (xm ? occx : occ));
   (xm ? kx : kern)<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(Y),
@@ -197,7 +217,7 @@ cudaError_t launch_dl_f32_k(dcdg_ctx* ctx, const void* H, const void* S, int P, 
   constexpr size_t smem =
       dcdg::CtaSmem<NPW*(BC * U * 8 + U * 8), dcdg::dl_scal_bytes(U), NPW, kWarps>::kBytes;
   auto kern = dcdg::dl_reg_f32<BC, U, G, kWarps, MINB, GAIN>;
-  static const int occ = occupancy_of(kern, smem);
+  const int occ = occupancy_of(ctx, kern, smem);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
   kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(S), P, C, K, rho_c,
@@ -219,7 +239,7 @@ cudaError_t launch_dl_f16_k(dcdg_ctx* ctx, const void* H, const void* S, int P, 
   constexpr size_t smem =
       dcdg::CtaSmem<NPW*(BC * U * 4 + U * 4), dcdg::dl_scal_bytes(U), NPW, kWarps>::kBytes;
   auto kern = dcdg::dl_reg_f16<BC, U, G, kWarps, MINB, GAIN>;
-  static const int occ = occupancy_of(kern, smem);
+  const int occ = occupancy_of(ctx, kern, smem);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
   kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(S), P, C, K,
@@ -243,7 +263,7 @@ cudaError_t launch_ul_mw(dcdg_ctx* ctx, const void* H, const void* Y, int P, int
   constexpr size_t smem = dcdg::MwSmem<dcdg::ul_mw_slot_bytes(BC, U, NW), dcdg::ul_scal_bytes(U, LB), NW,
                                        dcdg::mw_setup_floats(U, LB), 2 * LB>::kBytes;
   auto kern = dcdg::ul_mw_f32<BC, U, NW, MINB, LB>;
-  static const int occ = occupancy_of(kern, smem, 32 * NW);
+  const int occ = occupancy_of(ctx, kern, smem, 32 * NW);
   const int blocks = std::min(P, ctx->sms * occ);
   kern<<<blocks, 32 * NW, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K, kappa,
                                       static_cast<float2*>(X));
@@ -256,7 +276,7 @@ cudaError_t launch_dl_mw_k(dcdg_ctx* ctx, const void* H, const void* S, int P, i
   constexpr size_t smem = dcdg::MwSmem<dcdg::dl_mw_slot_bytes(BC, U, NW), dcdg::dl_scal_bytes(U), NW,
                                        dcdg::mw_setup_floats(U, 2), 4>::kBytes;
   auto kern = dcdg::dl_mw_f32<BC, U, NW, MINB, GAIN>;
-  static const int occ = occupancy_of(kern, smem, 32 * NW);
+  const int occ = occupancy_of(ctx, kern, smem, 32 * NW);
   const int blocks = std::min(P, ctx->sms * occ);
   kern<<<blocks, 32 * NW, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(S), P, C, K, rho_c,
                                       static_cast<float2*>(X), gp, ctx->d_status);
@@ -280,7 +300,7 @@ cudaError_t launch_ul_split(dcdg_ctx* ctx, const void* H, const void* Y, int P, 
   constexpr int NPW = 32 / G;
   constexpr size_t smem = dcdg::split_cols_bytes(BC, U, JR, G) + NPW * dcdg::ul_scal_bytes(U, 2);
   auto kern = dcdg::ul_split_f32<BC, U, G, JR, MINB, 1>;
-  static const int occ = occupancy_of(kern, smem, 32);
+  const int occ = occupancy_of(ctx, kern, smem, 32);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min(nsets, ctx->sms * occ);
   kern<<<blocks, 32, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K, kappa,
@@ -294,7 +314,7 @@ cudaError_t launch_dl_split_k(dcdg_ctx* ctx, const void* H, const void* S, int P
   constexpr int NPW = 32 / G;
   constexpr size_t smem = dcdg::split_cols_bytes(BC, U, JR, G) + NPW * dcdg::dl_scal_bytes(U);
   auto kern = dcdg::dl_split_f32<BC, U, G, JR, MINB, GAIN>;
-  static const int occ = occupancy_of(kern, smem, 32);
+  const int occ = occupancy_of(ctx, kern, smem, 32);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min(nsets, ctx->sms * occ);
   kern<<<blocks, 32, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(S), P, C, K, rho_c,
@@ -429,13 +449,13 @@ int launch_ul_gram(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, fl
   const int nsets = (P + NPW - 1) / NPW;
   if (sigma2) {
     auto kern = dcdg::ul_gram_f16<U, NPW, DCDG_GRAM_SIG_MINB, true>;
-    static const int occ = occupancy_of(kern, L::kAlloc, 32);
+    const int occ = occupancy_of(ctx, kern, L::kAlloc, 32);
     const int blocks = std::min(nsets, ctx->sms * occ);
     kern<<<blocks, 32, L::kAlloc, st>>>(map, static_cast<const __half2*>(Y), P, K, kappa, static_cast<__half2*>(X),
                                         sigma2, gam, scale, ctx->d_status);
   } else {
     auto kern = dcdg::ul_gram_f16<U, NPW, DCDG_GRAM_MINB, false>;
-    static const int occ = occupancy_of(kern, L::kAlloc, 32);
+    const int occ = occupancy_of(ctx, kern, L::kAlloc, 32);
     const int blocks = std::min(nsets, ctx->sms * occ);
     kern<<<blocks, 32, L::kAlloc, st>>>(map, static_cast<const __half2*>(Y), P, K, kappa, static_cast<__half2*>(X),
                                         nullptr, 0.f, 0.f, nullptr);
@@ -464,7 +484,7 @@ int launch_dl_gram(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, in
 #define DL_GRAM(GAIN)                                                                                              \
   {                                                                                                                \
     auto kern = dcdg::dl_gram_f16<U, NPW, DCDG_GRAM_MINB, GAIN>;                                                   \
-    static const int occ = occupancy_of(kern, L::kAlloc, 32);                                                      \
+    const int occ = occupancy_of(ctx, kern, L::kAlloc, 32);                                                      \
     const int blocks = std::min(nsets, ctx->sms * occ);                                                           \
     kern<<<blocks, 32, L::kAlloc, st>>>(map, static_cast<const __half2*>(H), static_cast<const __half2*>(S), P, C, K, \
                                         rho_c, static_cast<__half2*>(X), gp, ctx->d_status);                       \
@@ -576,9 +596,7 @@ template <typename T, int BT>
 int launch_pev16(dcdg_ctx* ctx, const void* H, int P, float gam, float scale, bool rnd, float* s2, cudaStream_t st) {
   constexpr size_t smem = 4 * (2 * 16 * (BT + 1) + 2 * 16 * 16) * sizeof(float2);
   auto k = dcdg::pev16_pair_kernel<T, BT>;
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  (void)attr;
+  occupancy_of(ctx, k, smem, 128);  // sets the shared-memory opt-in on this device (cached per device)
   k<<<(P + 7) / 8, 128, smem, st>>>(static_cast<const T*>(H), P, gam, scale, rnd, s2, ctx->d_status);
   ++ctx->launches;
   CUDA_TRY(cudaGetLastError(), "post_eq_variance launch");
@@ -752,6 +770,8 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
   if (fusion != DCDG_FUSION_OPTIMAL && fusion != DCDG_FUSION_UNIFORM)
     return fail(DCDG_EINVAL, "dcdg_ul_detect: unknown fusion mode");
   if (optimal && !(n0 > 0.0)) return fail(DCDG_EINVAL, "post_eq_variance: need N0 > 0 and E_x > 0");
+  // the variance kernels factorise U x U Grams with one lane per row
+  if (optimal && U > 32) return fail(DCDG_EINVAL, "dcdg_post_eq_variance: U > 32 not supported");
   if (!H || !y) return fail(DCDG_EINVAL, "dcdg_ul_detect: null input buffer");
   const long long P = static_cast<long long>(S) * C;
   if (P > 0x7fffffffLL) return fail(DCDG_EINVAL, "dcdg_ul_detect: batch too large (S*C must fit in int32)");
@@ -889,6 +909,33 @@ int dcdg_fuse(dcdg_ctx* ctx, const void* x_local, const float* sigma2, int S, in
   if (S <= 0) return DCDG_OK;
   CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
   return launch_fuse(ctx, x_local, sigma2, S, C, C_total, U, fmt, optimal, xhat, wsum, as_stream(stream));
+}
+
+int dcdg_gain_part(dcdg_ctx* ctx, const void* H, const void* x_dl, const void* s, int S, int C, int Bc, int U, int fmt,
+                   float* gain_part, void* stream) {
+  if (int rc = check_fmt(fmt)) return rc;
+  if (C <= 0 || S < 0 || Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "dcdg_gain_part: empty batch");
+  if (!H || !x_dl || !s || !gain_part) return fail(DCDG_EINVAL, "dcdg_gain_part: null buffer");
+  const long long P = static_cast<long long>(S) * C;
+  if (P > 0x7fffffffLL) return fail(DCDG_EINVAL, "dcdg_gain_part: batch too large (S*C must fit in int32)");
+  if (int rc = check_ctx(ctx)) return rc;
+  if (P == 0) return DCDG_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const unsigned blocks = static_cast<unsigned>((P + 3) / 4);
+  cudaStream_t st = as_stream(stream);
+  if (fmt == DCDG_FP16)
+    dcdg::gain_part_kernel<__half2><<<blocks, 128, 0, st>>>(static_cast<const __half2*>(H),
+                                                            static_cast<const __half2*>(x_dl),
+                                                            static_cast<const __half2*>(s), static_cast<int>(P), C, Bc,
+                                                            U, gain_part);
+  else
+    dcdg::gain_part_kernel<float2><<<blocks, 128, 0, st>>>(static_cast<const float2*>(H),
+                                                           static_cast<const float2*>(x_dl),
+                                                           static_cast<const float2*>(s), static_cast<int>(P), C, Bc, U,
+                                                           gain_part);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "gain_part launch");
+  return DCDG_OK;
 }
 
 int dcdg_fuse_finalize(dcdg_ctx* ctx, float* xhat, const float* wsum, int S, int U, void* stream) {
@@ -1268,6 +1315,7 @@ int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* 
   if (fusion != DCDG_FUSION_OPTIMAL && fusion != DCDG_FUSION_UNIFORM)
     return fail(DCDG_EINVAL, "dcdg_ul_detect: unknown fusion mode");
   if (optimal && !(n0 > 0.0)) return fail(DCDG_EINVAL, "post_eq_variance: need N0 > 0 and E_x > 0");
+  if (optimal && U > 32) return fail(DCDG_EINVAL, "dcdg_post_eq_variance: U > 32 not supported");
   if (!w) return fail(DCDG_EINVAL, "dcdg_ul_detect_xchg: null exchange window");
   if (c0 < 0 || c0 + C > C_total) return fail(DCDG_EINVAL, "dcdg_ul_detect_xchg: clusters [c0, c0+C) outside C_total");
   if (S % w->world) return fail(DCDG_EINVAL, "dcdg_ul_detect_xchg: S must divide over the ranks");
@@ -1384,7 +1432,7 @@ int dcdg_dl_precode_xchg(dcdg_ctx* ctx, dcdg_xwin* w, int root, const void* H, c
   dcdg::XMap m{};
   for (int q = 0; q < w->world; ++q) m.win[q] = w->peer[q];
   m.counter = w->counter;
-  m.epoch = ++w->dl_epoch;
+  m.epoch = ++w->epoch;
   m.buf_bytes = w->buf_bytes;
   m.sig_off = gain_off;
   m.world = w->world;

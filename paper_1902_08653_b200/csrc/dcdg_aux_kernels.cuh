@@ -1243,6 +1243,36 @@ __global__ void __launch_bounds__(128) dl_receive_kernel(const T* __restrict__ H
   }
 }
 
+// Per-cluster effective-gain share of finished beamformers (assemble_blocks,
+// precode.cpp:123-131): part[p] = Re(s^H H_dl,c x_c) = Re(sum_u conj(s_u) h_u^H x_c),
+// one warp per problem, lane u.  Used where the precoding kernel saw a
+// different s than the gain needs (fp16 messages_only: the clusters receive
+// the rounded broadcast, the gain uses the centre's own s).
+template <typename T>
+__global__ void __launch_bounds__(128) gain_part_kernel(const T* __restrict__ H, const T* __restrict__ X,
+                                                        const T* __restrict__ Sy, int P, int C, int BC, int U,
+                                                        float* __restrict__ part) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long p = static_cast<long long>(blockIdx.x) * 4 + warp;
+  if (p >= P) return;
+  const long long s = p / C;
+  const T* x = X + static_cast<size_t>(p) * BC;
+  float acc = 0.f;
+  for (int u = lane; u < U; u += 32) {
+    const T* h = H + (static_cast<size_t>(p) * U + u) * BC;  // column u of the tile
+    float yr = 0.f, yi = 0.f;
+    for (int b = 0; b < BC; ++b) {
+      const float2 hv = ldv(h, b), xv = ldc(x, b);
+      yr = fmaf(hv.x, xv.x, fmaf(hv.y, xv.y, yr));
+      yi = fmaf(hv.x, xv.y, fmaf(-hv.y, xv.x, yi));
+    }
+    const float2 sv = ldc(Sy, static_cast<size_t>(s) * U + u);
+    acc = fmaf(sv.x, yr, fmaf(sv.y, yi, acc));
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) part[p] = acc;
+}
+
 __global__ void fill_kernel(float* __restrict__ x, long long n, float v) {
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)

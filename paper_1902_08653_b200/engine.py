@@ -145,6 +145,11 @@ class Engine:
         if alg not in codes:
             raise ValueError(f"unknown fp16 algorithm {alg!r}")
         check(lib().dcdg_set_fp16_algorithm(self._ctx, codes[alg]))
+        self._fp16_alg = alg
+
+    @property
+    def fp16_algorithm(self) -> str:
+        return getattr(self, "_fp16_alg", "gram")
 
     def kernel_name(self, direction: int, bc: int, u: int, fmt: int) -> str:
         """Kernel this context dispatches a (direction, B_c, U, fmt) batch to."""

@@ -29,6 +29,7 @@ agree statistically, not bit for bit; the bit-exact parity of the detection
 path itself is tested on the reference's own batches (tests/)."""
 from __future__ import annotations
 
+import contextlib
 import math
 from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
@@ -188,6 +189,23 @@ def curve_of(points: Sequence[BerPoint], method: str, t: int) -> List[Tuple[floa
 # ---------------------------------------------------------------------------
 # one point
 # ---------------------------------------------------------------------------
+@contextlib.contextmanager
+def _fp16_arithmetic(eng: Engine, full: bool):
+    """fp16 'full' scope measures the loss of fp16 ARITHMETIC (precision.cpp,
+    full_storage), so it runs the half2 sweep kernels, not the default
+    tensor-core Gram kernels (fp32 arithmetic on fp16 storage); the engine's
+    previous choice is restored afterwards."""
+    if not full:
+        yield
+        return
+    prev = eng.fp16_algorithm
+    eng.set_fp16_algorithm("sweep")
+    try:
+        yield
+    finally:
+        eng.set_fp16_algorithm(prev)
+
+
 def _uplink_chunk(eng: Engine, spec: SweepSpec, method: str, t: int, n0: float, S: int, first_trial: int):
     U, C, Bc = spec.users, spec.clusters, spec.cluster_size
     central = method == "cd"
@@ -209,7 +227,8 @@ def _uplink_chunk(eng: Engine, spec: SweepSpec, method: str, t: int, n0: float, 
                 eng.round_fp16(s2)
             xhat = eng.fuse(r.x_local, s2, fusion=spec.fusion)
         else:
-            xhat = eng.ul_detect(Hd, yd, n0=n0, ex=spec.ex, K=t, fusion=spec.fusion, want_local=False).xhat
+            with _fp16_arithmetic(eng, full):
+                xhat = eng.ul_detect(Hd, yd, n0=n0, ex=spec.ex, K=t, fusion=spec.fusion, want_local=False).xhat
     elif method == "exact":
         if fp16:
             eng.round_fp16(y)
@@ -232,7 +251,8 @@ def _downlink_chunk(eng: Engine, spec: SweepSpec, method: str, t: int, n0: float
     full = fp16 and spec.scope == "full"
     if method in ("dcd", "cd"):
         if full:
-            x = to_complex64(eng.dl_precode(to_fp16_pairs(H), to_fp16(sym), rho=rho, K=t, want_gain=False).x)
+            with _fp16_arithmetic(eng, full):
+                x = to_complex64(eng.dl_precode(to_fp16_pairs(H), to_fp16(sym), rho=rho, K=t, want_gain=False).x)
         else:
             s_in = sym.clone() if fp16 else sym
             if fp16:

@@ -177,10 +177,10 @@ def criterion_9(eng, S=67200, reps=10):
             "spread": spread, "subcarriers": S}
 
 
-def main():
-    eng = Engine(0)
+def criteria_3_to_5(eng):
+    """Criteria 3-5 on the reference's sweep spec (acceptance.cpp:180-260):
+    returns ({3: .., 4: .., 5: ..}, curves, points)."""
     results = {}
-    t0 = time.time()
     ul = SweepSpec(direction="uplink", methods=("dcd", "exact", "mf"), users=8, cluster_size=32, clusters=4,
                    snr_db=(2, 3, 4, 5, 6, 7, 8), t_max=(3, 4), min_bits=1_000_000, seed=71)
     pts = run_ber_sweep(ul, eng)
@@ -188,7 +188,6 @@ def main():
     pts200 = run_ber_sweep(ul200, eng)
     dl = dataclasses.replace(ul, direction="downlink", methods=("dcd", "exact", "mf"), t_max=(3,))
     dpts = run_ber_sweep(dl, eng)
-    t_main = time.time() - t0
 
     curves = {"ul_dcd3": curve_of(pts, "dcd", 3), "ul_dcd4": curve_of(pts, "dcd", 4),
               "ul_exact": curve_of(pts, "exact", 0), "ul_mf": curve_of(pts, "mf", 0),
@@ -210,15 +209,28 @@ def main():
     c4, c200 = snr_at_ber(curves["ul_dcd4"], 1e-3), snr_at_ber(curves["ul_dcd200"], 1e-3)
     ok5 = math.isfinite(c4 - c200) and abs(c4 - c200) <= 0.5
     results[5] = {"pass": ok5, "t4_db": c4, "t200_db": c200, "gap_db": c4 - c200}
-    # 6: binary16 full-storage penalty <= 0.3 dB (acceptance.cpp:265-291)
-    t1 = time.time()
+    return results, curves, pts + pts200 + dpts
+
+
+def criterion_6(eng):
+    """binary16 full-storage penalty <= 0.3 dB (acceptance.cpp:265-291); the
+    fp16 'full' scope runs the half2 sweep kernels (fp16 arithmetic)."""
     s6 = SweepSpec(direction="uplink", methods=("dcd",), users=8, cluster_size=32, clusters=2,
                    snr_db=(6, 7, 8, 9, 10, 11, 12), t_max=(3,), min_bits=1_000_000, seed=73)
     c64 = snr_at_ber(curve_of(run_ber_sweep(s6, eng), "dcd", 3), 1e-3)
     c16 = snr_at_ber(curve_of(run_ber_sweep(dataclasses.replace(s6, precision="fp16", scope="full"), eng), "dcd", 3),
                      1e-3)
     ok6 = math.isfinite(c16 - c64) and c16 - c64 <= 0.3
-    results[6] = {"pass": ok6, "fp16_db": c16, "fp64_db": c64, "gap_db": c16 - c64}
+    return {"pass": ok6, "fp16_db": c16, "fp64_db": c64, "gap_db": c16 - c64}
+
+
+def main():
+    eng = Engine(0)
+    t0 = time.time()
+    results, curves, all_pts = criteria_3_to_5(eng)
+    t_main = time.time() - t0
+    t1 = time.time()
+    results[6] = criterion_6(eng)
     t6 = time.time() - t1
 
     t_other = time.time()
@@ -239,10 +251,10 @@ def main():
         r = results[k]
         detail = ", ".join(f"{a}={v:.3g}" if isinstance(v, float) else f"{a}={v}" for a, v in r.items() if a != "pass")
         print(f"[{'PASS' if r['pass'] else 'FAIL'}] {k}: {names[k]} ({detail})")
-    device_s = sum(p.seconds for p in pts + pts200 + dpts)
+    device_s = sum(p.seconds for p in all_pts)
     summary = {"criteria": results, "wall_s_criteria_3_5": t_main, "wall_s_criterion_6": t6,
                "wall_s_criteria_1_2_7_8_9": t_other,
-               "device_s_criteria_3_5": device_s, "points": len(pts) + len(pts200) + len(dpts),
+               "device_s_criteria_3_5": device_s, "points": len(all_pts),
                "curves": curves,
                "reference_cpu_probe": {"acceptance_total_s": 273, "ul_gap_db": 1.42, "dl_gap_db": 0.90,
                                        "fp16_gap_db": 0.00, "source": "SURVEY.md §4 (criteria 1-9, 8-core host)"}}

@@ -11,6 +11,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "dcd_gpu.hpp"
@@ -20,6 +21,7 @@ using dcd::gpu::cf64;
 using dcd::gpu::ClusterData;
 using dcd::gpu::ComplexMatrix;
 using dcd::gpu::ComplexVector;
+using dcd::gpu::DetectionResult;
 using dcd::gpu::DetectorConfig;
 using dcd::gpu::FusionMode;
 using dcd::gpu::PrecisionFormat;
@@ -476,6 +478,115 @@ TEST_CASE("exchange window (world 1) reproduces the batched detector and precode
   CHECK(std::memcmp(ga.data(), gb.data(), ga.size() * 4) == 0);
   CHECK(throws_with<std::invalid_argument>([&] { dcd::gpu::ExchangeWindow bad(eng, 3, 0, S, C, U, DCDG_FP32); },
                                            "S must divide over the ranks"));
+}
+
+// ---------------------------------------------------------------- batched round API
+namespace {
+std::vector<ClusterData> random_clusters(int C, int Bc, int U) {
+  std::vector<ClusterData> cl(C);
+  for (auto& c : cl) {
+    c.h = random_matrix(Bc, U);
+    c.y = random_vector(Bc);
+  }
+  return cl;
+}
+bool same_bits(const ComplexVector& a, const ComplexVector& b) {
+  return a.size() == b.size() && std::memcmp(a.data(), b.data(), a.size() * sizeof(cf64)) == 0;
+}
+}  // namespace
+
+TEST_CASE("batched detection is bitwise the per-subcarrier calls (both fusions)", t_ul_batch) {
+  const int S = 6, C = 8, Bc = 32, U = 16;
+  std::vector<std::vector<ClusterData>> subs;
+  for (int s = 0; s < S; ++s) subs.push_back(random_clusters(C, Bc, U));
+  for (FusionMode f : {FusionMode::uniform, FusionMode::optimal}) {
+    DetectorConfig cfg;
+    cfg.n0 = 1.6;
+    cfg.fusion = f;
+    const auto all = dcd::gpu::decentralized_cd_detect_batch(subs, cfg);
+    CHECK(all.size() == static_cast<std::size_t>(S));
+    for (int s = 0; s < S; ++s) {
+      const auto one = dcd::gpu::decentralized_cd_detect(subs[s], cfg);
+      CHECK(same_bits(all[s].xhat, one.xhat));
+      for (int c = 0; c < C; ++c) CHECK(same_bits(all[s].local[c], one.local[c]));
+      CHECK(all[s].weights == one.weights);
+      CHECK(all[s].sigma2 == one.sigma2);
+    }
+  }
+  // the reference's checks per subcarrier, in its order
+  subs[3][2].y.pop_back();
+  CHECK(throws_with<std::invalid_argument>(
+      [&] { dcd::gpu::decentralized_cd_detect_batch(subs, DetectorConfig{}); },
+      "detector: observation length must match antenna count"));
+}
+
+TEST_CASE("batched detection with uneven clusters falls back per subcarrier", t_ul_batch_uneven) {
+  std::vector<std::vector<ClusterData>> subs;
+  for (int s = 0; s < 3; ++s) {
+    auto cl = random_clusters(2, 24, 6);
+    cl.push_back({random_matrix(20, 6), random_vector(20)});
+    subs.push_back(std::move(cl));
+  }
+  DetectorConfig cfg;
+  cfg.n0 = 0.4;
+  cfg.fusion = FusionMode::uniform;
+  const auto all = dcd::gpu::decentralized_cd_detect_batch(subs, cfg);
+  for (int s = 0; s < 3; ++s) CHECK(same_bits(all[s].xhat, dcd::gpu::decentralized_cd_detect(subs[s], cfg).xhat));
+}
+
+TEST_CASE("batched precoding is bitwise the per-subcarrier calls", t_dl_batch) {
+  const int S = 5, C = 8, Bc = 32, U = 16;
+  std::vector<std::vector<ComplexMatrix>> blocks(S);
+  std::vector<ComplexVector> syms;
+  for (int s = 0; s < S; ++s) {
+    for (int c = 0; c < C; ++c) blocks[s].push_back(random_matrix(Bc, U).hermitian());
+    syms.push_back(random_vector(U));
+  }
+  PrecoderConfig cfg;
+  cfg.rho = 4.0;
+  const auto all = dcd::gpu::decentralized_cd_precode_batch(blocks, syms, cfg);
+  for (int s = 0; s < S; ++s) {
+    const auto one = dcd::gpu::decentralized_cd_precode(blocks[s], syms[s], cfg);
+    CHECK(same_bits(all[s].x, one.x));
+    CHECK(all[s].effective_gain == one.effective_gain);
+  }
+}
+
+TEST_CASE("fp16 messages-only precoding: clusters get the rounded broadcast, the gain the centre's s", t_dl_msg16) {
+  const auto s = random_vector(8);
+  std::vector<ComplexMatrix> blocks;
+  std::vector<double> tiles;
+  for (int k = 0; k < 4; ++k) {
+    blocks.push_back(random_matrix(32, 8).hermitian());
+    for (auto z : blocks.back().flat()) tiles.insert(tiles.end(), {z.real(), z.imag()});
+  }
+  PrecoderConfig cfg;
+  cfg.rho = std::sqrt(8.0);
+  cfg.precision = {PrecisionFormat::fp16, PrecisionScope::messages_only};
+  const auto got = dcd::gpu::decentralized_cd_precode(blocks, s, cfg);
+  const int bc[4] = {32, 32, 32, 32};
+  ComplexVector want(128);
+  double gain = 0;
+  dcdo_decentralized_cd_precode(4, bc, 8, tiles.data(), reinterpret_cast<const double*>(s.data()), cfg.rho, 3, 2, 0,
+                                reinterpret_cast<double*>(want.data()), &gain);  // fmt fp16, messages_only
+  CHECK(rel_dist(got.x, want) <= kTol);
+  CHECK(std::abs(got.effective_gain - gain) <= kTol * std::abs(gain));
+}
+
+TEST_CASE("engines on separate host threads run concurrently and agree", t_threads) {
+  const auto subs = random_clusters(8, 32, 16);
+  DetectorConfig cfg;
+  cfg.n0 = 1.6;
+  cfg.fusion = FusionMode::uniform;
+  const auto want = dcd::gpu::decentralized_cd_detect(subs, cfg);
+  std::vector<DetectionResult> got(4);
+  std::vector<std::thread> ts;
+  for (int t = 0; t < 4; ++t)
+    ts.emplace_back([&, t] {
+      for (int i = 0; i < 20; ++i) got[t] = dcd::gpu::decentralized_cd_detect(subs, cfg);  // thread_local engine
+    });
+  for (auto& th : ts) th.join();
+  for (const auto& g : got) CHECK(same_bits(g.xhat, want.xhat));
 }
 
 int main() {

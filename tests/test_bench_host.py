@@ -44,3 +44,25 @@ def test_reference_arm_prints_the_contract_line():
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"] == {"value": line["value"], "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert line["config"]["B"] == 256 and line["config"]["U"] == 16 and line["config"]["C"] == 8
+
+
+@pytest.mark.skipif(not _ref_built(), reason="oracle/_ref (the reference built from source) is not built")
+def test_gpus_flag_relaunches_one_rank_per_gpu():
+    # `bench.py --gpus 2` outside torchrun re-executes itself under
+    # torch.distributed.run with 2 ranks; the reference arm prints from rank 0 only
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "3", "--cpu-seconds", "1"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    assert lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--no-cpu"],
+                         capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert out.returncode != 0
+    assert "WORLD_SIZE=3" in out.stderr

@@ -195,3 +195,61 @@ def test_ranks_on_one_gpu_bitwise(engine, tmp_path, world, fmt, fusion):
                 assert torch.equal(gain, want_dl.gain.cpu())
     msg = (tmp_path / "timeout.txt").read_text()
     assert "CudaError" in msg and "never published" in msg, msg
+
+
+def _alternate_main(rank, world, port_, out_dir):
+    """Uplink and downlink calls alternating on ONE window with no host sync in
+    between: both directions share the window's epoch/parity sequence, so a
+    call never overwrites a parity buffer a peer may still be reading."""
+    import torch.distributed as dist
+
+    from paper_1902_08653_b200 import Engine
+    from paper_1902_08653_b200.distributed import CudaCompute, DistributedCD, partition
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    C, BC, U, S = 8, 32, 16, 64
+    g = torch.Generator().manual_seed(5)
+    H = torch.randn((S, C, U, BC), dtype=torch.complex64, generator=g)
+    y = torch.randn((S, C, BC), dtype=torch.complex64, generator=g) * 2.0
+    sy = torch.randn((S, U), dtype=torch.complex64, generator=g)
+    part = partition(C, world, rank, S)
+    eng = Engine(0)
+    Hl = H[:, part.c_lo:part.c_hi].contiguous().cuda()
+    yl = y[:, part.c_lo:part.c_hi].contiguous().cuda()
+    syd = sy.cuda()
+    dcd = DistributedCD(part, CudaCompute(eng), mode="p2p")
+    ul, dl = [], []
+    for i in range(8):  # UL, DL, UL, DL, ... all enqueued, read back only at the end
+        ul.append(dcd.uplink(Hl, yl, n0=1.6, K=3, fusion="uniform" if i % 4 else "optimal").clone())
+        x, gain = dcd.downlink(Hl, dcd.broadcast_symbols(syd), rho=4.0, K=3)
+        dl.append((x.clone(), gain.clone()))
+    eng.sync()
+    torch.save({"ul": [u.cpu() for u in ul], "dl": [(x.cpu(), gn.cpu()) for x, gn in dl]},
+               os.path.join(out_dir, f"alt{rank}.pt"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_alternating_directions_share_one_window(engine, tmp_path, world):
+    import torch.multiprocessing as mp
+    mp.spawn(_alternate_main, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    C, BC, U, S = 8, 32, 16, 64
+    g = torch.Generator().manual_seed(5)
+    H = torch.randn((S, C, U, BC), dtype=torch.complex64, generator=g).cuda()
+    y = (torch.randn((S, C, BC), dtype=torch.complex64, generator=g) * 2.0).cuda()
+    sy = torch.randn((S, U), dtype=torch.complex64, generator=g).cuda()
+    want_u = _single(engine, H, y, fusion="uniform", n0=1.6).cpu()
+    want_o = _single(engine, H, y, fusion="optimal", n0=1.6).cpu()
+    want_dl = engine.dl_precode(H, sy, rho=4.0, K=3, want_gain=True)
+    engine.sync()
+    cl, so = C // world, S // world
+    for r in range(world):
+        got = torch.load(tmp_path / f"alt{r}.pt")
+        for i, u in enumerate(got["ul"]):
+            want = (want_u if i % 4 else want_o)[r * so:(r + 1) * so]
+            assert torch.equal(torch.view_as_real(u), torch.view_as_real(want)), (r, i)
+        for x, gain in got["dl"]:
+            assert torch.equal(torch.view_as_real(x), torch.view_as_real(want_dl.x[:, cl * r:cl * (r + 1)].cpu()))
+            assert torch.equal(gain, want_dl.gain.cpu())
