@@ -47,18 +47,21 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
         os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE)]
     if not force and not _stale(LIB, deps):
         return LIB
-    objs = []
+    objs, procs = [], []
     build_dir = os.path.join(PKG, "_build")
     os.makedirs(build_dir, exist_ok=True)
-    for src in sources():
+    for src in sources():  # the translation units compile in parallel
         obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = [nvcc(), "-x", "cu", *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
+        procs.append((cmd, subprocess.Popen(cmd)))
         objs.append(obj)
+    for cmd, proc in procs:
+        if proc.wait() != 0:
+            raise subprocess.CalledProcessError(proc.returncode, cmd)
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs, "-lcudart"]
     if verbose:
         print(" ".join(cmd))

@@ -188,7 +188,32 @@ cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, in
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * (xm ? occx : occ));
   (xm ? kx : kern)<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P,
-                                                       K, kappa, static_cast<float2*>(X), xm ? *xm : dcdg::XMap{});
+                                                       K, kappa, static_cast<float2*>(X), xm ? *xm : dcdg::XMap{},
+                                                       nullptr, 0.f, 0.f, nullptr);
+  return cudaGetLastError();
+}
+
+// Optimal fusion at the north-star tile (B_c = 32, U = 16, fp32): the CD
+// kernel with post_eq_variance fused (ul_reg_f32<..., SIG = true>): one pass
+// over H for the estimates and sigma^2.
+#ifndef DCDG_UL_SIG_MINB
+#define DCDG_UL_SIG_MINB 8
+#endif
+#ifndef DCDG_UL_SIG
+#define DCDG_UL_SIG 1
+#endif
+bool ul_sig_shape(int bc, int u, int fmt) { return DCDG_UL_SIG && fmt == DCDG_FP32 && bc == 32 && u == 16; }
+
+cudaError_t launch_ul_f32_sig(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                              float* s2, float gam, float scale, cudaStream_t st) {
+  constexpr int BC = 32, U = 16, G = 8, NPW = 32 / G, LB = 2;
+  constexpr size_t smem = dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U, LB), NPW, kWarps>::kBytes;
+  auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps, DCDG_UL_SIG_MINB, LB, false, true>;
+  const int occ = occupancy_of(ctx, kern, smem);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
+  kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K, kappa,
+                                          static_cast<float2*>(X), dcdg::XMap{}, s2, gam, scale, ctx->d_status);
   return cudaGetLastError();
 }
 
@@ -800,6 +825,10 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
     if (int rc = launch_ul_gram(ctx, H, y, static_cast<int>(P), K, kappa, x_local, st, optimal ? sigma2 : nullptr,
                                 static_cast<float>(ex / n0), static_cast<float>(ex / U)))
       return rc;
+  } else if (optimal && ul_sig_shape(Bc, U, fmt)) {
+    CUDA_TRY(launch_ul_f32_sig(ctx, H, y, static_cast<int>(P), K, kappa, x_local, sigma2, static_cast<float>(ex / n0),
+                               static_cast<float>(ex / U), st),
+             "ul_detect (fused variance) launch");
   } else if (spec) {
     CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, x_local, nullptr, st), "ul_detect launch");
   } else {
@@ -819,7 +848,7 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
     CUDA_TRY(cudaGetLastError(), "ul_generic launch");
   }
   ++ctx->launches;
-  if (optimal && !gram)  // the Gram kernel computed sigma^2 itself
+  if (optimal && !gram && !ul_sig_shape(Bc, U, fmt))  // the Gram / fused kernels computed sigma^2 themselves
     if (int rc = launch_post_eq(ctx, H, static_cast<int>(P), Bc, U, n0, ex, fmt, sigma2, st)) return rc;
   if (xhat)
     if (int rc = launch_fuse(ctx, x_local, sigma2, S, C, C_total, U, fmt, optimal, xhat, wsum, st)) return rc;

@@ -286,4 +286,172 @@ __device__ __forceinline__ void xchg_cta_done(const XMap& m) {
   }
 }
 
+// complex c -= a * b
+__device__ __forceinline__ void csub_mul(float& cr, float& ci, float ar, float ai, float br, float bi) {
+  cr = fmaf(-ar, br, fmaf(ai, bi, cr));
+  ci = fmaf(-ar, bi, fmaf(-ai, br, ci));
+}
+
+// post_eq_variance of a problem from the Gram rows its 8 lanes hold
+// (detect.cpp:112-130): sigma^2 = (E_x/U) tr (I + (E_x/N0) G)^-1.  The
+// inverse's trace comes from the sweep operator in place on the lanes' rows
+// (lane k: rows 2k, 2k+1 of A = I + gam G): pivot kk in ascending order, its
+// row broadcast through shared memory,
+//     d = a_kk,kk;  a_ij -= (a_i,kk / d) a_kk,j  (i, j != kk);
+//     a_i,kk <- a_i,kk / d;  a_kk,j <- a_kk,j / d;  a_kk,kk <- -1/d,
+// after which A holds -A^-1.  The pivots are the Cholesky pivots of the
+// reference's hermitian_solve, so its singularity test (d > 1e-14 max A_jj,
+// numerics.cpp:38-41,55-56) applies unchanged.  Returns tr A^-1 (on every lane
+// of the problem); `singular` is set on the lanes that saw a failing pivot.
+template <int U>
+__device__ __forceinline__ float gram_trace_inverse(float (&ar0)[U], float (&ai0)[U], float (&ar1)[U],
+                                                    float (&ai1)[U], int k, float gam, float4* prow,
+                                                    bool& singular) {
+  // A = I + gam G in place over the Gram rows (they are dead after the sweeps)
+#pragma unroll
+  for (int j = 0; j < U; ++j) {
+    ar0[j] = fmaf(gam, ar0[j], j == 2 * k ? 1.f : 0.f);
+    ai0[j] *= gam;
+    ar1[j] = fmaf(gam, ar1[j], j == 2 * k + 1 ? 1.f : 0.f);
+    ai1[j] *= gam;
+  }
+  float dmax = 0.f;
+#pragma unroll
+  for (int jp = 0; jp < U / 2; ++jp)
+    if (k == jp) dmax = fmaxf(ar0[2 * jp], ar1[2 * jp + 1]);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  const float floor_ = 1e-14f * dmax;
+#pragma unroll
+  for (int kk = 0; kk < U; ++kk) {
+    float4* slot = prow + (kk & 1) * (U / 2);  // alternating [U/2] float4 rows (pairs of entries)
+    if (k == kk / 2) {
+#pragma unroll
+      for (int j = 0; j < U / 2; ++j)
+        slot[j] = (kk & 1) ? make_float4(ar1[2 * j], ai1[2 * j], ar1[2 * j + 1], ai1[2 * j + 1])
+                           : make_float4(ar0[2 * j], ai0[2 * j], ar0[2 * j + 1], ai0[2 * j + 1]);
+    }
+    __syncwarp();
+    const float d = reinterpret_cast<const float*>(slot)[2 * kk];
+    if (!(d > floor_)) singular = true;
+    const float inv = __frcp_rn(d);
+    const bool piv0 = (2 * k == kk), piv1 = (2 * k + 1 == kk);
+    // pivot row: a_kk,j - (1 - 1/d) a_kk,j = a_kk,j / d with the same update
+    const float f0r = piv0 ? 1.f - inv : ar0[kk] * inv, f0i = piv0 ? 0.f : ai0[kk] * inv;
+    const float f1r = piv1 ? 1.f - inv : ar1[kk] * inv, f1i = piv1 ? 0.f : ai1[kk] * inv;
+#pragma unroll
+    for (int jq = 0; jq < U / 2; ++jq) {
+      const float4 v = slot[jq];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 2 * jq + h;
+        if (j == kk) continue;
+        const float br = h ? v.z : v.x, bi = h ? v.w : v.y;
+        csub_mul(ar0[j], ai0[j], f0r, f0i, br, bi);
+        csub_mul(ar1[j], ai1[j], f1r, f1i, br, bi);
+      }
+    }
+    ar0[kk] = piv0 ? -inv : f0r;
+    ai0[kk] = piv0 ? 0.f : f0i;
+    ar1[kk] = piv1 ? -inv : f1r;
+    ai1[kk] = piv1 ? 0.f : f1i;
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int jp = 0; jp < U / 2; ++jp)
+    if (k == jp) t = -(ar0[2 * jp] + ar1[2 * jp + 1]);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+
+// Shared-memory image of A = I + gam G for the paired sweep operator below:
+// row i, column pair jq (columns 2jq, 2jq+1) at float4 slot
+// i*U/2 + (jq ^ ((i >> 1) & 7)):
+//     (Re A[i][2jq], Re A[i][2jq+1], Im A[i][2jq], Im A[i][2jq+1]).
+// The XOR skew makes the 8 lanes' reads of rows 2k (or 2k+1) conflict-free.
+template <int U>
+__device__ __forceinline__ int apair_slot(int i, int jq) {
+  return i * (U / 2) + (jq ^ ((i >> 1) & 7));
+}
+
+// post_eq_variance from A = I + gam G held as COLUMN PAIRS
+// (detect.cpp:112-130): lane k of the problem's 8 lanes keeps rows 2k and
+// 2k+1 as R?r[jq] = (Re A[i][2jq], Re A[i][2jq+1]) and R?i[jq] likewise, so
+// every update of the sweep operator (same pivots and arithmetic as
+// gram_trace_inverse above) is 4 FFMA2 per column pair and row, the row's
+// coefficient a broadcast .F32 operand:
+//     a_ij -= (a_i,kk / d) a_kk,j   (i != kk; column kk is overwritten after).
+// The pivot row is broadcast through `prow` (2 x U/2 float4 per problem) in
+// the same column-pair layout.  Returns tr A^-1 on every lane of the problem;
+// `singular` as in gram_trace_inverse.
+template <int U>
+__device__ __forceinline__ float gram_trace_inverse_cpairs(float2 (&R0r)[U / 2], float2 (&R0i)[U / 2],
+                                                           float2 (&R1r)[U / 2], float2 (&R1i)[U / 2], int k,
+                                                           float4* prow, bool& singular) {
+  constexpr int NQ = U / 2;
+  float dmax = 0.f;
+#pragma unroll
+  for (int jq = 0; jq < NQ; ++jq)
+    if (k == jq) dmax = fmaxf(R0r[jq].x, R1r[jq].y);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  const float floor_ = 1e-14f * dmax;
+#pragma unroll
+  for (int kk = 0; kk < U; ++kk) {
+    const int h = kk & 1, qk = kk >> 1;  // owner's row h; the pivot column is in pair qk, half h
+    float4* slot = prow + h * NQ;        // alternating broadcast rows
+    if (k == qk) {
+#pragma unroll
+      for (int jq = 0; jq < NQ; ++jq) {
+        const float2 r = h ? R1r[jq] : R0r[jq], i = h ? R1i[jq] : R0i[jq];
+        slot[jq] = make_float4(r.x, r.y, i.x, i.y);
+      }
+    }
+    __syncwarp();
+    const float d = reinterpret_cast<const float*>(slot + qk)[h];
+    if (!(d > floor_)) singular = true;
+    const float inv = __frcp_rn(d);
+    const bool piv0 = (2 * k == kk), piv1 = (2 * k + 1 == kk);
+    // row coefficients f_i = a_i,kk / d; the pivot row's is 1 - 1/d (a_kk,j / d
+    // with the same update)
+    const float a0r = h ? R0r[qk].y : R0r[qk].x, a0i = h ? R0i[qk].y : R0i[qk].x;
+    const float a1r = h ? R1r[qk].y : R1r[qk].x, a1i = h ? R1i[qk].y : R1i[qk].x;
+    const float f0r = piv0 ? 1.f - inv : a0r * inv, f0i = piv0 ? 0.f : a0i * inv;
+    const float f1r = piv1 ? 1.f - inv : a1r * inv, f1i = piv1 ? 0.f : a1i * inv;
+#pragma unroll
+    for (int jq = 0; jq < NQ; ++jq) {
+      const float4 v = slot[jq];
+      const float2 br = make_float2(v.x, v.y), bi = make_float2(v.z, v.w);
+      // (ar + i ai) -= (fr + i fi)(br + i bi) over the column pair
+      R0r[jq] = ffma2(f0i, bi, ffma2(-f0r, br, R0r[jq]));
+      R0i[jq] = ffma2(-f0i, br, ffma2(-f0r, bi, R0i[jq]));
+      R1r[jq] = ffma2(f1i, bi, ffma2(-f1r, br, R1r[jq]));
+      R1i[jq] = ffma2(-f1i, br, ffma2(-f1r, bi, R1i[jq]));
+    }
+    // column kk: a_i,kk <- a_i,kk / d, the pivot's own entry -1/d
+    const float n0r = piv0 ? -inv : f0r, n0i = piv0 ? 0.f : f0i;
+    const float n1r = piv1 ? -inv : f1r, n1i = piv1 ? 0.f : f1i;
+    if (h) {
+      R0r[qk].y = n0r;
+      R0i[qk].y = n0i;
+      R1r[qk].y = n1r;
+      R1i[qk].y = n1i;
+    } else {
+      R0r[qk].x = n0r;
+      R0i[qk].x = n0i;
+      R1r[qk].x = n1r;
+      R1i[qk].x = n1i;
+    }
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int jq = 0; jq < NQ; ++jq)
+    if (k == jq) t = -(R0r[jq].x + R1r[jq].y);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
 }  // namespace dcdg

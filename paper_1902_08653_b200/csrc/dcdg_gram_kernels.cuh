@@ -112,11 +112,6 @@ __device__ __forceinline__ float4 pair_bcast(float4 v, int JP, int k, int base, 
 #endif
 }
 
-// complex c -= a * b
-__device__ __forceinline__ void csub_mul(float& cr, float& ci, float ar, float ai, float br, float bi) {
-  cr = fmaf(-ar, br, fmaf(ai, bi, cr));
-  ci = fmaf(-ar, bi, fmaf(-ai, br, ci));
-}
 
 // Tensor-core phase of a set (shared by the uplink and downlink kernels): the
 // Gram G = H^H H (and, with Z, the matched filter z = H^H y) of each of the
@@ -201,79 +196,6 @@ __device__ __forceinline__ void gram_tc_phase(unsigned char* sm, uint32_t sbase,
       ci[1] = zv.w;
     }
   }
-}
-
-// post_eq_variance of a problem from the Gram rows its 8 lanes hold
-// (detect.cpp:112-130): sigma^2 = (E_x/U) tr (I + (E_x/N0) G)^-1.  The
-// inverse's trace comes from the sweep operator in place on the lanes' rows
-// (lane k: rows 2k, 2k+1 of A = I + gam G): pivot kk in ascending order, its
-// row broadcast through shared memory,
-//     d = a_kk,kk;  a_ij -= (a_i,kk / d) a_kk,j  (i, j != kk);
-//     a_i,kk <- a_i,kk / d;  a_kk,j <- a_kk,j / d;  a_kk,kk <- -1/d,
-// after which A holds -A^-1.  The pivots are the Cholesky pivots of the
-// reference's hermitian_solve, so its singularity test (d > 1e-14 max A_jj,
-// numerics.cpp:38-41,55-56) applies unchanged.  Returns tr A^-1 (on every lane
-// of the problem); `singular` is set on the lanes that saw a failing pivot.
-template <int U>
-__device__ __forceinline__ float gram_trace_inverse(float (&ar0)[U], float (&ai0)[U], float (&ar1)[U],
-                                                    float (&ai1)[U], int k, float gam, float4* prow,
-                                                    bool& singular) {
-  // A = I + gam G in place over the Gram rows (they are dead after the sweeps)
-#pragma unroll
-  for (int j = 0; j < U; ++j) {
-    ar0[j] = fmaf(gam, ar0[j], j == 2 * k ? 1.f : 0.f);
-    ai0[j] *= gam;
-    ar1[j] = fmaf(gam, ar1[j], j == 2 * k + 1 ? 1.f : 0.f);
-    ai1[j] *= gam;
-  }
-  float dmax = 0.f;
-#pragma unroll
-  for (int jp = 0; jp < U / 2; ++jp)
-    if (k == jp) dmax = fmaxf(ar0[2 * jp], ar1[2 * jp + 1]);
-#pragma unroll
-  for (int o = 4; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-  const float floor_ = 1e-14f * dmax;
-#pragma unroll
-  for (int kk = 0; kk < U; ++kk) {
-    float4* slot = prow + (kk & 1) * (U / 2);  // alternating [U/2] float4 rows (pairs of entries)
-    if (k == kk / 2) {
-#pragma unroll
-      for (int j = 0; j < U / 2; ++j)
-        slot[j] = (kk & 1) ? make_float4(ar1[2 * j], ai1[2 * j], ar1[2 * j + 1], ai1[2 * j + 1])
-                           : make_float4(ar0[2 * j], ai0[2 * j], ar0[2 * j + 1], ai0[2 * j + 1]);
-    }
-    __syncwarp();
-    const float d = reinterpret_cast<const float*>(slot)[2 * kk];
-    if (!(d > floor_)) singular = true;
-    const float inv = __frcp_rn(d);
-    const bool piv0 = (2 * k == kk), piv1 = (2 * k + 1 == kk);
-    // pivot row: a_kk,j - (1 - 1/d) a_kk,j = a_kk,j / d with the same update
-    const float f0r = piv0 ? 1.f - inv : ar0[kk] * inv, f0i = piv0 ? 0.f : ai0[kk] * inv;
-    const float f1r = piv1 ? 1.f - inv : ar1[kk] * inv, f1i = piv1 ? 0.f : ai1[kk] * inv;
-#pragma unroll
-    for (int jq = 0; jq < U / 2; ++jq) {
-      const float4 v = slot[jq];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = 2 * jq + h;
-        if (j == kk) continue;
-        const float br = h ? v.z : v.x, bi = h ? v.w : v.y;
-        csub_mul(ar0[j], ai0[j], f0r, f0i, br, bi);
-        csub_mul(ar1[j], ai1[j], f1r, f1i, br, bi);
-      }
-    }
-    ar0[kk] = piv0 ? -inv : f0r;
-    ai0[kk] = piv0 ? 0.f : f0i;
-    ar1[kk] = piv1 ? -inv : f1r;
-    ai1[kk] = piv1 ? 0.f : f1i;
-  }
-  float t = 0.f;
-#pragma unroll
-  for (int jp = 0; jp < U / 2; ++jp)
-    if (k == jp) t = -(ar0[2 * jp] + ar1[2 * jp + 1]);
-#pragma unroll
-  for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  return t;
 }
 
 template <int U, int NPW, int MINB, bool SIG = false>

@@ -133,6 +133,12 @@ __host__ __device__ constexpr int ul_scal_bytes(int U, int LB = 2) {
   return U * 16 + (U / LB) * (LB * (LB - 1) / 2) * 16 + 16 * LB + 16;
 }
 __host__ __device__ constexpr int dl_scal_bytes(int U) { return U * 32 + 32 + 16; }
+// row of packed lower-triangle entry e = i (i + 1) / 2 + j (compile-time after unrolling)
+__host__ __device__ constexpr int tri_row(int e) {
+  int i = 0;
+  while ((i + 1) * (i + 2) / 2 <= e) ++i;
+  return i;
+}
 
 // Shared-memory layout of one CTA: [W staging slots][W*NPW scalar blocks][W mbarriers]
 template <int SLOT_B, int SCAL_B, int NPW, int W>
@@ -153,11 +159,14 @@ struct CtaSmem {
 // Scalar block per problem: float4 mnx[U] = (m_j, n_j, Re x_j, Im x_j) and
 // float4 gb[U/LB][LB(LB-1)/2] = (Re G, Im G, -Im G, Re G).
 // ===========================================================================
-template <int BC, int U, int G, int W, int MINB, int LB, bool XCHG = false>
+template <int BC, int U, int G, int W, int MINB, int LB, bool XCHG = false, bool SIG = false>
 __global__ void __launch_bounds__(32 * W, MINB)
     ul_reg_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
-               float2* __restrict__ X, const XMap xm) {
+               float2* __restrict__ X, const XMap xm, float* __restrict__ sigma2 = nullptr, float gam = 0.f,
+               float scale = 0.f, unsigned long long* __restrict__ status = nullptr) {
   static_assert(32 % G == 0 && BC % (2 * G) == 0 && U % LB == 0, "shape");
+  static_assert(!SIG || (G == 8 && U == 16 && LB == 2 && !XCHG),
+                "fused variance: 8 lanes per problem hold rows 2k, 2k+1 of the 16 x 16 Gram");
   constexpr int NPW = 32 / G, R = BC / G, NP = R / 2;
   constexpr int T = LB * (LB - 1) / 2;  // Gram entries per block
   constexpr int TILE_B = BC * U * 8, Y_B = BC * 8, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
@@ -206,9 +215,11 @@ __global__ void __launch_bounds__(32 * W, MINB)
         ri[c] = pair(v.y, v.w);
       }
     }
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
+    if constexpr (!SIG) {  // the fused-variance kernel keeps the slot until its Gram image is read
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
+    }
 
     // ---- per-problem scalars: ||h_j||^2 (detect.cpp:86-90) and block Grams,
     // each reduce-scattered over the group (lane k keeps a contiguous slice)
@@ -359,6 +370,81 @@ __global__ void __launch_bounds__(32 * W, MINB)
       for (int i = k; i < U / 2; i += G) {
         const float4 u0 = mnx[2 * i], u1 = mnx[2 * i + 1];
         xo[i] = make_float4(u0.z, u0.w, u1.z, u1.w);
+      }
+    }
+    if constexpr (SIG) {
+      // ---- post_eq_variance (detect.cpp:112-130) from the tile still in
+      // registers: the whole Gram G_ij = h_i^H h_j (i >= j, detect.cpp:21-28),
+      // chunks of 8 packed lower-triangle entries reduce-scattered over the
+      // group (lane k finishes entry e = 8ch + k), stored as A = I + (E_x/N0) G
+      // and A_ji = conj(A_ij) into an image (apair_slot) over the problem's own
+      // consumed tile in the staging slot.
+      constexpr int NE = U * (U + 1) / 2, NCH = (NE + 7) / 8;
+      float* af = reinterpret_cast<float*>(slot + g * TILE_B);
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        float v[16];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const int e = ch * 8 + m;
+          if (e >= NE) {
+            v[2 * m] = v[2 * m + 1] = 0.f;
+            continue;
+          }
+          const int i = tri_row(e), j = e - i * (i + 1) / 2;
+          float2 gr = fmul2(hr[i][0], hr[j][0]);
+          gr = ffma2(hi[i][0], hi[j][0], gr);
+#pragma unroll
+          for (int c = 1; c < NP; ++c) gr = ffma2(hi[i][c], hi[j][c], ffma2(hr[i][c], hr[j][c], gr));
+          v[2 * m] = hsum(gr);
+          if (i == j) {
+            v[2 * m + 1] = 0.f;
+          } else {
+            float2 gi = fmul2(hr[i][0], hi[j][0]);
+            gi = ffma2(neg2(hi[i][0]), hr[j][0], gi);
+#pragma unroll
+            for (int c = 1; c < NP; ++c) gi = ffma2(neg2(hi[i][c]), hr[j][c], ffma2(hr[i][c], hi[j][c], gi));
+            v[2 * m + 1] = hsum(gi);
+          }
+        }
+        group_reduce_scatter<G>(v, k);
+        const int e = ch * 8 + k;
+        if (e < NE) {
+          const int i = static_cast<int>((__fsqrt_rn(8.f * e + 1.f) - 1.f) * 0.5f), j = e - i * (i + 1) / 2;
+          const float are = fmaf(gam, v[0], i == j ? 1.f : 0.f), aim = gam * v[1];
+          const int s0 = apair_slot<U>(i, j >> 1) * 4 + (j & 1);
+          af[s0] = are;
+          af[s0 + 2] = aim;
+          if (i != j) {
+            const int s1 = apair_slot<U>(j, i >> 1) * 4 + (i & 1);
+            af[s1] = are;
+            af[s1 + 2] = -aim;
+          }
+        }
+      }
+      __syncwarp();
+      // lane k takes rows 2k, 2k+1 of A as column pairs; then the slot is free
+      // for the next set's copy
+      float2 R0r[U / 2], R0i[U / 2], R1r[U / 2], R1i[U / 2];
+      const float4* a4 = reinterpret_cast<const float4*>(af);
+#pragma unroll
+      for (int jq = 0; jq < U / 2; ++jq) {
+        const float4 a = a4[apair_slot<U>(2 * k, jq)], b = a4[apair_slot<U>(2 * k + 1, jq)];
+        R0r[jq] = make_float2(a.x, a.y);
+        R0i[jq] = make_float2(a.z, a.w);
+        R1r[jq] = make_float2(b.x, b.y);
+        R1i[jq] = make_float2(b.z, b.w);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
+      // the pivot rows go through the problem's scalar block (dead after the sweeps)
+      bool singular = false;
+      const float tr = gram_trace_inverse_cpairs<U>(R0r, R0i, R1r, R1i, k, mnx, singular);
+      const unsigned sing = __ballot_sync(0xffffffffu, singular);
+      if (p < P && k == 0) {
+        sigma2[p] = scale * tr;
+        if ((sing >> (G * g)) & 0xffu) record_status(status, p, ST_SINGULAR, 0);
       }
     }
     __syncwarp();

@@ -515,9 +515,13 @@ TEST_CASE("batched detection is bitwise the per-subcarrier calls (both fusions)"
   }
   // the reference's checks per subcarrier, in its order
   subs[3][2].y.pop_back();
-  CHECK(throws_with<std::invalid_argument>(
-      [&] { dcd::gpu::decentralized_cd_detect_batch(subs, DetectorConfig{}); },
-      "detector: observation length must match antenna count"));
+  DetectorConfig bad;
+  bad.n0 = 1.6;
+  CHECK(throws_with<std::invalid_argument>([&] { dcd::gpu::decentralized_cd_detect_batch(subs, bad); },
+                                           "detector: observation length must match antenna count"));
+  // N0 = 0 with optimal fusion: subcarrier 0's post_eq_variance throws first (detect.cpp:116-117)
+  CHECK(throws_with<std::invalid_argument>([&] { dcd::gpu::decentralized_cd_detect_batch(subs, DetectorConfig{}); },
+                                           "post_eq_variance: need N0 > 0 and E_x > 0"));
 }
 
 TEST_CASE("batched detection with uneven clusters falls back per subcarrier", t_ul_batch_uneven) {
