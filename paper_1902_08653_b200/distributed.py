@@ -232,10 +232,14 @@ class DistributedCD:
         async_op)."""
         p = self.part
         if p.world == 1:
-            xl, s2 = self.compute.ul_local(H, y, n0=n0, ex=ex, K=K, fusion=fusion)
+            # one call: the CD kernel and the ascending-cluster fusion (launched as
+            # its programmatic dependent inside dcdg_ul_detect)
+            out, wsum, xl, _ = self.compute.ul_partial(H, y, n0=n0, ex=ex, K=K, fusion=fusion, C_total=p.C_total,
+                                                       want_local=True)
+            if wsum is not None:  # a compute that leaves the optimal weights' sum to the caller
+                out = out / wsum.reshape(-1, 1)
             self._log_uplink(xl.shape[0], xl.shape[-1] if xl.dtype != torch.float16 else xl.shape[-2],
                              bytes_per_complex(xl), fusion == "optimal")
-            out = self.compute.fuse(xl, s2, fusion=fusion, C_total=p.C_total)
             return _Deferred(None, lambda: out) if async_op else out
         if self.mode == "p2p":
             return self._uplink_p2p(H, y, n0=n0, ex=ex, K=K, fusion=fusion, async_op=async_op)
