@@ -121,6 +121,20 @@ int dcdg_dl_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, i
                     int Bc, int U, int K, double rho, int fmt, void* x_dl, float* gain_part,
                     float* gain, void* stream);
 
+/* Per-update traces of ONE problem (the SweepObserver debug path,
+ * include/dcd/detect.hpp:28-36): the CD iterates after every coordinate
+ * update, in the reference's order (sweep t, coordinate j -> entry t*U + j),
+ * from the one-warp generic kernels (fp32 arithmetic on the stored inputs).
+ *   dcdg_ul_trace: x_trace [K*U][U], r_trace [K*U][Bc] complex fp32
+ *                  (x and the maintained residual, detect.cpp:106);
+ *   dcdg_dl_trace: x_trace [K*U][Bc] complex fp32 (the unscaled beamformer,
+ *                  precode.cpp:95).
+ * H / y / s as one problem of dcdg_ul_detect / dcdg_dl_precode; same checks. */
+int dcdg_ul_trace(dcdg_ctx* ctx, const void* H, const void* y, int Bc, int U, int K, double n0,
+                  double ex, int fmt, float* x_trace, float* r_trace, void* stream);
+int dcdg_dl_trace(dcdg_ctx* ctx, const void* H, const void* s, int Bc, int U, int K, int fmt,
+                  float* x_trace, void* stream);
+
 /* sigma2[p] = (E_x/U) tr((I + (E_x/N0) H_p^H H_p)^-1)  (detect.cpp:112-130). */
 int dcdg_post_eq_variance(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, double n0,
                           double ex, int fmt, float* sigma2, void* stream);

@@ -58,6 +58,9 @@ SIGNATURES = {
                                   C.c_double, C.c_int, _vp, _vp, _vp, _vp]),
     "dcdg_post_eq_variance": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
                                         _vp, _vp]),
+    "dcdg_ul_trace": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
+                                _vp, _vp, _vp]),
+    "dcdg_dl_trace": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp]),
     "dcdg_fuse": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp]),
     "dcdg_gain_reduce": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp]),
     "dcdg_fuse_finalize": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, _vp]),

@@ -170,10 +170,10 @@ void check_downlink(const ComplexMatrix& h_dl, const ComplexVector& s) {
   if (s.size() != h_dl.rows()) throw std::invalid_argument("precoder: symbol count must match user count");
 }
 
-void reject_observer(SweepObserver* o) {
-  if (o)
-    throw std::invalid_argument(
-        "dcd::gpu: per-update SweepObserver hooks cannot run on the GPU (use the reference or oracle for probes)");
+// fp32 complex device trace entries -> cf64
+void trace_vec(const float* f, std::size_t n, ComplexVector& out) {
+  out.resize(n);
+  for (std::size_t i = 0; i < n; ++i) out[i] = cf64{f[2 * i], f[2 * i + 1]};
 }
 
 // Reciprocity: uplink tile (B_c x U, column-major) of a U x B_c downlink block.
@@ -487,10 +487,35 @@ ComplexVector cd_detect(const ComplexMatrix& h, const ComplexVector& y, double n
                         const PrecisionMode& prec, SweepObserver* observer, Engine& eng) {
   check_system(h, y.size(), n0, ex);
   if (t_max == 0) throw std::invalid_argument("cd_detect: need at least one sweep");
-  reject_observer(observer);
   std::lock_guard<std::mutex> lk(eng.mutex());
   const DevPrecision dp = map_precision(prec);
   const std::size_t b = h.rows(), u = h.cols(), es = esize(dp.fmt), bd = dev_rows(b, dp.fmt);
+  if (observer) {
+    // per-update hooks (detect.cpp:106): the debug trace kernel dumps x and r
+    // after every update; the hooks replay them in order on this thread, and
+    // the result is the traced run's final iterate
+    const std::size_t n = static_cast<std::size_t>(t_max) * u;
+    Layout L;
+    const std::size_t oH = L.take(bd * u * es), oY = L.take(bd * es);
+    L.close_inputs();
+    const std::size_t oXT = L.take(n * u * 8), oRT = L.take(n * bd * 8);
+    Call k(eng, L);
+    pack_tile(h.flat().data(), b, u, dp.fmt, k.h(oH));
+    pack_tile(y.data(), b, 1, dp.fmt, k.h(oY));
+    k.upload(L);
+    Engine::check(dcdg_ul_trace(eng.ctx(), k.d(oH), k.d(oY), static_cast<int>(bd), static_cast<int>(u),
+                                static_cast<int>(t_max), n0, ex, dp.fmt, k.d<float>(oXT), k.d<float>(oRT),
+                                eng.stream()));
+    k.download(L);
+    eng.sync();
+    ComplexVector x, r;
+    for (std::size_t e = 0; e < n; ++e) {
+      trace_vec(k.h<float>(oXT) + 2 * e * u, u, x);
+      trace_vec(k.h<float>(oRT) + 2 * e * bd, b, r);
+      observer->after_update(static_cast<unsigned>(e / u), e % u, x, r);
+    }
+    return x;
+  }
   Layout L;
   const std::size_t oH = L.take(bd * u * es), oY = L.take(bd * es);
   L.close_inputs();
@@ -604,10 +629,33 @@ ComplexVector cd_precode(const ComplexMatrix& h_dl, const ComplexVector& s, unsi
                          const PrecisionMode& prec, SweepObserver* observer, Engine& eng) {
   check_downlink(h_dl, s);
   if (t_max == 0) throw std::invalid_argument("cd_precode: need at least one sweep");
-  reject_observer(observer);
   std::lock_guard<std::mutex> lk(eng.mutex());
   const DevPrecision dp = map_precision(prec);
   const std::size_t u = h_dl.rows(), b = h_dl.cols(), es = esize(dp.fmt), bd = dev_rows(b, dp.fmt);
+  if (observer) {
+    // per-update hooks (precode.cpp:95): x after every update, empty residual
+    const std::size_t n = static_cast<std::size_t>(t_max) * u;
+    Layout L;
+    const std::size_t oH = L.take(bd * u * es), oS = L.take(u * es);
+    L.close_inputs();
+    const std::size_t oXT = L.take(n * bd * 8);
+    Call k(eng, L);
+    std::vector<cf64> tile(b * u);
+    uplink_tile_of(h_dl, tile.data());
+    pack_tile(tile.data(), b, u, dp.fmt, k.h(oH));
+    pack(s.data(), u, dp.fmt, k.h(oS));
+    k.upload(L);
+    Engine::check(dcdg_dl_trace(eng.ctx(), k.d(oH), k.d(oS), static_cast<int>(bd), static_cast<int>(u),
+                                static_cast<int>(t_max), dp.fmt, k.d<float>(oXT), eng.stream()));
+    k.download(L);
+    eng.sync();
+    ComplexVector x;
+    for (std::size_t e = 0; e < n; ++e) {
+      trace_vec(k.h<float>(oXT) + 2 * e * bd, b, x);
+      observer->after_update(static_cast<unsigned>(e / u), e % u, x, {});
+    }
+    return x;
+  }
   Layout L;
   const std::size_t oH = L.take(bd * u * es), oS = L.take(u * es);
   L.close_inputs();

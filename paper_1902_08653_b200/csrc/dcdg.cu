@@ -838,12 +838,12 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
       auto k = dcdg::ul_generic<__half2>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       k<<<blocks, 128, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(y), static_cast<int>(P),
-                                   Bc, U, K, kappa, static_cast<__half2*>(x_local));
+                                   Bc, U, K, kappa, static_cast<__half2*>(x_local), nullptr, nullptr);
     } else {
       auto k = dcdg::ul_generic<float2>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       k<<<blocks, 128, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(y), static_cast<int>(P),
-                                   Bc, U, K, kappa, static_cast<float2*>(x_local));
+                                   Bc, U, K, kappa, static_cast<float2*>(x_local), nullptr, nullptr);
     }
     CUDA_TRY(cudaGetLastError(), "ul_generic launch");
   }
@@ -897,7 +897,7 @@ int dcdg_dl_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, i
     auto k = dcdg::dl_generic<T, GAIN>;                                                                         \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));               \
     k<<<blocks, 128, smem, st>>>(static_cast<const T*>(H), static_cast<const T*>(s), static_cast<int>(P), C, Bc, \
-                                 U, K, rho_c, static_cast<T*>(x_dl), gain_part, ctx->d_status);                \
+                                 U, K, rho_c, static_cast<T*>(x_dl), gain_part, ctx->d_status, nullptr);       \
   }
     if (fmt == DCDG_FP16) {
       if (gain_part) DL_GENERIC(__half2, true) else DL_GENERIC(__half2, false)
@@ -909,6 +909,74 @@ int dcdg_dl_precode(dcdg_ctx* ctx, const void* H, const void* s, int S, int C, i
   }
   ++ctx->launches;
   if (gain) return dcdg_gain_reduce(ctx, gain_part, s, S, C, U, fmt, gain, stream);
+  return DCDG_OK;
+}
+
+int dcdg_ul_trace(dcdg_ctx* ctx, const void* H, const void* y, int Bc, int U, int K, double n0, double ex, int fmt,
+                  float* x_trace, float* r_trace, void* stream) {
+  NvtxRange nvtx_("dcdg_ul_trace");
+  if (int rc = check_fmt(fmt)) return rc;
+  // cd_detect's checks (detect.cpp:12-19,71-72)
+  if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "detector: empty channel matrix");
+  if (n0 < 0.0 || !(ex > 0.0)) return fail(DCDG_EINVAL, "detector: need N0 >= 0 and E_x > 0");
+  if (K <= 0) return fail(DCDG_EINVAL, "cd_detect: need at least one sweep");
+  if (fmt == DCDG_FP16 && (Bc & 1))
+    return fail(DCDG_EINVAL, "dcdg: fp16 row-pair planar tiles need an even antenna count B_c");
+  if (!H || !y || !x_trace || !r_trace) return fail(DCDG_EINVAL, "dcdg_ul_trace: null buffer");
+  if (int rc = check_ctx(ctx)) return rc;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = as_stream(stream);
+  const size_t xl_bytes = static_cast<size_t>(U) * 8;
+  if (int rc = ensure_scratch(ctx, xl_bytes)) return rc;
+  const size_t smem = 4 * (static_cast<size_t>(Bc) + 2 * U) * sizeof(float2);
+  const float kappa = static_cast<float>(n0 / ex);
+  auto* xt = reinterpret_cast<float2*>(x_trace);
+  auto* rt = reinterpret_cast<float2*>(r_trace);
+  if (fmt == DCDG_FP16) {
+    auto k = dcdg::ul_generic<__half2, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<1, 128, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(y), 1, Bc, U, K, kappa,
+                            static_cast<__half2*>(ctx->scratch), xt, rt);
+  } else {
+    auto k = dcdg::ul_generic<float2, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<1, 128, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(y), 1, Bc, U, K, kappa,
+                            static_cast<float2*>(ctx->scratch), xt, rt);
+  }
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "ul_trace launch");
+  return DCDG_OK;
+}
+
+int dcdg_dl_trace(dcdg_ctx* ctx, const void* H, const void* s, int Bc, int U, int K, int fmt, float* x_trace,
+                  void* stream) {
+  NvtxRange nvtx_("dcdg_dl_trace");
+  if (int rc = check_fmt(fmt)) return rc;
+  // cd_precode's checks (precode.cpp:11-16,57-58)
+  if (Bc <= 0 || U <= 0) return fail(DCDG_EINVAL, "precoder: empty channel matrix");
+  if (K <= 0) return fail(DCDG_EINVAL, "cd_precode: need at least one sweep");
+  if (fmt == DCDG_FP16 && (Bc & 1))
+    return fail(DCDG_EINVAL, "dcdg: fp16 row-pair planar tiles need an even antenna count B_c");
+  if (!H || !s || !x_trace) return fail(DCDG_EINVAL, "dcdg_dl_trace: null buffer");
+  if (int rc = check_ctx(ctx)) return rc;
+  CUDA_TRY(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = as_stream(stream);
+  if (int rc = ensure_scratch(ctx, static_cast<size_t>(Bc) * 8)) return rc;
+  const size_t smem = 4 * (static_cast<size_t>(Bc) + 2 * U) * sizeof(float2);
+  auto* xt = reinterpret_cast<float2*>(x_trace);
+  if (fmt == DCDG_FP16) {
+    auto k = dcdg::dl_generic<__half2, false, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<1, 128, smem, st>>>(static_cast<const __half2*>(H), static_cast<const __half2*>(s), 1, 1, Bc, U, K, 0.f,
+                            static_cast<__half2*>(ctx->scratch), nullptr, ctx->d_status, xt);
+  } else {
+    auto k = dcdg::dl_generic<float2, false, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<1, 128, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(s), 1, 1, Bc, U, K, 0.f,
+                            static_cast<float2*>(ctx->scratch), nullptr, ctx->d_status, xt);
+  }
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "dl_trace launch");
   return DCDG_OK;
 }
 

@@ -12,9 +12,15 @@ namespace dcdg {
 // whose B_c is not a multiple of 4G.  Residual / beamformer and scalars live
 // in shared memory; lane l owns rows l, l+32, ...
 // ===========================================================================
-template <typename T>
+//
+// TRACE (the SweepObserver debug path, detect.hpp:28-36): after every
+// coordinate update of problem 0 the iterate x and the residual r are dumped
+// to xt[(t U + j) U ..] and rt[(t U + j) B_c ..] (fp32 complex), the values the
+// reference hands to observer->after_update (detect.cpp:106, precode.cpp:95).
+template <typename T, bool TRACE = false>
 __global__ void __launch_bounds__(128) ul_generic(const T* __restrict__ H, const T* __restrict__ Y, int P, int BC,
-                                                  int U, int K, float kappa, T* __restrict__ X) {
+                                                  int U, int K, float kappa, T* __restrict__ X,
+                                                  float2* __restrict__ xt = nullptr, float2* __restrict__ rt = nullptr) {
   extern __shared__ float2 gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long p = static_cast<long long>(blockIdx.x) * 4 + warp;
@@ -62,14 +68,22 @@ __global__ void __launch_bounds__(128) ul_generic(const T* __restrict__ H, const
         r[i] = rv;
       }
       __syncwarp();
+      if (TRACE && p == 0) {
+        const size_t e = static_cast<size_t>(t) * U + j;
+        for (int i = lane; i < U; i += 32) xt[e * U + i] = x[i];
+        for (int i = lane; i < BC; i += 32) rt[e * BC + i] = r[i];
+      }
     }
   for (int j = lane; j < U; j += 32) stc(X, static_cast<size_t>(p) * U + j, x[j]);
 }
 
-template <typename T, bool GAIN>
+// TRACE: the beamformer x after every update of problem 0 to xt[(t U + j) B_c ..]
+// (precode.cpp:95 hands the observer x and an empty residual).
+template <typename T, bool GAIN, bool TRACE = false>
 __global__ void __launch_bounds__(128)
     dl_generic(const T* __restrict__ H, const T* __restrict__ Sy, int P, int C, int BC, int U, int K, float rho_c,
-               T* __restrict__ X, float* __restrict__ gain_part, unsigned long long* __restrict__ status) {
+               T* __restrict__ X, float* __restrict__ gain_part, unsigned long long* __restrict__ status,
+               float2* __restrict__ xt = nullptr) {
   extern __shared__ float2 gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long p = static_cast<long long>(blockIdx.x) * 4 + warp;
@@ -119,6 +133,7 @@ __global__ void __launch_bounds__(128)
         xv.x = fmaf(-dr, hv.x, fmaf(di, hv.y, xv.x));
         xv.y = fmaf(-dr, hv.y, fmaf(-di, hv.x, xv.y));
         x[i] = xv;
+        if (TRACE && p == 0) xt[(static_cast<size_t>(t) * U + j) * BC + i] = xv;  // each lane its own rows
       }
     }
   float e = 0.f;

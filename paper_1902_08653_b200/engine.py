@@ -192,6 +192,31 @@ class Engine:
                                    fu, _ptr(x_local), _ptr(sigma2), _ptr(xhat), _ptr(wsum), self._stream(stream)))
         return UplinkResult(x_local, xhat, sigma2, wsum)
 
+    def ul_trace(self, H, y, *, n0: float, ex: float = 1.0, K: int = 3, stream=None):
+        """Per-update iterates of ONE problem (the SweepObserver debug path,
+        detect.hpp:28-36): H [U, Bc] / y [Bc] (or [1,1,...] batches of one) ->
+        (x [K*U, U], r [K*U, Bc]) complex64, entry t*U + j after update (t, j)."""
+        fmt = _fmt_of(H)
+        U, Bc = _shape(H, fmt)[-2:]
+        _need(H, "H")
+        _need(y, "y")
+        xt = torch.empty((K * U, U), dtype=torch.complex64, device=H.device)
+        rt = torch.empty((K * U, Bc), dtype=torch.complex64, device=H.device)
+        check(lib().dcdg_ul_trace(self._ctx, _ptr(H), _ptr(y), Bc, U, K, float(n0), float(ex), fmt, _ptr(xt),
+                                  _ptr(rt), self._stream(stream)))
+        return xt, rt
+
+    def dl_trace(self, H, s, *, K: int = 3, stream=None):
+        """Per-update beamformers of ONE problem (precode.cpp:95): H [U, Bc],
+        s [U] -> x [K*U, Bc] complex64 (unscaled, as cd_precode)."""
+        fmt = _fmt_of(H)
+        U, Bc = _shape(H, fmt)[-2:]
+        _need(H, "H")
+        _need(s, "s")
+        xt = torch.empty((K * U, Bc), dtype=torch.complex64, device=H.device)
+        check(lib().dcdg_dl_trace(self._ctx, _ptr(H), _ptr(s), Bc, U, K, fmt, _ptr(xt), self._stream(stream)))
+        return xt
+
     def post_eq_variance(self, H, *, n0: float, ex: float = 1.0, out=None, stream=None):
         fmt = _fmt_of(H)
         S, Cn, U, Bc = _shape(H, fmt)

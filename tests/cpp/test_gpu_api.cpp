@@ -157,10 +157,123 @@ TEST_CASE("detector input validation", t_validation) {
   CHECK(throws_with<std::invalid_argument>([&] { dcd::gpu::cd_detect(h, random_vector(16), 0.1, 1.0, 0); },
                                            "cd_detect: need at least one sweep"));
   struct Probe : dcd::gpu::SweepObserver {
-    void after_update(unsigned, std::size_t, std::span<const cf64>, std::span<const cf64>) override {}
+    int calls = 0;
+    void after_update(unsigned, std::size_t, std::span<const cf64>, std::span<const cf64>) override { ++calls; }
   } probe;
-  CHECK(throws_with<std::invalid_argument>(
-      [&] { dcd::gpu::cd_detect(h, random_vector(16), 0.1, 1.0, 3, {}, &probe); }, "SweepObserver"));
+  // the checks run before any observer call
+  CHECK(throws_with<std::invalid_argument>([&] { dcd::gpu::cd_detect(h, random_vector(15), 0.1, 1.0, 3, {}, &probe); },
+                                           "detector: observation length must match antenna count"));
+  CHECK(probe.calls == 0);
+}
+
+// ---- per-update probes through the debug trace kernels (the reference's
+// DescentProbe / ZeroingProbe, tests/test_detect.cpp:149-200 and
+// tests/test_precode.cpp:170-224, with fp32 tolerances)
+namespace {
+double objective(const ComplexMatrix& h, const ComplexVector& y, const ComplexVector& x, double kappa) {
+  const auto hx = matvec(h, x);
+  double j = 0.0;
+  for (std::size_t i = 0; i < y.size(); ++i) j += std::norm(y[i] - hx[i]);
+  for (const auto& z : x) j += kappa * std::norm(z);
+  return j;
+}
+double vnorm(const ComplexVector& v) {
+  double s = 0.0;
+  for (const auto& z : v) s += std::norm(z);
+  return std::sqrt(s);
+}
+struct DescentProbe : dcd::gpu::SweepObserver {
+  const ComplexMatrix* h = nullptr;
+  const ComplexVector* y = nullptr;
+  double kappa = 0.0, last_j = 0.0, slack = 0.0, rtol = 0.0;
+  int violations = 0, checked = 0;
+  unsigned expect_t = 0;
+  std::size_t expect_j = 0;
+  void after_update(unsigned t, std::size_t j, std::span<const cf64> x, std::span<const cf64> residual) override {
+    if (t != expect_t || j != expect_j) ++violations;  // the reference's order
+    if (++expect_j == h->cols()) {
+      expect_j = 0;
+      ++expect_t;
+    }
+    ComplexVector xv(x.begin(), x.end());
+    const double jv = objective(*h, *y, xv, kappa);
+    if (jv > last_j + slack) ++violations;
+    last_j = jv;
+    ++checked;
+    // the maintained residual equals y - H x
+    const auto hx = matvec(*h, xv);
+    double d = 0.0;
+    for (std::size_t i = 0; i < residual.size(); ++i) d += std::norm((*y)[i] - hx[i] - residual[i]);
+    if (residual.size() != y->size() || std::sqrt(d) > rtol) ++violations;
+  }
+};
+struct ZeroingProbe : dcd::gpu::SweepObserver {
+  const ComplexMatrix* hn = nullptr;  // normalised rows
+  const ComplexVector* sb = nullptr;  // normalised targets
+  const ComplexMatrix* h_raw = nullptr;
+  int violations = 0, sweep_checks = 0;
+  void after_update(unsigned, std::size_t coord, std::span<const cf64> x, std::span<const cf64> residual) override {
+    if (!residual.empty()) ++violations;  // precode.cpp:95 passes no residual
+    cf64 r{0.0, 0.0};
+    for (std::size_t j = 0; j < x.size(); ++j) r += (*hn)(coord, j) * x[j];
+    r -= (*sb)[coord];
+    if (std::abs(r) > 1e-5 * (1.0 + std::abs((*sb)[coord]))) ++violations;
+    if (coord + 1 == hn->rows()) {  // sweep boundary: x in the channel row space
+      ComplexVector xv(x.begin(), x.end());
+      const auto px = zf_exact(*h_raw, matvec(*h_raw, xv));
+      double d = 0.0;
+      for (std::size_t j = 0; j < xv.size(); ++j) d += std::norm(xv[j] - px[j]);
+      if (std::sqrt(d) > 1e-5 * (1.0 + vnorm(xv))) ++violations;
+      ++sweep_checks;
+    }
+  }
+};
+}  // namespace
+
+TEST_CASE("every coordinate update descends and keeps the residual consistent (trace kernel)", t_descent) {
+  for (int trial = 0; trial < 10; ++trial) {
+    const std::size_t b = 16 + 16 * (trial % 2), u = 4 + (trial % 5);
+    const auto h = random_matrix(b, u);
+    const auto y = random_vector(b);
+    DescentProbe probe;
+    probe.h = &h;
+    probe.y = &y;
+    probe.kappa = 0.2;
+    probe.last_j = vnorm(y) * vnorm(y);
+    probe.slack = 1e-5 * probe.last_j;
+    probe.rtol = 1e-5 * (1.0 + vnorm(y));
+    const auto xt = dcd::gpu::cd_detect(h, y, 0.2, 1.0, 3, {}, &probe);
+    CHECK(probe.checked == static_cast<int>(3 * u));
+    CHECK(probe.violations == 0);
+    // the traced run ends where the batched kernels and the reference end
+    CHECK(rel_dist(xt, dcd::gpu::cd_detect(h, y, 0.2, 1.0, 3)) <= kTol);
+    CHECK(rel_dist(xt, cd_detect_ref(h, y, 0.2, 1.0, 3)) <= kTol);
+  }
+}
+
+TEST_CASE("each dual update zeroes its constraint and stays in the row space (trace kernel)", t_zeroing) {
+  for (int trial = 0; trial < 10; ++trial) {
+    const std::size_t u = 3 + trial % 5, b = 8 + 4 * (trial % 4);
+    const auto h = random_matrix(u, b);
+    const auto s = random_vector(u);
+    ComplexMatrix hn = h;
+    ComplexVector sb = s;
+    for (std::size_t i = 0; i < u; ++i) {
+      double nrm = 0.0;
+      for (std::size_t j = 0; j < b; ++j) nrm += std::norm(hn(i, j));
+      nrm = std::sqrt(nrm);
+      for (std::size_t j = 0; j < b; ++j) hn(i, j) /= nrm;
+      sb[i] /= nrm;
+    }
+    ZeroingProbe probe;
+    probe.hn = &hn;
+    probe.sb = &sb;
+    probe.h_raw = &h;
+    const auto xt = dcd::gpu::cd_precode(h, s, 3, {}, &probe);
+    CHECK(probe.violations == 0);
+    CHECK(probe.sweep_checks == 3);
+    CHECK(rel_dist(xt, dcd::gpu::cd_precode(h, s, 3)) <= kTol);
+  }
 }
 
 TEST_CASE("post-equalization variance closed forms", t_pev) {
