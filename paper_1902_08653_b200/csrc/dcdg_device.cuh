@@ -286,6 +286,25 @@ __device__ __forceinline__ void xchg_cta_done(const XMap& m) {
   }
 }
 
+// D += A B, mma.sync m16n8k16, fp16 operands, fp32 accumulate
+__device__ __forceinline__ void mma_f16f32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// x = hi + lo in binary16 pairs (the split operands of an fp32-accurate Gram
+// on the fp16 tensor cores): hi = rn(x), lo = rn(x - hi)
+__device__ __forceinline__ void split_h2(float2 x, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __float22half2_rn(x);
+  const float2 hf = __half22float2(h);
+  hi = h2_as_u32(h);
+  lo = h2_as_u32(__float22half2_rn(make_float2(x.x - hf.x, x.y - hf.y)));
+}
+// W' word of an interleaved (re, im) binary16 pair: (im, -re)
+__device__ __forceinline__ uint32_t wprime(uint32_t w) { return __byte_perm(w, 0, 0x1032) ^ 0x80000000u; }
+
 // complex c -= a * b
 __device__ __forceinline__ void csub_mul(float& cr, float& ci, float ar, float ai, float br, float bi) {
   cr = fmaf(-ar, br, fmaf(ai, bi, cr));
@@ -402,11 +421,14 @@ __device__ __forceinline__ float gram_trace_inverse_cpairs(float2 (&R0r)[U / 2],
   for (int kk = 0; kk < U; ++kk) {
     const int h = kk & 1, qk = kk >> 1;  // owner's row h; the pivot column is in pair qk, half h
     float4* slot = prow + h * NQ;        // alternating broadcast rows
-    if (k == qk) {
+    if (k == qk) {  // two 8-B stores per slot straight from the register pairs (asm: no merged 16-B
+                    // store, which costs four re-pairing moves per slot)
+      const uint32_t a = smem_u32(slot);
 #pragma unroll
       for (int jq = 0; jq < NQ; ++jq) {
         const float2 r = h ? R1r[jq] : R0r[jq], i = h ? R1i[jq] : R0i[jq];
-        slot[jq] = make_float4(r.x, r.y, i.x, i.y);
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a + 16 * jq), "f"(r.x), "f"(r.y) : "memory");
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a + 16 * jq + 8), "f"(i.x), "f"(i.y) : "memory");
       }
     }
     __syncwarp();

@@ -133,12 +133,6 @@ __host__ __device__ constexpr int ul_scal_bytes(int U, int LB = 2) {
   return U * 16 + (U / LB) * (LB * (LB - 1) / 2) * 16 + 16 * LB + 16;
 }
 __host__ __device__ constexpr int dl_scal_bytes(int U) { return U * 32 + 32 + 16; }
-// row of packed lower-triangle entry e = i (i + 1) / 2 + j (compile-time after unrolling)
-__host__ __device__ constexpr int tri_row(int e) {
-  int i = 0;
-  while ((i + 1) * (i + 2) / 2 <= e) ++i;
-  return i;
-}
 
 // Shared-memory layout of one CTA: [W staging slots][W*NPW scalar blocks][W mbarriers]
 template <int SLOT_B, int SCAL_B, int NPW, int W>
@@ -221,6 +215,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
       if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
     }
 
+    float emax = 0.f;
     // ---- per-problem scalars: ||h_j||^2 (detect.cpp:86-90) and block Grams,
     // each reduce-scattered over the group (lane k keeps a contiguous slice)
     {
@@ -237,6 +232,12 @@ __global__ void __launch_bounds__(32 * W, MINB)
 #pragma unroll
       for (int j = U; j < NV; ++j) v[j] = 0.f;
       group_reduce_scatter<G>(v, k);
+      if constexpr (SIG) {  // the problem's largest column energy (scale of the split Gram)
+#pragma unroll
+        for (int i = 0; i < NV / G; ++i) emax = fmaxf(emax, v[i]);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+      }
 #pragma unroll
       for (int i = 0; i < NV / G; ++i) {
         const int idx = k * (NV / G) + i;
@@ -373,55 +374,66 @@ __global__ void __launch_bounds__(32 * W, MINB)
       }
     }
     if constexpr (SIG) {
-      // ---- post_eq_variance (detect.cpp:112-130) from the tile still in
-      // registers: the whole Gram G_ij = h_i^H h_j (i >= j, detect.cpp:21-28),
-      // chunks of 8 packed lower-triangle entries reduce-scattered over the
-      // group (lane k finishes entry e = 8ch + k), stored as A = I + (E_x/N0) G
-      // and A_ji = conj(A_ij) into an image (apair_slot) over the problem's own
-      // consumed tile in the staging slot.
-      constexpr int NE = U * (U + 1) / 2, NCH = (NE + 7) / 8;
-      float* af = reinterpret_cast<float*>(slot + g * TILE_B);
+      // ---- post_eq_variance (detect.cpp:112-130).  The Gram G = H^H H
+      // (detect.cpp:21-28) of each problem of the set comes from the tensor
+      // cores, read from the problem's tile still in the staging slot: fp32
+      // entries scaled by a power of two (largest column energy -> ~1) and
+      // split x = hi + lo into binary16, G = hi.hi + hi.lo + lo.hi with fp32
+      // accumulation (mma.sync m16n8k16; each product of binary16 values is
+      // exact in fp32, the dropped lo.lo term is ~2^-22 of |h|^2).  Fragment
+      // k-order: k-step s takes complex rows 8s + 2t (k 2t, 2t+1) and 8s + 2t + 1
+      // (k 2t+8, 2t+9), one 16-B load per user; W' = (im, -re) per complex gives
+      // Im G.  A = I + (E_x/N0) G is written over the problem's consumed tile
+      // as the column-pair image (apair_slot) the sweep operator reads.
+      {
+        const int mg = lane >> 2, mt = lane & 3;  // mma fragment coordinates
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        float v[16];
+        for (int pl = 0; pl < NPW; ++pl) {
+          const float em = __shfl_sync(0xffffffffu, emax, pl * G);
+          // power-of-two scale: |h_ij|^2 <= em -> |h_ij sc| <= 1
+          const float sc = em > 0.f ? ldexpf(1.f, -static_cast<int>(ceilf(0.5f * __log2f(em)))) : 1.f;
+          const unsigned char* tb = slot + pl * TILE_B;
+          float gr0[4] = {}, gr1[4] = {}, gi0[4] = {}, gi1[4] = {};
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const int e = ch * 8 + m;
-          if (e >= NE) {
-            v[2 * m] = v[2 * m + 1] = 0.f;
-            continue;
+          for (int ks = 0; ks < BC / 8; ++ks) {
+            const float4 u0 = *reinterpret_cast<const float4*>(tb + mg * (BC * 8) + (8 * ks + 2 * mt) * 8);
+            const float4 u1 = *reinterpret_cast<const float4*>(tb + (mg + 8) * (BC * 8) + (8 * ks + 2 * mt) * 8);
+            const float2 x00 = fmul2(sc, make_float2(u0.x, u0.y)), x01 = fmul2(sc, make_float2(u0.z, u0.w));
+            const float2 x10 = fmul2(sc, make_float2(u1.x, u1.y)), x11 = fmul2(sc, make_float2(u1.z, u1.w));
+            uint32_t ah[4], al[4];
+            split_h2(x00, ah[0], al[0]);  // user mg,     row 8ks + 2mt
+            split_h2(x10, ah[1], al[1]);  // user mg + 8, row 8ks + 2mt
+            split_h2(x01, ah[2], al[2]);  // user mg,     row 8ks + 2mt + 1
+            split_h2(x11, ah[3], al[3]);  // user mg + 8, row 8ks + 2mt + 1
+            // B = W: n-tile 0 (users 0-7) = (a0, a2), n-tile 1 (users 8-15) = (a1, a3)
+            mma_f16f32(gr0, ah, ah[0], ah[2]);
+            mma_f16f32(gr0, ah, al[0], al[2]);
+            mma_f16f32(gr0, al, ah[0], ah[2]);
+            mma_f16f32(gr1, ah, ah[1], ah[3]);
+            mma_f16f32(gr1, ah, al[1], al[3]);
+            mma_f16f32(gr1, al, ah[1], ah[3]);
+            mma_f16f32(gi0, ah, wprime(ah[0]), wprime(ah[2]));
+            mma_f16f32(gi0, ah, wprime(al[0]), wprime(al[2]));
+            mma_f16f32(gi0, al, wprime(ah[0]), wprime(ah[2]));
+            mma_f16f32(gi1, ah, wprime(ah[1]), wprime(ah[3]));
+            mma_f16f32(gi1, ah, wprime(al[1]), wprime(al[3]));
+            mma_f16f32(gi1, al, wprime(ah[1]), wprime(ah[3]));
           }
-          const int i = tri_row(e), j = e - i * (i + 1) / 2;
-          float2 gr = fmul2(hr[i][0], hr[j][0]);
-          gr = ffma2(hi[i][0], hi[j][0], gr);
-#pragma unroll
-          for (int c = 1; c < NP; ++c) gr = ffma2(hi[i][c], hi[j][c], ffma2(hr[i][c], hr[j][c], gr));
-          v[2 * m] = hsum(gr);
-          if (i == j) {
-            v[2 * m + 1] = 0.f;
-          } else {
-            float2 gi = fmul2(hr[i][0], hi[j][0]);
-            gi = ffma2(neg2(hi[i][0]), hr[j][0], gi);
-#pragma unroll
-            for (int c = 1; c < NP; ++c) gi = ffma2(neg2(hi[i][c]), hr[j][c], ffma2(hr[i][c], hi[j][c], gi));
-            v[2 * m + 1] = hsum(gi);
-          }
-        }
-        group_reduce_scatter<G>(v, k);
-        const int e = ch * 8 + k;
-        if (e < NE) {
-          const int i = static_cast<int>((__fsqrt_rn(8.f * e + 1.f) - 1.f) * 0.5f), j = e - i * (i + 1) / 2;
-          const float are = fmaf(gam, v[0], i == j ? 1.f : 0.f), aim = gam * v[1];
-          const int s0 = apair_slot<U>(i, j >> 1) * 4 + (j & 1);
-          af[s0] = are;
-          af[s0 + 2] = aim;
-          if (i != j) {
-            const int s1 = apair_slot<U>(j, i >> 1) * 4 + (i & 1);
-            af[s1] = are;
-            af[s1 + 2] = -aim;
-          }
+          __syncwarp();  // every lane's reads of this tile are done before its image overwrites it
+          const float gs = gam / (sc * sc);
+          float4* img = reinterpret_cast<float4*>(slot + pl * TILE_B);
+          // C fragment: [0..1] row mg, cols 2mt, 2mt+1 of the n-tile; [2..3] row mg + 8
+          img[apair_slot<U>(mg, mt)] = make_float4(fmaf(gs, gr0[0], mg == 2 * mt ? 1.f : 0.f),
+                                                   fmaf(gs, gr0[1], mg == 2 * mt + 1 ? 1.f : 0.f), gs * gi0[0],
+                                                   gs * gi0[1]);
+          img[apair_slot<U>(mg, 4 + mt)] = make_float4(gs * gr1[0], gs * gr1[1], gs * gi1[0], gs * gi1[1]);
+          img[apair_slot<U>(mg + 8, mt)] = make_float4(gs * gr0[2], gs * gr0[3], gs * gi0[2], gs * gi0[3]);
+          img[apair_slot<U>(mg + 8, 4 + mt)] = make_float4(fmaf(gs, gr1[2], mg == 2 * mt ? 1.f : 0.f),
+                                                           fmaf(gs, gr1[3], mg == 2 * mt + 1 ? 1.f : 0.f),
+                                                           gs * gi1[2], gs * gi1[3]);
         }
       }
+      float* af = reinterpret_cast<float*>(slot + g * TILE_B);
       __syncwarp();
       // lane k takes rows 2k, 2k+1 of A as column pairs; then the slot is free
       // for the next set's copy
