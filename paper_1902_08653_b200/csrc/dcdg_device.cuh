@@ -325,14 +325,17 @@ __device__ __forceinline__ void csub_mul(float& cr, float& ci, float ar, float a
 template <int U>
 __device__ __forceinline__ float gram_trace_inverse(float (&ar0)[U], float (&ai0)[U], float (&ar1)[U],
                                                     float (&ai1)[U], int k, float gam, float4* prow,
-                                                    bool& singular) {
-  // A = I + gam G in place over the Gram rows (they are dead after the sweeps)
+                                                    bool& singular, bool rows_hold_a = false) {
+  // A = I + gam G in place over the Gram rows (they are dead after the sweeps),
+  // unless the rows already hold A
+  if (!rows_hold_a) {
 #pragma unroll
-  for (int j = 0; j < U; ++j) {
-    ar0[j] = fmaf(gam, ar0[j], j == 2 * k ? 1.f : 0.f);
-    ai0[j] *= gam;
-    ar1[j] = fmaf(gam, ar1[j], j == 2 * k + 1 ? 1.f : 0.f);
-    ai1[j] *= gam;
+    for (int j = 0; j < U; ++j) {
+      ar0[j] = fmaf(gam, ar0[j], j == 2 * k ? 1.f : 0.f);
+      ai0[j] *= gam;
+      ar1[j] = fmaf(gam, ar1[j], j == 2 * k + 1 ? 1.f : 0.f);
+      ai1[j] *= gam;
+    }
   }
   float dmax = 0.f;
 #pragma unroll

@@ -192,6 +192,9 @@ __device__ __forceinline__ void gram_tc_phase(unsigned char* sm, uint32_t sbase,
   }
 }
 
+#ifndef DCDG_GRAM_SIG_CPAIRS
+#define DCDG_GRAM_SIG_CPAIRS 0  // lab: column-pair FFMA2 sweep operator here, 0.268 -> 0.296 ms (slower)
+#endif
 template <int U, int NPW, int MINB, bool SIG = false>
 __global__ void __launch_bounds__(32, MINB)
     ul_gram_f16(const __grid_constant__ CUtensorMap tmH, const __half2* __restrict__ Y, int P, int K, float kappa,
@@ -297,7 +300,20 @@ __global__ void __launch_bounds__(32, MINB)
       // format as the reference rounds the messages (detect.cpp:170-173)
       bool singular = false;
       float4* prow = reinterpret_cast<float4*>(sm + L::kGOff) + q * U;
+#if DCDG_GRAM_SIG_CPAIRS
+      // A = I + gam G as column pairs, then the FFMA2 sweep operator (as ul_reg_f32's fused variance)
+      float2 R0r[U / 2], R0i[U / 2], R1r[U / 2], R1i[U / 2];
+#pragma unroll
+      for (int jq = 0; jq < U / 2; ++jq) {
+        R0r[jq] = make_float2(fmaf(gam, g0r[2 * jq], jq == k ? 1.f : 0.f), gam * g0r[2 * jq + 1]);
+        R0i[jq] = make_float2(gam * g0i[2 * jq], gam * g0i[2 * jq + 1]);
+        R1r[jq] = make_float2(gam * g1r[2 * jq], fmaf(gam, g1r[2 * jq + 1], jq == k ? 1.f : 0.f));
+        R1i[jq] = make_float2(gam * g1i[2 * jq], gam * g1i[2 * jq + 1]);
+      }
+      const float tr = gram_trace_inverse_cpairs<U>(R0r, R0i, R1r, R1i, k, prow, singular);
+#else
       const float tr = gram_trace_inverse<U>(g0r, g0i, g1r, g1i, k, gam, prow, singular);
+#endif
       const unsigned sing = __ballot_sync(0xffffffffu, singular);
       if (p < P && k == 0) {
         sigma2[p] = __half2float(__float2half_rn(scale * tr));

@@ -47,6 +47,11 @@ namespace dcdg {
 #ifndef DCDG_UL_DIRECT_DX
 #define DCDG_UL_DIRECT_DX 0
 #endif
+// fused variance (ul_reg_f32<..., SIG>): column-pair FFMA2 sweep operator (1)
+// or the scalar FFMA one of the fp16 Gram kernel (0)
+#ifndef DCDG_SIG_CPAIRS
+#define DCDG_SIG_CPAIRS 1
+#endif
 #ifndef DCDG_SCATTER_MIN_G_UL
 #define DCDG_SCATTER_MIN_G_UL 32
 #endif
@@ -437,6 +442,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
       __syncwarp();
       // lane k takes rows 2k, 2k+1 of A as column pairs; then the slot is free
       // for the next set's copy
+#if DCDG_SIG_CPAIRS
       float2 R0r[U / 2], R0i[U / 2], R1r[U / 2], R1i[U / 2];
       const float4* a4 = reinterpret_cast<const float4*>(af);
 #pragma unroll
@@ -447,12 +453,33 @@ __global__ void __launch_bounds__(32 * W, MINB)
         R1r[jq] = make_float2(b.x, b.y);
         R1i[jq] = make_float2(b.z, b.w);
       }
+#else
+      // scalar rows of G for the FFMA sweep operator (A = I + gam G formed inside)
+      float ar0[U], ai0[U], ar1[U], ai1[U];
+      const float4* a4 = reinterpret_cast<const float4*>(af);
+#pragma unroll
+      for (int jq = 0; jq < U / 2; ++jq) {
+        const float4 a = a4[apair_slot<U>(2 * k, jq)], b = a4[apair_slot<U>(2 * k + 1, jq)];
+        ar0[2 * jq] = a.x;
+        ar0[2 * jq + 1] = a.y;
+        ai0[2 * jq] = a.z;
+        ai0[2 * jq + 1] = a.w;
+        ar1[2 * jq] = b.x;
+        ar1[2 * jq + 1] = b.y;
+        ai1[2 * jq] = b.z;
+        ai1[2 * jq + 1] = b.w;
+      }
+#endif
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
       // the pivot rows go through the problem's scalar block (dead after the sweeps)
       bool singular = false;
+#if DCDG_SIG_CPAIRS
       const float tr = gram_trace_inverse_cpairs<U>(R0r, R0i, R1r, R1i, k, mnx, singular);
+#else
+      const float tr = gram_trace_inverse<U>(ar0, ai0, ar1, ai1, k, 0.f, mnx, singular, true);
+#endif
       const unsigned sing = __ballot_sync(0xffffffffu, singular);
       if (p < P && k == 0) {
         sigma2[p] = scale * tr;
