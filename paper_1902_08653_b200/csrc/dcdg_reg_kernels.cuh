@@ -52,6 +52,10 @@ namespace dcdg {
 #ifndef DCDG_SIG_CPAIRS
 #define DCDG_SIG_CPAIRS 1
 #endif
+// downlink GAIN: v = H_c s before the sweeps (1) or after them (0)
+#ifndef DCDG_DL_GAIN_EARLY
+#define DCDG_DL_GAIN_EARLY 0
+#endif
 #ifndef DCDG_SCATTER_MIN_G_UL
 #define DCDG_SCATTER_MIN_G_UL 32
 #endif
@@ -792,6 +796,23 @@ __global__ void __launch_bounds__(32 * W, MINB)
     }
     __syncwarp();
 
+    float2 vr[NP], vi[NP];  // GAIN: v = H_c s = sum_u s_u h_u (the effective-gain share's left vector)
+#if DCDG_DL_GAIN_EARLY
+    // accumulated before the sweeps, independent of their dependency chain
+    if (GAIN) {
+#pragma unroll
+      for (int c = 0; c < NP; ++c) vr[c] = vi[c] = z2;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const float2 sj = sraw[j];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          vr[c] = ffma2(-sj.y, hi[j][c], ffma2(sj.x, hr[j][c], vr[c]));
+          vi[c] = ffma2(sj.y, hr[j][c], ffma2(sj.x, hi[j][c], vi[c]));
+        }
+      }
+    }
+#endif
     float2 xr[NP], xi[NP];
 #pragma unroll
     for (int c = 0; c < NP; ++c) xr[c] = xi[c] = z2;
@@ -855,7 +876,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
     // gain share Re(s^H H_dl,c x_c) = Re(v^H x_c), v = H_c s = sum_u s_u h_u
     float gq = 0.f;
     if (GAIN) {
-      float2 vr[NP], vi[NP];
+#if !DCDG_DL_GAIN_EARLY
 #pragma unroll
       for (int c = 0; c < NP; ++c) vr[c] = vi[c] = z2;
 #pragma unroll
@@ -868,6 +889,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
           vi[c] = ffma2(ci, hr[j][c], ffma2(cr, hi[j][c], vi[c]));
         }
       }
+#endif
       float2 q2 = fmul2(vr[0], xr[0]);
       q2 = ffma2(vi[0], xi[0], q2);
 #pragma unroll
