@@ -30,7 +30,9 @@
 #include <cstddef>
 #include <cstdint>
 #include <memory>
+#include <functional>
 #include <mutex>
+#include <string>
 #include <span>
 #include <vector>
 
@@ -141,8 +143,17 @@ class Engine {
   /// Pinned host staging of at least `bytes` (grow-only).  Callers hold mutex().
   void* host_staging(std::size_t bytes);
   std::mutex& mutex() { return *mu_; }
+  /// Runs one call's stream work (`enqueue`: its H2D copy, kernels and D2H
+  /// copy on stream()), waits for it and rethrows any recorded numerical
+  /// error.  Calls with the same `key` (shapes, scalars, buffer addresses)
+  /// replay a CUDA graph captured on the key's second use, so a warm call is
+  /// one graph launch and one synchronisation.  Callers hold mutex().
+  void run(const std::string& key, const std::function<void()>& enqueue);
 
  private:
+  struct Graphs;
+  std::unique_ptr<Graphs> graphs_;
+  unsigned long long* status_host_ = nullptr;  // pinned status word of run()
   dcdg_ctx* ctx_ = nullptr;
   void* stream_ = nullptr;
   int device_ = 0;

@@ -172,6 +172,14 @@ int dcdg_fusion_weights(dcdg_ctx* ctx, const float* sigma2, int S, int C, float*
  * (dcdg_last_error) is the reference's exception text; the failing problem
  * index is available from dcdg_last_error_problem(). */
 int dcdg_sync_status(dcdg_ctx* ctx, void* stream);
+
+/* The same check without a blocking read: dcdg_status_enqueue copies the
+ * device status word to `host_word` (pinned memory) on `stream` (capturable
+ * into a CUDA graph with the call it follows); after the caller has
+ * synchronised the stream, dcdg_status_decode(ctx, *host_word) returns and
+ * clears the recorded error exactly as dcdg_sync_status does. */
+int dcdg_status_enqueue(dcdg_ctx* ctx, unsigned long long* host_word, void* stream);
+int dcdg_status_decode(dcdg_ctx* ctx, unsigned long long key);
 long long dcdg_last_error_problem(void);
 
 /* Number of kernel launches issued through this context (for bench.py). */

@@ -68,6 +68,8 @@ SIGNATURES = {
     "dcdg_power_scale": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_double, C.c_int, _vp]),
     "dcdg_fusion_weights": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp]),
     "dcdg_sync_status": (C.c_int, [_vp, _vp]),
+    "dcdg_status_enqueue": (C.c_int, [_vp, _vp, _vp]),
+    "dcdg_status_decode": (C.c_int, [_vp, C.c_ulonglong]),
     "dcdg_launch_count": (C.c_uint64, [_vp]),
     "dcdg_round_fp16": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
     "dcdg_mmse_bias": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _vp,

@@ -4,17 +4,19 @@
 // batched device call per decentralized operation.  Host code here only moves
 // and re-lays-out data (fp64 <-> fp32/fp16 packing, H_dl <-> uplink tiles);
 // all arithmetic of the path runs in the CUDA kernels.
-#include <algorithm>
 #include "dcd_gpu.hpp"
 
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
+#include <unordered_set>
 
 namespace dcd::gpu {
 
@@ -157,6 +159,17 @@ struct Call {
   void download(const Layout& l) const { d2h(host + l.in_end, dev + l.in_end, l.end - l.in_end, eng.stream()); }
 };
 
+// Graph-cache key of one call (Engine::run): the bytes of every value that
+// shapes its stream work (sizes, scalars, buffer addresses).
+struct Key {
+  std::string s;
+  template <class T>
+  Key& operator<<(const T& v) {
+    s.append(reinterpret_cast<const char*>(&v), sizeof v);
+    return *this;
+  }
+};
+
 // detect.cpp:12-19
 void check_system(const ComplexMatrix& h, std::size_t ylen, double n0, double ex) {
   if (h.rows() == 0 || h.cols() == 0) throw std::invalid_argument("detector: empty channel matrix");
@@ -261,11 +274,16 @@ std::vector<DetectionResult> detect_impl(std::span<const ClusterSpan> subs, std:
       pack_tile(cl.h.flat().data(), cl.h.rows(), u, dp.fmt, k.h(oH + s * hsub + hoff[c]));
       pack_tile(cl.y.data(), cl.y.size(), 1, dp.fmt, k.h(oY + s * ysub + yoff[c]));
     }
-  k.upload(L);
   const int fusion = optimal ? DCDG_FUSION_OPTIMAL : DCDG_FUSION_UNIFORM;
   const int ui = static_cast<int>(u), K = static_cast<int>(cfg.t_max), nci = static_cast<int>(nc);
   const int Si = static_cast<int>(S);
   float* s2 = optimal ? k.d<float>(oS2) : nullptr;
+  Key key;
+  key << 'U' << S << nc << u << K << cfg.n0 << cfg.ex << dp.fmt << dp.round_messages << fusion << uniform << k.host
+      << k.dev << L.end;
+  for (std::size_t c = 0; c < nc; ++c) key << subs[0][c].h.rows();
+  eng.run(key.s, [&] {
+  k.upload(L);
   if (uniform) {
     Engine::check(dcdg_ul_detect(eng.ctx(), k.d(oH), k.d(oY), Si, nci, nci,
                                  static_cast<int>(dev_rows(subs[0][0].h.rows(), dp.fmt)), ui, K, cfg.n0, cfg.ex,
@@ -286,7 +304,7 @@ std::vector<DetectionResult> detect_impl(std::span<const ClusterSpan> subs, std:
                           eng.stream()));
   if (optimal) Engine::check(dcdg_fusion_weights(eng.ctx(), s2, Si, nci, k.d<float>(oW), eng.stream()));
   k.download(L);
-  eng.sync();
+  });
 
   std::vector<DetectionResult> out(S);
   for (std::size_t s = 0; s < S; ++s) {
@@ -346,6 +364,11 @@ std::vector<PrecodeResult> precode_impl(std::span<const BlockSpan> blocks,
     pack(syms[s].data(), u, dp.fmt, k.h(oS + s * u * es));
     if (dp.round_messages) pack(syms[s].data(), u, dp.fmt, k.h(oSw + s * u * es));
   }
+  Key key;
+  key << 'D' << S << nc << u << cfg.t_max << cfg.rho << dp.fmt << dp.round_messages << uniform << k.host << k.dev
+      << L.end;
+  for (std::size_t c = 0; c < nc; ++c) key << blocks[0][c].cols();
+  eng.run(key.s, [&] {
   k.upload(L);
   const void* s_in = k.d(oS);
   if (dp.round_messages) {  // broadcast boundary (precode.cpp:157-160)
@@ -377,7 +400,7 @@ std::vector<PrecodeResult> precode_impl(std::span<const BlockSpan> blocks,
   }
   Engine::check(dcdg_gain_reduce(eng.ctx(), gp, k.d(oS), Si, nci, ui, dp.fmt, k.d<float>(oG), eng.stream()));
   k.download(L);
-  eng.sync();
+  });
 
   std::vector<PrecodeResult> out(S);
   for (std::size_t s = 0; s < S; ++s) {
@@ -404,8 +427,26 @@ void Engine::check(int status) {
   throw_status(status, dcdg_last_error());
 }
 
-Engine::Engine(int device) : device_(device), mu_(std::make_unique<std::mutex>()) {
+// Captured calls of one Engine: key -> instantiated graph (keys seen once run
+// eagerly, which also warms the kernels' one-time attribute setup).
+struct Engine::Graphs {
+  std::unordered_map<std::string, cudaGraphExec_t> exec;
+  std::unordered_set<std::string> seen;
+  void clear() {
+    for (auto& kv : exec) cudaGraphExecDestroy(kv.second);
+    exec.clear();
+    seen.clear();
+  }
+  ~Graphs() { clear(); }
+};
+
+Engine::Engine(int device)
+    : graphs_(std::make_unique<Graphs>()), device_(device), mu_(std::make_unique<std::mutex>()) {
   check(dcdg_init(device, &ctx_));
+  if (cudaMallocHost(reinterpret_cast<void**>(&status_host_), sizeof(unsigned long long)) != cudaSuccess) {
+    dcdg_destroy(ctx_);
+    throw std::runtime_error("dcd::gpu: pinned host allocation failed");
+  }
   // PrecisionMode{fp16, full_storage} mirrors the reference's fp16 arithmetic
   // emulation: the half2 sweep kernel, not the fp32-arithmetic Gram kernel
   check(dcdg_set_fp16_algorithm(ctx_, DCDG_ALG_SWEEP));
@@ -419,6 +460,8 @@ Engine::Engine(int device) : device_(device), mu_(std::make_unique<std::mutex>()
 
 Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
+  graphs_->clear();
+  if (status_host_) cudaFreeHost(status_host_);
   if (dscratch_) cudaFree(dscratch_);
   if (hstage_) cudaFreeHost(hstage_);
   if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
@@ -426,6 +469,43 @@ Engine::~Engine() {
 }
 
 void Engine::sync() { check(dcdg_sync_status(ctx_, stream_)); }
+
+void Engine::run(const std::string& key, const std::function<void()>& enqueue) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  auto finish = [&] {
+    if (cudaStreamSynchronize(st) != cudaSuccess) throw std::runtime_error("dcd::gpu: stream synchronize failed");
+    check(dcdg_status_decode(ctx_, *status_host_));
+  };
+  auto it = graphs_->exec.find(key);
+  if (it == graphs_->exec.end()) {
+    if (graphs_->seen.insert(key).second) {  // first use: eager
+      enqueue();
+      check(dcdg_status_enqueue(ctx_, status_host_, stream_));
+      finish();
+      return;
+    }
+    if (graphs_->exec.size() >= 64) graphs_->clear();  // bounded: a long-running caller with many shapes
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+      throw std::runtime_error("dcd::gpu: stream capture failed");
+    try {
+      enqueue();
+      check(dcdg_status_enqueue(ctx_, status_host_, stream_));
+    } catch (...) {
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaGraphExec_t ex = nullptr;
+    const bool ok = cudaStreamEndCapture(st, &g) == cudaSuccess && g &&
+                    cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) throw std::runtime_error("dcd::gpu: graph instantiation failed");
+    it = graphs_->exec.emplace(key, ex).first;
+  }
+  if (cudaGraphLaunch(it->second, st) != cudaSuccess) throw std::runtime_error("dcd::gpu: graph launch failed");
+  finish();
+}
 
 namespace {
 std::size_t grow_to(std::size_t have, std::size_t need) {
@@ -438,6 +518,7 @@ std::size_t grow_to(std::size_t have, std::size_t need) {
 void* Engine::device_scratch(std::size_t bytes) {
   if (bytes <= dscratch_bytes_) return dscratch_;
   const std::size_t n = grow_to(dscratch_bytes_, bytes);
+  graphs_->clear();  // captured calls hold the old addresses
   cudaSetDevice(device_);
   if (dscratch_) {
     cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));  // the old buffer may still be in use
@@ -456,6 +537,7 @@ void* Engine::device_scratch(std::size_t bytes) {
 void* Engine::host_staging(std::size_t bytes) {
   if (bytes <= hstage_bytes_) return hstage_;
   const std::size_t n = grow_to(hstage_bytes_, bytes);
+  graphs_->clear();  // captured calls hold the old addresses
   if (hstage_) {
     cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
     cudaFreeHost(hstage_);
@@ -523,12 +605,15 @@ ComplexVector cd_detect(const ComplexMatrix& h, const ComplexVector& y, double n
   Call k(eng, L);
   pack_tile(h.flat().data(), b, u, dp.fmt, k.h(oH));
   pack_tile(y.data(), b, 1, dp.fmt, k.h(oY));
-  k.upload(L);
-  Engine::check(dcdg_ul_detect(eng.ctx(), k.d(oH), k.d(oY), 1, 1, 1, static_cast<int>(bd), static_cast<int>(u),
-                               static_cast<int>(t_max), n0, ex, dp.fmt, DCDG_FUSION_UNIFORM, k.d(oX), nullptr, nullptr,
-                               nullptr, eng.stream()));
-  k.download(L);
-  eng.sync();
+  Key key;
+  key << 'u' << b << u << t_max << n0 << ex << dp.fmt << k.host << k.dev << L.end;
+  eng.run(key.s, [&] {
+    k.upload(L);
+    Engine::check(dcdg_ul_detect(eng.ctx(), k.d(oH), k.d(oY), 1, 1, 1, static_cast<int>(bd), static_cast<int>(u),
+                                 static_cast<int>(t_max), n0, ex, dp.fmt, DCDG_FUSION_UNIFORM, k.d(oX), nullptr,
+                                 nullptr, nullptr, eng.stream()));
+    k.download(L);
+  });
   ComplexVector x(u);
   unpack(k.h(oX), u, dp.fmt, x.data());
   return x;
@@ -665,12 +750,15 @@ ComplexVector cd_precode(const ComplexMatrix& h_dl, const ComplexVector& s, unsi
   uplink_tile_of(h_dl, tile.data());
   pack_tile(tile.data(), b, u, dp.fmt, k.h(oH));
   pack(s.data(), u, dp.fmt, k.h(oS));
-  k.upload(L);
-  // rho == 0: unnormalised beamformer, exactly what cd_precode returns
-  Engine::check(dcdg_dl_precode(eng.ctx(), k.d(oH), k.d(oS), 1, 1, 1, static_cast<int>(bd), static_cast<int>(u),
-                                static_cast<int>(t_max), 0.0, dp.fmt, k.d(oX), nullptr, nullptr, eng.stream()));
-  k.download(L);
-  eng.sync();
+  Key key;
+  key << 'd' << b << u << t_max << dp.fmt << k.host << k.dev << L.end;
+  eng.run(key.s, [&] {
+    k.upload(L);
+    // rho == 0: unnormalised beamformer, exactly what cd_precode returns
+    Engine::check(dcdg_dl_precode(eng.ctx(), k.d(oH), k.d(oS), 1, 1, 1, static_cast<int>(bd), static_cast<int>(u),
+                                  static_cast<int>(t_max), 0.0, dp.fmt, k.d(oX), nullptr, nullptr, eng.stream()));
+    k.download(L);
+  });
   ComplexVector x(b);
   unpack(k.h(oX), b, dp.fmt, x.data());
   return x;

@@ -740,6 +740,20 @@ int dcdg_sync_status(dcdg_ctx* ctx, void* stream) {
   CUDA_TRY(cudaStreamSynchronize(as_stream(stream)), "stream synchronize");
   unsigned long long key = ~0ULL;
   CUDA_TRY(cudaMemcpy(&key, ctx->d_status, sizeof key, cudaMemcpyDeviceToHost), "status read");
+  return dcdg_status_decode(ctx, key);
+}
+
+int dcdg_status_enqueue(dcdg_ctx* ctx, unsigned long long* host_word, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!host_word) return fail(DCDG_EINVAL, "dcdg_status_enqueue: null host word");
+  CUDA_TRY(cudaMemcpyAsync(host_word, ctx->d_status, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           as_stream(stream)),
+           "status copy");
+  return DCDG_OK;
+}
+
+int dcdg_status_decode(dcdg_ctx* ctx, unsigned long long key) {
+  if (int rc = check_ctx(ctx)) return rc;
   if (key == ~0ULL) return DCDG_OK;
   CUDA_TRY(cudaMemset(ctx->d_status, 0xff, sizeof(unsigned long long)), "status reset");
   const unsigned code = static_cast<unsigned>((key >> 16) & 0xff);
