@@ -319,12 +319,16 @@ cudaError_t launch_dl_mw(dcdg_ctx* ctx, const void* H, const void* S, int P, int
 // 1 multi-warp (a = warps per problem), 2 split tile (a = lanes, b = register
 // columns; dcdg_split_kernels.cuh).
 // Split-tile kernels (dcdg_split_kernels.cuh): one-warp CTAs, grid = SMs x occupancy.
+// DCDG_SPLIT_PF: sets of L2 prefetch lead.
+#ifndef DCDG_SPLIT_PF
+#define DCDG_SPLIT_PF 1
+#endif
 template <int BC, int U, int G, int JR, int MINB>
 cudaError_t launch_ul_split(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
                             const dcdg::XMap* /*exchange via xchg_put_kernel*/, cudaStream_t st) {
   constexpr int NPW = 32 / G;
   constexpr size_t smem = dcdg::split_cols_bytes(BC, U, JR, G) + NPW * dcdg::ul_scal_bytes(U, 2);
-  auto kern = dcdg::ul_split_f32<BC, U, G, JR, MINB, 1>;
+  auto kern = dcdg::ul_split_f32<BC, U, G, JR, MINB, DCDG_SPLIT_PF>;
   const int occ = occupancy_of(ctx, kern, smem, 32);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min(nsets, ctx->sms * occ);
@@ -338,7 +342,7 @@ cudaError_t launch_dl_split_k(dcdg_ctx* ctx, const void* H, const void* S, int P
                               float* gp, cudaStream_t st) {
   constexpr int NPW = 32 / G;
   constexpr size_t smem = dcdg::split_cols_bytes(BC, U, JR, G) + NPW * dcdg::dl_scal_bytes(U);
-  auto kern = dcdg::dl_split_f32<BC, U, G, JR, MINB, GAIN>;
+  auto kern = dcdg::dl_split_f32<BC, U, G, JR, MINB, GAIN, DCDG_SPLIT_PF>;
   const int occ = occupancy_of(ctx, kern, smem, 32);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min(nsets, ctx->sms * occ);

@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(32, MINB)
 // Downlink, fp32, split tile (see dl_reg_f32 for the algorithm, the
 // unnormalised-row form of the update and the scalar block layout).
 // ===========================================================================
-template <int BC, int U, int G, int JR, int MINB, bool GAIN>
+template <int BC, int U, int G, int JR, int MINB, bool GAIN, int PF = 1>
 __global__ void __launch_bounds__(32, MINB)
     dl_split_f32(const float2* __restrict__ H, const float2* __restrict__ Sy, int P, int C, int K, float rho_c,
                  float2* __restrict__ X, float* __restrict__ gain_part, unsigned long long* __restrict__ status) {
@@ -298,10 +298,12 @@ __global__ void __launch_bounds__(32, MINB)
       prefetch_l2(Sy + static_cast<size_t>(v0) * U, nv * U * 8);
     }
   };
-  if (lane == 0) prefetch(set);
+  if (lane == 0)
+#pragma unroll
+    for (int f = 0; f < PF; ++f) prefetch(set + f * nw);
   const float2 z2 = make_float2(0.f, 0.f);
   for (; set < nsets; set += nw) {
-    if (lane == 0) prefetch(set + nw);
+    if (lane == 0) prefetch(set + PF * nw);
     const int p = set * NPW + g;
     const int pc = min(p, P - 1);
     const float4* h4 = reinterpret_cast<const float4*>(H) + static_cast<size_t>(pc) * T4;

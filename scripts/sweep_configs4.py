@@ -3,7 +3,7 @@ C in {1,2,4,8}, 64-QAM, K=3, fp32, one GPU holding all C clusters.  For each
 shape: UL and DL CD-kernel time, Gbps (S*U*log2(64)/t), batch latency
 (kernel + fusion / gain) and fraction of the measured HBM roofline.  The
 downlink needs B_c >= U (precode.cpp:147-151); infeasible shapes are reported
-as such.  usage: python scripts/sweep_configs4.py [out.json]"""
+as such.  usage: python scripts/sweep_configs4.py [out.json] [U filter, e.g. 32]"""
 import json
 import math
 import os
@@ -36,8 +36,9 @@ def timed(fn, reps=10):
 
 
 rows = []
+UF = [int(sys.argv[2])] if len(sys.argv) > 2 else (16, 32)
 for B in (128, 256, 512):
-    for U in (16, 32):
+    for U in UF:
         for C in (1, 2, 4, 8):
             Bc = B // C
             per = (Bc * U + Bc + U) * 8
@@ -67,6 +68,6 @@ for B in (128, 256, 512):
             print(json.dumps(row), flush=True)
             del H, y, s
             torch.cuda.empty_cache()
-out = sys.argv[1] if len(sys.argv) > 1 else None
+out = sys.argv[1] if len(sys.argv) > 1 and sys.argv[1] != "-" else None
 if out:
     json.dump({"peak_hbm_gbs": hbm, "fmt": "fp32", "K": 3, "qam": 64, "rows": rows}, open(out, "w"), indent=1)
