@@ -130,6 +130,32 @@ __device__ __forceinline__ float2 shfl_xor2(float2 v, int o) {
   return make_float2(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
 }
 
+// Group-wide sums of NV float2 values over aligned groups of G lanes, every
+// lane of a group ending with bitwise the same sums.  DCDG_BFLY_SHALLOW
+// levels at the bottom of the xor butterfly are replaced by one gather round:
+// the remaining 2^L partners are read with independent shuffles and summed
+// as a pairwise tree, so the dependency chain has L - 1 fewer shuffle
+// latencies for (2^L - 1) / L times the shuffles of those levels.  Every lane
+// adds the same partial sums in a commuted order, so the results agree.
+#ifndef DCDG_BFLY_SHALLOW
+#define DCDG_BFLY_SHALLOW 0
+#endif
+template <int G, int NV>
+__device__ __forceinline__ void group_allreduce2(float2 (&d)[NV]) {
+  constexpr int L = (DCDG_BFLY_SHALLOW >= 2 && G >= 4) ? 2 : 0;  // gathered bottom levels (xor 1, 2)
+#pragma unroll
+  for (int o = G / 2; o >= (L ? 4 : 1); o >>= 1)
+#pragma unroll
+    for (int a = 0; a < NV; ++a) d[a] = fadd2(d[a], shfl_xor2(d[a], o));
+  if constexpr (L == 2) {
+#pragma unroll
+    for (int a = 0; a < NV; ++a) {
+      const float2 s1 = shfl_xor2(d[a], 1), s2 = shfl_xor2(d[a], 2), s3 = shfl_xor2(d[a], 3);
+      d[a] = fadd2(fadd2(d[a], s1), fadd2(s2, s3));
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // complex element access for the two storage formats
 // ---------------------------------------------------------------------------

@@ -329,10 +329,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
 #pragma unroll
           for (int a = 0; a < LB; ++a) d[a] = reinterpret_cast<const float2*>(db)[a];
         } else {
-#pragma unroll
-          for (int o = G / 2; o > 0; o >>= 1)
-#pragma unroll
-            for (int a = 0; a < LB; ++a) d[a] = fadd2(d[a], shfl_xor2(d[a], o));
+          group_allreduce2<G>(d);
         }
         float2 dx[LB];
 #pragma unroll
@@ -841,11 +838,10 @@ __global__ void __launch_bounds__(32 * W, MINB)
           d0 = make_float2(dd.x, dd.y);
           d1 = make_float2(dd.z, dd.w);
         } else {
-#pragma unroll
-          for (int o = G / 2; o > 0; o >>= 1) {
-            d0 = fadd2(d0, shfl_xor2(d0, o));
-            d1 = fadd2(d1, shfl_xor2(d1, o));
-          }
+          float2 dd[2] = {d0, d1};
+          group_allreduce2<G>(dd);
+          d0 = dd[0];
+          d1 = dd[1];
         }
         // r_u = q_u (h_u^H x - s_u) ; x -= r_u h_u   (precode.cpp:89-94 on unnormalised rows)
         const float2 r0 = ffma2(S0.z, d0, make_float2(-S0.x, -S0.y));
