@@ -83,6 +83,11 @@ struct GramSmem {
   static constexpr int kAlloc = kBytes + 1024;      // slack to align the swizzled slot to 1024 B
 };
 
+// Gram fragments by 8-B loads in a (re, im)-paired k-order (1) or ldmatrix
+// plus a lane-pair shuffle for W' (0)
+#ifndef DCDG_GRAM_LDS64
+#define DCDG_GRAM_LDS64 1
+#endif
 #ifndef DCDG_GRAM_SMEM_BCAST
 #define DCDG_GRAM_SMEM_BCAST 0
 #endif
@@ -129,6 +134,36 @@ __device__ __forceinline__ void gram_tc_phase(unsigned char* sm, uint32_t sbase,
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       uint32_t a[4];
+#if DCDG_GRAM_LDS64
+      // k-order: thread t of k-step ks takes row pair 4ks + t, its (re, im)
+      // word pair in one 8-B load per user (k 2t, 2t+1 = re pair, k 2t+8, 2t+9
+      // = im pair), so W' = (im, -re) is a register swap and a sign flip
+      {
+        const int row0 = pl * U + g, row1 = row0 + 8, ch = 2 * ks + (t >> 1), off = (t & 1) * 8;
+        const uint2 u0 = *reinterpret_cast<const uint2*>(sm + row0 * L::kRowB + ((ch ^ (row0 & 7)) << 4) + off);
+        const uint2 u1 = *reinterpret_cast<const uint2*>(sm + row1 * L::kRowB + ((ch ^ (row1 & 7)) << 4) + off);
+        a[0] = u0.x;
+        a[1] = u1.x;
+        a[2] = u0.y;
+        a[3] = u1.y;
+      }
+      (void)lu;
+      (void)lch;
+      mma_f16f32(gr[0], a, a[0], a[2]);
+      mma_f16f32(gr[1], a, a[1], a[3]);
+      mma_f16f32(gi[0], a, a[2], a[0] ^ 0x80008000u);
+      mma_f16f32(gi[1], a, a[3], a[1] ^ 0x80008000u);
+      if (Z) {
+        // B = [Y, Y', 0 ...]: column g = 0 is y, g = 1 = (im, -re), same k-order
+        uint32_t y0 = 0, y1 = 0;
+        if (g < 2) {
+          const uint2 yv = reinterpret_cast<const uint2*>(sm + L::kYOff + pl * 128)[4 * ks + t];
+          y0 = g ? yv.y : yv.x;
+          y1 = g ? (yv.x ^ 0x80008000u) : yv.y;
+        }
+        mma_f16f32(zz, a, y0, y1);
+      }
+#else
       const int ch = 2 * ks + lch;
       ldsm_x4(a, sbase + row * L::kRowB + ((ch ^ (row & 7)) << 4));
       // B = W: n-tile 0 (users 0-7) = (a0, a2), n-tile 1 (users 8-15) = (a1, a3)
@@ -148,6 +183,7 @@ __device__ __forceinline__ void gram_tc_phase(unsigned char* sm, uint32_t sbase,
         }
         mma_f16f32(zz, a, y0, y1);
       }
+#endif
     }
     // problem pl's rows of the slot are consumed: its G goes there, swizzled
     // [k][chunk j ^ k][rows 2k, 2k+1] (2048 B, conflict-free 16-B reads), and
