@@ -130,7 +130,9 @@ __device__ __forceinline__ void gram_tc_phase(unsigned char* sm, uint32_t sbase,
 #pragma unroll
   for (int pl = 0; pl < NPW; ++pl) {
     float gr[2][4] = {}, gi[2][4] = {}, zz[4] = {};
+#if !DCDG_GRAM_LDS64
     const int row = pl * U + lu;
+#endif
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       uint32_t a[4];
