@@ -394,6 +394,10 @@ struct Spec {
 #ifndef DCDG_F16_G_TARGET
 #define DCDG_F16_G_TARGET 4
 #endif
+// lanes per problem of the paper's 32x8 tile (configs[0])
+#ifndef DCDG_G_32x8
+#define DCDG_G_32x8 4
+#endif
 constexpr int minb(int warps) { return warps / kWarps > 0 ? warps / kWarps : 1; }
 constexpr int minb_mw(int warps, int nw) { return warps / nw > 0 ? warps / nw : 1; }
 
@@ -411,7 +415,7 @@ constexpr int minb_mw(int warps, int nw) { return warps / nw > 0 ? warps / nw : 
 // several warps per problem; at B_c = 32, U = 16 the register kernel stays.
 const Spec kSpecs[] = {
     {32, 16, DCDG_FP32, UL_REG(32, 16, 8), DL_REG(32, 16, 8)},  // north-star target: B=256, C=8, U=16
-    {32, 8, DCDG_FP32, UL_REG(32, 8, 4), DL_REG(32, 8, 4)},     // paper / config 1: B_c=32, U=8
+    {32, 8, DCDG_FP32, UL_REG(32, 8, DCDG_G_32x8), DL_REG(32, 8, DCDG_G_32x8)},  // paper / config 1: B_c=32, U=8
     {16, 16, DCDG_FP32, UL_REG(16, 16, 4), DL_REG(16, 16, 4)},  // B=128, C=8
     {64, 16, DCDG_FP32, UL_REG(64, 16, 16), DL_REG(64, 16, 16)},  // B=256, C=4 / B=512, C=8
     {64, 8, DCDG_FP32, UL_REG(64, 8, 8), DL_REG(64, 8, 8)},
