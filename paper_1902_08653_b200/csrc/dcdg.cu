@@ -202,11 +202,14 @@ cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, in
 #ifndef DCDG_UL_SIG
 #define DCDG_UL_SIG 1
 #endif
-bool ul_sig_shape(int bc, int u, int fmt) { return DCDG_UL_SIG && fmt == DCDG_FP32 && bc == 32 && u == 16; }
+bool ul_sig_shape(int bc, int u, int fmt) {
+  return DCDG_UL_SIG && fmt == DCDG_FP32 && bc == 32 && (u == 16 || u == 8);
+}
 
-cudaError_t launch_ul_f32_sig(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
-                              float* s2, float gam, float scale, cudaStream_t st) {
-  constexpr int BC = 32, U = 16, G = 8, NPW = 32 / G, LB = 2;
+template <int BC, int U, int G>
+cudaError_t launch_ul_f32_sig_k(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                                float* s2, float gam, float scale, cudaStream_t st) {
+  constexpr int NPW = 32 / G, LB = 2;
   constexpr size_t smem = dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U, LB), NPW, kWarps>::kBytes;
   auto kern = dcdg::ul_reg_f32<BC, U, G, kWarps, DCDG_UL_SIG_MINB, LB, false, true>;
   const int occ = occupancy_of(ctx, kern, smem);
@@ -215,6 +218,14 @@ cudaError_t launch_ul_f32_sig(dcdg_ctx* ctx, const void* H, const void* Y, int P
   kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K, kappa,
                                           static_cast<float2*>(X), dcdg::XMap{}, s2, gam, scale, ctx->d_status);
   return cudaGetLastError();
+}
+
+// B_c = 32 with U = 16 (the north-star tile, 8 lanes per problem) or U = 8
+// (the paper's / configs[0] tile, 4 lanes per problem)
+cudaError_t launch_ul_f32_sig(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                              float* s2, float gam, float scale, int U, cudaStream_t st) {
+  return U == 8 ? launch_ul_f32_sig_k<32, 8, 4>(ctx, H, Y, P, K, kappa, X, s2, gam, scale, st)
+                : launch_ul_f32_sig_k<32, 16, 8>(ctx, H, Y, P, K, kappa, X, s2, gam, scale, st);
 }
 
 template <int BC, int U, int G, int MINB>
@@ -849,7 +860,7 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
       return rc;
   } else if (optimal && ul_sig_shape(Bc, U, fmt)) {
     CUDA_TRY(launch_ul_f32_sig(ctx, H, y, static_cast<int>(P), K, kappa, x_local, sigma2, static_cast<float>(ex / n0),
-                               static_cast<float>(ex / U), st),
+                               static_cast<float>(ex / U), U, st),
              "ul_detect (fused variance) launch");
   } else if (spec) {
     CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, x_local, nullptr, st), "ul_detect launch");

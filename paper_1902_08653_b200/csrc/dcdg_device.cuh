@@ -425,7 +425,7 @@ __device__ __forceinline__ int apair_slot(int i, int jq) {
 }
 
 // post_eq_variance from A = I + gam G held as COLUMN PAIRS
-// (detect.cpp:112-130): lane k of the problem's 8 lanes keeps rows 2k and
+// (detect.cpp:112-130): lane k of the problem's U/2 lanes keeps rows 2k and
 // 2k+1 as R?r[jq] = (Re A[i][2jq], Re A[i][2jq+1]) and R?i[jq] likewise, so
 // every update of the sweep operator (same pivots and arithmetic as
 // gram_trace_inverse above) is 4 FFMA2 per column pair and row, the row's
@@ -444,7 +444,7 @@ __device__ __forceinline__ float gram_trace_inverse_cpairs(float2 (&R0r)[U / 2],
   for (int jq = 0; jq < NQ; ++jq)
     if (k == jq) dmax = fmaxf(R0r[jq].x, R1r[jq].y);
 #pragma unroll
-  for (int o = 4; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  for (int o = U / 4; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   const float floor_ = 1e-14f * dmax;
 #pragma unroll
   for (int kk = 0; kk < U; ++kk) {
@@ -501,7 +501,7 @@ __device__ __forceinline__ float gram_trace_inverse_cpairs(float2 (&R0r)[U / 2],
   for (int jq = 0; jq < NQ; ++jq)
     if (k == jq) t = -(R0r[jq].x + R1r[jq].y);
 #pragma unroll
-  for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  for (int o = U / 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   return t;
 }
 

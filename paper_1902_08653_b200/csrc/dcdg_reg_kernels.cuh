@@ -168,8 +168,9 @@ __global__ void __launch_bounds__(32 * W, MINB)
                float2* __restrict__ X, const XMap xm, float* __restrict__ sigma2 = nullptr, float gam = 0.f,
                float scale = 0.f, unsigned long long* __restrict__ status = nullptr) {
   static_assert(32 % G == 0 && BC % (2 * G) == 0 && U % LB == 0, "shape");
-  static_assert(!SIG || (G == 8 && U == 16 && LB == 2 && !XCHG),
-                "fused variance: 8 lanes per problem hold rows 2k, 2k+1 of the 16 x 16 Gram");
+  static_assert(!SIG || ((U == 16 || U == 8) && G == U / 2 && BC % 16 == 0 && LB == 2 && !XCHG),
+                "fused variance: U/2 lanes per problem hold rows 2k, 2k+1 of the U x U Gram");
+  static_assert(!SIG || DCDG_SIG_CPAIRS || U == 16, "the scalar sweep operator is the U = 16 form");
   constexpr int NPW = 32 / G, R = BC / G, NP = R / 2;
   constexpr int T = LB * (LB - 1) / 2;  // Gram entries per block
   constexpr int TILE_B = BC * U * 8, Y_B = BC * 8, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
@@ -403,27 +404,33 @@ __global__ void __launch_bounds__(32 * W, MINB)
 #pragma unroll
           for (int ks = 0; ks < BC / 8; ++ks) {
             const float4 u0 = *reinterpret_cast<const float4*>(tb + mg * (BC * 8) + (8 * ks + 2 * mt) * 8);
-            const float4 u1 = *reinterpret_cast<const float4*>(tb + (mg + 8) * (BC * 8) + (8 * ks + 2 * mt) * 8);
             const float2 x00 = fmul2(sc, make_float2(u0.x, u0.y)), x01 = fmul2(sc, make_float2(u0.z, u0.w));
-            const float2 x10 = fmul2(sc, make_float2(u1.x, u1.y)), x11 = fmul2(sc, make_float2(u1.z, u1.w));
             uint32_t ah[4], al[4];
             split_h2(x00, ah[0], al[0]);  // user mg,     row 8ks + 2mt
-            split_h2(x10, ah[1], al[1]);  // user mg + 8, row 8ks + 2mt
             split_h2(x01, ah[2], al[2]);  // user mg,     row 8ks + 2mt + 1
-            split_h2(x11, ah[3], al[3]);  // user mg + 8, row 8ks + 2mt + 1
+            if constexpr (U == 16) {
+              const float4 u1 = *reinterpret_cast<const float4*>(tb + (mg + 8) * (BC * 8) + (8 * ks + 2 * mt) * 8);
+              const float2 x10 = fmul2(sc, make_float2(u1.x, u1.y)), x11 = fmul2(sc, make_float2(u1.z, u1.w));
+              split_h2(x10, ah[1], al[1]);  // user mg + 8, row 8ks + 2mt
+              split_h2(x11, ah[3], al[3]);  // user mg + 8, row 8ks + 2mt + 1
+            } else {  // U = 8: A rows 8-15 are zero
+              ah[1] = ah[3] = al[1] = al[3] = 0u;
+            }
             // B = W: n-tile 0 (users 0-7) = (a0, a2), n-tile 1 (users 8-15) = (a1, a3)
             mma_f16f32(gr0, ah, ah[0], ah[2]);
             mma_f16f32(gr0, ah, al[0], al[2]);
             mma_f16f32(gr0, al, ah[0], ah[2]);
-            mma_f16f32(gr1, ah, ah[1], ah[3]);
-            mma_f16f32(gr1, ah, al[1], al[3]);
-            mma_f16f32(gr1, al, ah[1], ah[3]);
             mma_f16f32(gi0, ah, wprime(ah[0]), wprime(ah[2]));
             mma_f16f32(gi0, ah, wprime(al[0]), wprime(al[2]));
             mma_f16f32(gi0, al, wprime(ah[0]), wprime(ah[2]));
-            mma_f16f32(gi1, ah, wprime(ah[1]), wprime(ah[3]));
-            mma_f16f32(gi1, ah, wprime(al[1]), wprime(al[3]));
-            mma_f16f32(gi1, al, wprime(ah[1]), wprime(ah[3]));
+            if constexpr (U == 16) {
+              mma_f16f32(gr1, ah, ah[1], ah[3]);
+              mma_f16f32(gr1, ah, al[1], al[3]);
+              mma_f16f32(gr1, al, ah[1], ah[3]);
+              mma_f16f32(gi1, ah, wprime(ah[1]), wprime(ah[3]));
+              mma_f16f32(gi1, ah, wprime(al[1]), wprime(al[3]));
+              mma_f16f32(gi1, al, wprime(ah[1]), wprime(ah[3]));
+            }
           }
           __syncwarp();  // every lane's reads of this tile are done before its image overwrites it
           const float gs = gam / (sc * sc);
@@ -432,11 +439,13 @@ __global__ void __launch_bounds__(32 * W, MINB)
           img[apair_slot<U>(mg, mt)] = make_float4(fmaf(gs, gr0[0], mg == 2 * mt ? 1.f : 0.f),
                                                    fmaf(gs, gr0[1], mg == 2 * mt + 1 ? 1.f : 0.f), gs * gi0[0],
                                                    gs * gi0[1]);
-          img[apair_slot<U>(mg, 4 + mt)] = make_float4(gs * gr1[0], gs * gr1[1], gs * gi1[0], gs * gi1[1]);
-          img[apair_slot<U>(mg + 8, mt)] = make_float4(gs * gr0[2], gs * gr0[3], gs * gi0[2], gs * gi0[3]);
-          img[apair_slot<U>(mg + 8, 4 + mt)] = make_float4(fmaf(gs, gr1[2], mg == 2 * mt ? 1.f : 0.f),
-                                                           fmaf(gs, gr1[3], mg == 2 * mt + 1 ? 1.f : 0.f),
-                                                           gs * gi1[2], gs * gi1[3]);
+          if constexpr (U == 16) {
+            img[apair_slot<U>(mg, 4 + mt)] = make_float4(gs * gr1[0], gs * gr1[1], gs * gi1[0], gs * gi1[1]);
+            img[apair_slot<U>(mg + 8, mt)] = make_float4(gs * gr0[2], gs * gr0[3], gs * gi0[2], gs * gi0[3]);
+            img[apair_slot<U>(mg + 8, 4 + mt)] = make_float4(fmaf(gs, gr1[2], mg == 2 * mt ? 1.f : 0.f),
+                                                             fmaf(gs, gr1[3], mg == 2 * mt + 1 ? 1.f : 0.f),
+                                                             gs * gi1[2], gs * gi1[3]);
+          }
         }
       }
       float* af = reinterpret_cast<float*>(slot + g * TILE_B);
@@ -484,7 +493,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
       const unsigned sing = __ballot_sync(0xffffffffu, singular);
       if (p < P && k == 0) {
         sigma2[p] = scale * tr;
-        if ((sing >> (G * g)) & 0xffu) record_status(status, p, ST_SINGULAR, 0);
+        if ((sing >> (G * g)) & ((1u << G) - 1u)) record_status(status, p, ST_SINGULAR, 0);
       }
     }
     __syncwarp();
