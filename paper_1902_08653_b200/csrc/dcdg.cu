@@ -22,6 +22,7 @@
 #include "dcdg_aux_kernels.cuh"
 #include "dcdg_gram_kernels.cuh"
 #include "dcdg_mw_kernels.cuh"
+#include "dcdg_pev_kernels.cuh"
 #include "dcdg_sweep_kernels.cuh"
 #include "dcdg_reg_kernels.cuh"
 #include "dcdg_split_kernels.cuh"
@@ -647,12 +648,41 @@ int launch_pev16(dcdg_ctx* ctx, const void* H, int P, float gam, float scale, bo
   return DCDG_OK;
 }
 
+// fp32 tiles with U in {8, 16, 32}: the tensor-core Gram + column-pair sweep
+// operator kernel (dcdg_pev_kernels.cuh)
+#ifndef DCDG_PEV_TC
+#define DCDG_PEV_TC 1
+#endif
+#ifndef DCDG_PEV_TC_MINB
+#define DCDG_PEV_TC_MINB 8
+#endif
+template <int U>
+int launch_pev_tc(dcdg_ctx* ctx, const void* H, int P, int Bc, float gam, float scale, float* s2, cudaStream_t st) {
+  using L = dcdg::PevTcSmem<U>;
+  constexpr size_t smem = L::kWarpB;
+  auto k = dcdg::pev_tc_kernel<U, DCDG_PEV_TC_MINB>;
+  const int occ = occupancy_of(ctx, k, smem, 32);
+  const int nsets = (P + L::kNpw - 1) / L::kNpw;
+  const int blocks = std::min(nsets, ctx->sms * occ);
+  k<<<blocks, 32, smem, st>>>(static_cast<const float2*>(H), P, Bc, gam, scale, s2, ctx->d_status);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "post_eq_variance launch");
+  return DCDG_OK;
+}
+
 #ifndef DCDG_PEV_PAIR
 #define DCDG_PEV_PAIR 1
 #endif
 int launch_post_eq(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, double n0, double ex, int fmt, float* s2,
                    cudaStream_t st) {
   const float gam = static_cast<float>(ex / n0), scale = static_cast<float>(ex / U);
+  // (B_c <= 256: beyond that the tensor cores' fp32 accumulation over 2 B_c
+  // real terms leaves sigma^2 at the 1e-5 parity edge; the FFMA Gram is used)
+  if (DCDG_PEV_TC && fmt == DCDG_FP32 && Bc % 4 == 0 && Bc <= 256) {
+    if (U == 16) return launch_pev_tc<16>(ctx, H, P, Bc, gam, scale, s2, st);
+    if (U == 32) return launch_pev_tc<32>(ctx, H, P, Bc, gam, scale, s2, st);
+    if (U == 8) return launch_pev_tc<8>(ctx, H, P, Bc, gam, scale, s2, st);
+  }
   if (DCDG_PEV_PAIR && U == 16) {
     const bool rnd = fmt == DCDG_FP16;
 #define PEV16(BT)                                                                                  \

@@ -1,0 +1,166 @@
+// Standalone post-equalization variance on the tensor cores (fp32 tiles):
+//     sigma^2_p = (E_x/U) tr((I + (E_x/N0) G_p)^-1),  G_p = H_p^H H_p
+// (post_eq_variance, src/detect.cpp:112-130; gram at :21-28), for the tile
+// shapes whose CD kernel has no fused variance (ul_reg_f32<..., SIG> covers
+// B_c = 32 with U = 8 and 16).
+//
+// Mapping: one warp per set of NPW = 64/U problems, U/2 lanes per problem in
+// the factorisation (lane k keeps rows 2k, 2k+1 of A as column pairs).
+//   * Gram: the whole warp, problem by problem, mma.sync.m16n8k8 TF32 with
+//     fp32 accumulation and a 3-pass split x = hi + lo (hi = rna-TF32(x),
+//     lo = rna-TF32(x - hi)): G = hi.hi + hi.lo + lo.hi, ~2^-21 relative to
+//     |h|^2, with fp32 range (no scaling).  Used up to B_c = 256 (the launcher
+//     keeps the FFMA Gram beyond, where the accumulation over 2 B_c real terms
+//     reaches the 1e-5 parity edge).  k-order: thread t of k-step s takes complex row
+//     4s + t, its re on k = t and its im on k = t + 4 (one 8-B load per user),
+//     so W' = (im, -re) is a register swap and a sign flip.  Tiles are read
+//     straight from global memory (each element once per problem).
+//   * A = I + gam G goes to a per-problem column-pair image in shared memory;
+//     the U/2 lanes read their rows and run the column-pair FFMA2 sweep
+//     operator (gram_trace_inverse_cpairs): 16 or 32 pivots in ascending
+//     order, the reference's pivot test (numerics.cpp:38-41,55-56).
+#pragma once
+
+#include "dcdg_device.cuh"
+
+namespace dcdg {
+
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// hi = rna-TF32(x), lo = rna-TF32(x - hi)
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = tf32_rna(x);
+  lo = tf32_rna(x - __uint_as_float(hi));
+}
+
+// D += A B, mma.sync m16n8k8, TF32 operands, fp32 accumulate
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int U>
+struct PevTcSmem {
+  static constexpr int kNpw = 64 / U;                      // problems per warp
+  static constexpr int kImgB = U * (U / 2) * 16;            // column-pair image of one problem
+  static constexpr int kRowB = 2 * (U / 2) * 16;            // pivot-row broadcast of one problem
+  static constexpr int kWarpB = kNpw * (kImgB + kRowB);
+};
+
+template <int U, int MINB>
+__global__ void __launch_bounds__(32, MINB)
+    pev_tc_kernel(const float2* __restrict__ H, int P, int BC, float gam, float scale, float* __restrict__ sigma2,
+                  unsigned long long* __restrict__ status) {
+  static_assert(U == 8 || U == 16 || U == 32, "U in {8, 16, 32}");
+  using L = PevTcSmem<U>;
+  constexpr int NPW = L::kNpw, MT = (U + 15) / 16, NT = U / 8, NQ = U / 2;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x;
+  const int mg = lane >> 2, mt = lane & 3;           // mma fragment coordinates
+  const int q = lane / NQ, k = lane % NQ;            // factorisation: problem q of the set, rows 2k, 2k+1
+  float4* img_all = reinterpret_cast<float4*>(smem);
+  float4* prow_all = reinterpret_cast<float4*>(smem + NPW * L::kImgB);
+  const int nsets = (P + NPW - 1) / NPW;
+  // the tiles are read once, straight from global memory: the next set is
+  // prefetched into L2 one set ahead (one bulk prefetch per set)
+  auto prefetch = [&](int s_) {
+    if (lane == 0 && s_ < nsets) {
+      const int p0 = s_ * NPW, n = min(NPW, P - p0);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(H + static_cast<size_t>(p0) * BC * U),
+                   "r"(static_cast<uint32_t>(n * BC * U * 8))
+                   : "memory");
+    }
+  };
+  prefetch(blockIdx.x);
+  for (int set = blockIdx.x; set < nsets; set += gridDim.x) {
+    prefetch(set + gridDim.x);
+    // ---- Gram of each problem of the set on the tensor cores -> image of A
+#pragma unroll 1
+    for (int pl = 0; pl < NPW; ++pl) {
+      const int pc = min(set * NPW + pl, P - 1);
+      const float2* h = H + static_cast<size_t>(pc) * BC * U;
+      float gr[MT][NT][4] = {}, gi[MT][NT][4] = {};
+#pragma unroll 2
+      for (int ks = 0; ks < BC / 4; ++ks) {
+        const int row = 4 * ks + mt;
+        uint32_t ah[MT][4], al[MT][4];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          const int u0 = 16 * m + mg, u1 = u0 + 8;
+          const float2 v0 = h[static_cast<size_t>(u0) * BC + row];
+          split_tf32(v0.x, ah[m][0], al[m][0]);  // re: k = mt
+          split_tf32(v0.y, ah[m][2], al[m][2]);  // im: k = mt + 4
+          if (u1 < U) {
+            const float2 v1 = h[static_cast<size_t>(u1) * BC + row];
+            split_tf32(v1.x, ah[m][1], al[m][1]);
+            split_tf32(v1.y, ah[m][3], al[m][3]);
+          } else {
+            ah[m][1] = ah[m][3] = al[m][1] = al[m][3] = 0u;
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            // B column users 8n + mg: registers of m-tile n/2, rows (n & 1) ? +8 : +0
+            const int bm = n >> 1, bo = n & 1;
+            const uint32_t bh0 = ah[bm][bo], bh1 = ah[bm][2 + bo], bl0 = al[bm][bo], bl1 = al[bm][2 + bo];
+            mma_tf32(gr[m][n], ah[m], bh0, bh1);
+            mma_tf32(gr[m][n], ah[m], bl0, bl1);
+            mma_tf32(gr[m][n], al[m], bh0, bh1);
+            // W' = (im, -re): k = mt takes im, k = mt + 4 takes -re
+            mma_tf32(gi[m][n], ah[m], bh1, bh0 ^ 0x80000000u);
+            mma_tf32(gi[m][n], ah[m], bl1, bl0 ^ 0x80000000u);
+            mma_tf32(gi[m][n], al[m], bh1, bh0 ^ 0x80000000u);
+          }
+      }
+      // C fragment: [0..1] row 16m + mg, cols 8n + 2mt, +1; [2..3] row 16m + mg + 8
+      float4* img = img_all + pl * (L::kImgB / 16);
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int i = 16 * m + mg + 8 * hh;
+            if (i >= U) continue;
+            const int jq = 4 * n + mt, j0 = 2 * jq;
+            img[apair_slot<U>(i, jq)] =
+                make_float4(fmaf(gam, gr[m][n][2 * hh], i == j0 ? 1.f : 0.f),
+                            fmaf(gam, gr[m][n][2 * hh + 1], i == j0 + 1 ? 1.f : 0.f), gam * gi[m][n][2 * hh],
+                            gam * gi[m][n][2 * hh + 1]);
+          }
+    }
+    __syncwarp();
+    // ---- factorisation: lane k of problem q takes rows 2k, 2k+1 of A
+    float2 R0r[NQ], R0i[NQ], R1r[NQ], R1i[NQ];
+    {
+      const float4* a4 = img_all + q * (L::kImgB / 16);
+#pragma unroll
+      for (int jq = 0; jq < NQ; ++jq) {
+        const float4 a = a4[apair_slot<U>(2 * k, jq)], b = a4[apair_slot<U>(2 * k + 1, jq)];
+        R0r[jq] = make_float2(a.x, a.y);
+        R0i[jq] = make_float2(a.z, a.w);
+        R1r[jq] = make_float2(b.x, b.y);
+        R1i[jq] = make_float2(b.z, b.w);
+      }
+    }
+    bool singular = false;
+    const float tr = gram_trace_inverse_cpairs<U>(R0r, R0i, R1r, R1i, k, prow_all + q * (L::kRowB / 16), singular);
+    const unsigned sing = __ballot_sync(0xffffffffu, singular);
+    const int p = set * NPW + q;
+    if (p < P && k == 0) {
+      sigma2[p] = scale * tr;
+      if ((sing >> (NQ * q)) & static_cast<unsigned>((1ull << NQ) - 1)) record_status(status, p, ST_SINGULAR, 0);
+    }
+    __syncwarp();  // the image and pivot rows are reused by the next set
+  }
+}
+
+}  // namespace dcdg
