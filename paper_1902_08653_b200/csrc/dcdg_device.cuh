@@ -505,4 +505,123 @@ __device__ __forceinline__ float gram_trace_inverse_cpairs(float2 (&R0r)[U / 2],
   return t;
 }
 
+// Sweep operator with 2x2 block pivots (1) or single pivots (0): measured per
+// kernel (profiles/lab/README.md) -- the fused fp32 variance keeps single
+// pivots (0.402 vs 0.420 ms), the tensor-core variance kernel takes block
+// pivots at U <= 16 (U=16: 0.366 -> 0.314 ms) and single pivots at U = 32.
+#ifndef DCDG_SIG_BLOCK2
+#define DCDG_SIG_BLOCK2 0
+#endif
+#ifndef DCDG_PEV_TC_BLOCK2_MAXU
+#define DCDG_PEV_TC_BLOCK2_MAXU 16
+#endif
+// The same sweep operator two pivots at a time (a 2x2 block pivot on the
+// column pair qk = rows 2qk, 2qk+1 = the pair lane qk owns): with
+// P = A[{2qk,2qk+1}][{2qk,2qk+1}] = [[d0, c], [conj c, e]],
+//     a_ij -= A_iP P^-1 A_Pj  (i, j outside P),  A_iP <- A_iP P^-1,
+//     A_Pj <- P^-1 A_Pj,  A_PP <- -P^-1,
+// which is the two single sweeps composed, so A still ends as -A^-1.  The
+// pivots checked against the floor are those of the sequential sweep
+// (d0, then the Schur complement e - |c|^2/d0), as hermitian_solve's.  Half the
+// pivot chain (broadcast, barrier, reciprocal) per sweep; the same FFMA2 count.
+// `prow`: 2 x U/2 float4 per problem (both pivot rows of the block).
+template <int U>
+__device__ __forceinline__ float gram_trace_inverse_cpairs2(float2 (&R0r)[U / 2], float2 (&R0i)[U / 2],
+                                                            float2 (&R1r)[U / 2], float2 (&R1i)[U / 2], int k,
+                                                            float4* prow, bool& singular) {
+  constexpr int NQ = U / 2;
+  float dmax = 0.f;
+#pragma unroll
+  for (int jq = 0; jq < NQ; ++jq)
+    if (k == jq) dmax = fmaxf(R0r[jq].x, R1r[jq].y);
+#pragma unroll
+  for (int o = U / 4; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  const float floor_ = 1e-14f * dmax;
+  float4* slot0 = prow;
+  float4* slot1 = prow + NQ;
+#pragma unroll
+  for (int qk = 0; qk < NQ; ++qk) {
+    const bool own = (k == qk);
+    if (own) {  // both pivot rows, 8-B stores straight from the register pairs
+      const uint32_t a0 = smem_u32(slot0), a1 = smem_u32(slot1);
+#pragma unroll
+      for (int jq = 0; jq < NQ; ++jq) {
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a0 + 16 * jq), "f"(R0r[jq].x), "f"(R0r[jq].y) : "memory");
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a0 + 16 * jq + 8), "f"(R0i[jq].x), "f"(R0i[jq].y)
+                     : "memory");
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a1 + 16 * jq), "f"(R1r[jq].x), "f"(R1r[jq].y) : "memory");
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a1 + 16 * jq + 8), "f"(R1i[jq].x), "f"(R1i[jq].y)
+                     : "memory");
+      }
+    }
+    __syncwarp();
+    const float4 p0 = slot0[qk], p1 = slot1[qk];
+    const float d0 = p0.x, cr = p0.y, ci = p0.w, e = p1.y;  // P = [[d0, c], [conj c, e]]
+    const float cc = fmaf(cr, cr, ci * ci);
+    if (!(d0 > floor_)) singular = true;
+    const float det = fmaf(d0, e, -cc);                      // d0 (e - |c|^2 / d0)
+    if (!(det > floor_ * d0)) singular = true;
+    const float id = __frcp_rn(det);
+    // P^-1 = id [[e, -c], [-conj c, d0]]
+    const float q00 = id * e, q11 = id * d0, q01r = -id * cr, q01i = -id * ci;  // (P^-1)_01 = -id c
+    // row coefficients: f = A_iP P^-1 (i outside P) or I - P^-1 (the owner's rows)
+    float f00r, f00i, f01r, f01i, f10r, f10i, f11r, f11i;
+    {
+      // row 2k: a0 = A[2k][2qk], a1 = A[2k][2qk+1]
+      const float a0r = R0r[qk].x, a0i = R0i[qk].x, a1r = R0r[qk].y, a1i = R0i[qk].y;
+      // f0 = a0 q00 + a1 conj(q01) ;  f1 = a0 q01 + a1 q11   ((P^-1)_10 = conj((P^-1)_01))
+      f00r = fmaf(a0r, q00, fmaf(a1r, q01r, a1i * q01i));
+      f00i = fmaf(a0i, q00, fmaf(a1i, q01r, -a1r * q01i));
+      f01r = fmaf(a0r, q01r, fmaf(-a0i, q01i, a1r * q11));
+      f01i = fmaf(a0r, q01i, fmaf(a0i, q01r, a1i * q11));
+      const float b0r = R1r[qk].x, b0i = R1i[qk].x, b1r = R1r[qk].y, b1i = R1i[qk].y;
+      f10r = fmaf(b0r, q00, fmaf(b1r, q01r, b1i * q01i));
+      f10i = fmaf(b0i, q00, fmaf(b1i, q01r, -b1r * q01i));
+      f11r = fmaf(b0r, q01r, fmaf(-b0i, q01i, b1r * q11));
+      f11i = fmaf(b0r, q01i, fmaf(b0i, q01r, b1i * q11));
+    }
+    if (own) {  // I - P^-1
+      f00r = 1.f - q00;
+      f00i = 0.f;
+      f01r = -q01r;
+      f01i = -q01i;
+      f10r = -q01r;   // -(P^-1)_10 = -conj(q01)
+      f10i = q01i;
+      f11r = 1.f - q11;
+      f11i = 0.f;
+    }
+#pragma unroll
+    for (int jq = 0; jq < NQ; ++jq) {
+      const float4 v0 = slot0[jq], v1 = slot1[jq];
+      const float2 b0r = make_float2(v0.x, v0.y), b0i = make_float2(v0.z, v0.w);
+      const float2 b1r = make_float2(v1.x, v1.y), b1i = make_float2(v1.z, v1.w);
+      // (ar + i ai) -= f0 b0 + f1 b1 over the column pair, both rows
+      R0r[jq] = ffma2(f01i, b1i, ffma2(-f01r, b1r, ffma2(f00i, b0i, ffma2(-f00r, b0r, R0r[jq]))));
+      R0i[jq] = ffma2(-f01i, b1r, ffma2(-f01r, b1i, ffma2(-f00i, b0r, ffma2(-f00r, b0i, R0i[jq]))));
+      R1r[jq] = ffma2(f11i, b1i, ffma2(-f11r, b1r, ffma2(f10i, b0i, ffma2(-f10r, b0r, R1r[jq]))));
+      R1i[jq] = ffma2(-f11i, b1r, ffma2(-f11r, b1i, ffma2(-f10i, b0r, ffma2(-f10r, b0i, R1i[jq]))));
+    }
+    // the pivot columns: A_iP <- f (outside P), A_PP <- -P^-1 (the owner)
+    if (own) {
+      R0r[qk] = make_float2(-q00, -q01r);
+      R0i[qk] = make_float2(0.f, -q01i);
+      R1r[qk] = make_float2(-q01r, -q11);
+      R1i[qk] = make_float2(q01i, 0.f);
+    } else {
+      R0r[qk] = make_float2(f00r, f01r);
+      R0i[qk] = make_float2(f00i, f01i);
+      R1r[qk] = make_float2(f10r, f11r);
+      R1i[qk] = make_float2(f10i, f11i);
+    }
+    __syncwarp();  // every lane has read this block's rows before the next owner stores
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int jq = 0; jq < NQ; ++jq)
+    if (k == jq) t = -(R0r[jq].x + R1r[jq].y);
+#pragma unroll
+  for (int o = U / 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
 }  // namespace dcdg

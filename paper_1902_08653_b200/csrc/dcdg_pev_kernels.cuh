@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(32, MINB)
       }
     }
     bool singular = false;
-    const float tr = gram_trace_inverse_cpairs<U>(R0r, R0i, R1r, R1i, k, prow_all + q * (L::kRowB / 16), singular);
+    float4* prow = prow_all + q * (L::kRowB / 16);
+    const float tr = U <= DCDG_PEV_TC_BLOCK2_MAXU ? gram_trace_inverse_cpairs2<U>(R0r, R0i, R1r, R1i, k, prow, singular)
+                                       : gram_trace_inverse_cpairs<U>(R0r, R0i, R1r, R1i, k, prow, singular);
     const unsigned sing = __ballot_sync(0xffffffffu, singular);
     const int p = set * NPW + q;
     if (p < P && k == 0) {

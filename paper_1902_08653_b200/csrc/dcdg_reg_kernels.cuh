@@ -486,7 +486,8 @@ __global__ void __launch_bounds__(32 * W, MINB)
       // the pivot rows go through the problem's scalar block (dead after the sweeps)
       bool singular = false;
 #if DCDG_SIG_CPAIRS
-      const float tr = gram_trace_inverse_cpairs<U>(R0r, R0i, R1r, R1i, k, mnx, singular);
+      const float tr = DCDG_SIG_BLOCK2 ? gram_trace_inverse_cpairs2<U>(R0r, R0i, R1r, R1i, k, mnx, singular)
+                                         : gram_trace_inverse_cpairs<U>(R0r, R0i, R1r, R1i, k, mnx, singular);
 #else
       const float tr = gram_trace_inverse<U>(ar0, ai0, ar1, ai1, k, 0.f, mnx, singular, true);
 #endif
