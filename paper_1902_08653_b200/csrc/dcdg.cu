@@ -656,15 +656,15 @@ int launch_pev16(dcdg_ctx* ctx, const void* H, int P, float gam, float scale, bo
 #ifndef DCDG_PEV_TC_MINB
 #define DCDG_PEV_TC_MINB 8
 #endif
-template <int U>
+template <int U, typename T = float2>
 int launch_pev_tc(dcdg_ctx* ctx, const void* H, int P, int Bc, float gam, float scale, float* s2, cudaStream_t st) {
   using L = dcdg::PevTcSmem<U>;
   constexpr size_t smem = L::kWarpB;
-  auto k = dcdg::pev_tc_kernel<U, DCDG_PEV_TC_MINB>;
+  auto k = dcdg::pev_tc_kernel<U, DCDG_PEV_TC_MINB, T>;
   const int occ = occupancy_of(ctx, k, smem, 32);
   const int nsets = (P + L::kNpw - 1) / L::kNpw;
   const int blocks = std::min(nsets, ctx->sms * occ);
-  k<<<blocks, 32, smem, st>>>(static_cast<const float2*>(H), P, Bc, gam, scale, s2, ctx->d_status);
+  k<<<blocks, 32, smem, st>>>(static_cast<const T*>(H), P, Bc, gam, scale, s2, ctx->d_status);
   ++ctx->launches;
   CUDA_TRY(cudaGetLastError(), "post_eq_variance launch");
   return DCDG_OK;
@@ -682,6 +682,12 @@ int launch_post_eq(dcdg_ctx* ctx, const void* H, int P, int Bc, int U, double n0
     if (U == 16) return launch_pev_tc<16>(ctx, H, P, Bc, gam, scale, s2, st);
     if (U == 32) return launch_pev_tc<32>(ctx, H, P, Bc, gam, scale, s2, st);
     if (U == 8) return launch_pev_tc<8>(ctx, H, P, Bc, gam, scale, s2, st);
+  }
+  // fp16 tiles: the stored binary16 values multiply exactly on the tensor cores
+  if (DCDG_PEV_TC && fmt == DCDG_FP16 && Bc % 8 == 0) {
+    if (U == 16) return launch_pev_tc<16, __half2>(ctx, H, P, Bc, gam, scale, s2, st);
+    if (U == 32) return launch_pev_tc<32, __half2>(ctx, H, P, Bc, gam, scale, s2, st);
+    if (U == 8) return launch_pev_tc<8, __half2>(ctx, H, P, Bc, gam, scale, s2, st);
   }
   if (DCDG_PEV_PAIR && U == 16) {
     const bool rnd = fmt == DCDG_FP16;

@@ -21,6 +21,8 @@
 //     order, the reference's pivot test (numerics.cpp:38-41,55-56).
 #pragma once
 
+#include <type_traits>
+
 #include "dcdg_device.cuh"
 
 namespace dcdg {
@@ -53,10 +55,18 @@ struct PevTcSmem {
   static constexpr int kWarpB = kNpw * (kImgB + kRowB);
 };
 
-template <int U, int MINB>
+// fp16 tiles (row-pair planar {re_2i, re_2i+1, im_2i, im_2i+1}): the stored
+// binary16 values are multiplied exactly (mma.sync.m16n8k16, fp32
+// accumulate), one pass per tile; thread t of k-step s takes row pair 4s + t,
+// its re pair on k 2t, 2t+1 and its im pair on k 2t+8, 2t+9 (one 8-B load
+// per user), W' = (im, -re) again a swap and a sign flip; sigma^2 is rounded
+// to the fp16 wire format as the reference rounds its messages
+// (detect.cpp:170-173).
+template <int U, int MINB, typename T = float2>
 __global__ void __launch_bounds__(32, MINB)
-    pev_tc_kernel(const float2* __restrict__ H, int P, int BC, float gam, float scale, float* __restrict__ sigma2,
+    pev_tc_kernel(const T* __restrict__ Hin, int P, int BC, float gam, float scale, float* __restrict__ sigma2,
                   unsigned long long* __restrict__ status) {
+  constexpr bool F16 = std::is_same_v<T, __half2>;
   static_assert(U == 8 || U == 16 || U == 32, "U in {8, 16, 32}");
   using L = PevTcSmem<U>;
   constexpr int NPW = L::kNpw, MT = (U + 15) / 16, NT = U / 8, NQ = U / 2;
@@ -72,8 +82,9 @@ __global__ void __launch_bounds__(32, MINB)
   auto prefetch = [&](int s_) {
     if (lane == 0 && s_ < nsets) {
       const int p0 = s_ * NPW, n = min(NPW, P - p0);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(H + static_cast<size_t>(p0) * BC * U),
-                   "r"(static_cast<uint32_t>(n * BC * U * 8))
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                       reinterpret_cast<const unsigned char*>(Hin) + static_cast<size_t>(p0) * BC * U * sizeof(T)),
+                   "r"(static_cast<uint32_t>(n * BC * U * sizeof(T)))
                    : "memory");
     }
   };
@@ -84,8 +95,39 @@ __global__ void __launch_bounds__(32, MINB)
 #pragma unroll 1
     for (int pl = 0; pl < NPW; ++pl) {
       const int pc = min(set * NPW + pl, P - 1);
-      const float2* h = H + static_cast<size_t>(pc) * BC * U;
       float gr[MT][NT][4] = {}, gi[MT][NT][4] = {};
+      if constexpr (F16) {
+        const uint2* h2 = reinterpret_cast<const uint2*>(Hin) + static_cast<size_t>(pc) * (BC / 2) * U;
+#pragma unroll 2
+        for (int ks = 0; ks < BC / 8; ++ks) {
+          const int rp = 4 * ks + mt;  // row pair
+          uint32_t a[MT][4];
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            const int u0 = 16 * m + mg, u1 = u0 + 8;
+            const uint2 v0 = h2[static_cast<size_t>(u0) * (BC / 2) + rp];
+            a[m][0] = v0.x;  // re pair: k 2mt, 2mt+1
+            a[m][2] = v0.y;  // im pair: k 2mt+8, 2mt+9
+            if (u1 < U) {
+              const uint2 v1 = h2[static_cast<size_t>(u1) * (BC / 2) + rp];
+              a[m][1] = v1.x;
+              a[m][3] = v1.y;
+            } else {
+              a[m][1] = a[m][3] = 0u;
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < MT; ++m)
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+              const int bm = n >> 1, bo = n & 1;
+              const uint32_t b0 = a[bm][bo], b1 = a[bm][2 + bo];
+              mma_f16f32(gr[m][n], a[m], b0, b1);
+              mma_f16f32(gi[m][n], a[m], b1, b0 ^ 0x80008000u);
+            }
+        }
+      } else {
+      const float2* h = reinterpret_cast<const float2*>(Hin) + static_cast<size_t>(pc) * BC * U;
 #pragma unroll 2
       for (int ks = 0; ks < BC / 4; ++ks) {
         const int row = 4 * ks + mt;
@@ -120,6 +162,7 @@ __global__ void __launch_bounds__(32, MINB)
             mma_tf32(gi[m][n], al[m], bh1, bh0 ^ 0x80000000u);
           }
       }
+      }  // F16
       // C fragment: [0..1] row 16m + mg, cols 8n + 2mt, +1; [2..3] row 16m + mg + 8
       float4* img = img_all + pl * (L::kImgB / 16);
 #pragma unroll
@@ -158,7 +201,7 @@ __global__ void __launch_bounds__(32, MINB)
     const unsigned sing = __ballot_sync(0xffffffffu, singular);
     const int p = set * NPW + q;
     if (p < P && k == 0) {
-      sigma2[p] = scale * tr;
+      sigma2[p] = F16 ? __half2float(__float2half_rn(scale * tr)) : scale * tr;
       if ((sing >> (NQ * q)) & static_cast<unsigned>((1ull << NQ) - 1)) record_status(status, p, ST_SINGULAR, 0);
     }
     __syncwarp();  // the image and pivot rows are reused by the next set
