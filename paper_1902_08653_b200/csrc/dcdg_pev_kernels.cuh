@@ -98,70 +98,89 @@ __global__ void __launch_bounds__(32, MINB)
       float gr[MT][NT][4] = {}, gi[MT][NT][4] = {};
       if constexpr (F16) {
         const uint2* h2 = reinterpret_cast<const uint2*>(Hin) + static_cast<size_t>(pc) * (BC / 2) * U;
-#pragma unroll 2
-        for (int ks = 0; ks < BC / 8; ++ks) {
-          const int rp = 4 * ks + mt;  // row pair
-          uint32_t a[MT][4];
+        // chunks of KC k-steps: every load of a chunk in flight before its mma
+        constexpr int KC = 4;
+        const int nks = BC / 8;
+#pragma unroll 1
+        for (int ks0 = 0; ks0 < nks; ks0 += KC) {
+          uint2 v[KC][MT][2];
 #pragma unroll
-          for (int m = 0; m < MT; ++m) {
-            const int u0 = 16 * m + mg, u1 = u0 + 8;
-            const uint2 v0 = h2[static_cast<size_t>(u0) * (BC / 2) + rp];
-            a[m][0] = v0.x;  // re pair: k 2mt, 2mt+1
-            a[m][2] = v0.y;  // im pair: k 2mt+8, 2mt+9
-            if (u1 < U) {
-              const uint2 v1 = h2[static_cast<size_t>(u1) * (BC / 2) + rp];
-              a[m][1] = v1.x;
-              a[m][3] = v1.y;
-            } else {
-              a[m][1] = a[m][3] = 0u;
+          for (int c = 0; c < KC; ++c)
+#pragma unroll
+            for (int m = 0; m < MT; ++m)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const int u = 16 * m + mg + 8 * hh;
+                v[c][m][hh] = (ks0 + c < nks && u < U) ? h2[static_cast<size_t>(u) * (BC / 2) + 4 * (ks0 + c) + mt]
+                                                      : make_uint2(0u, 0u);
+              }
+#pragma unroll
+          for (int c = 0; c < KC; ++c) {
+            if (ks0 + c >= nks) break;
+            uint32_t a[MT][4];
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+              a[m][0] = v[c][m][0].x;  // re pair of row pair 4ks + mt: k 2mt, 2mt+1
+              a[m][2] = v[c][m][0].y;  // im pair: k 2mt+8, 2mt+9
+              a[m][1] = v[c][m][1].x;
+              a[m][3] = v[c][m][1].y;
             }
+#pragma unroll
+            for (int m = 0; m < MT; ++m)
+#pragma unroll
+              for (int n = 0; n < NT; ++n) {
+                const int bm = n >> 1, bo = n & 1;
+                const uint32_t b0 = a[bm][bo], b1 = a[bm][2 + bo];
+                mma_f16f32(gr[m][n], a[m], b0, b1);
+                mma_f16f32(gi[m][n], a[m], b1, b0 ^ 0x80008000u);
+              }
           }
-#pragma unroll
-          for (int m = 0; m < MT; ++m)
-#pragma unroll
-            for (int n = 0; n < NT; ++n) {
-              const int bm = n >> 1, bo = n & 1;
-              const uint32_t b0 = a[bm][bo], b1 = a[bm][2 + bo];
-              mma_f16f32(gr[m][n], a[m], b0, b1);
-              mma_f16f32(gi[m][n], a[m], b1, b0 ^ 0x80008000u);
-            }
         }
       } else {
-      const float2* h = reinterpret_cast<const float2*>(Hin) + static_cast<size_t>(pc) * BC * U;
-#pragma unroll 2
-      for (int ks = 0; ks < BC / 4; ++ks) {
-        const int row = 4 * ks + mt;
-        uint32_t ah[MT][4], al[MT][4];
+        const float2* h = reinterpret_cast<const float2*>(Hin) + static_cast<size_t>(pc) * BC * U;
+        constexpr int KC = 8;
+        const int nks = BC / 4;
+#pragma unroll 1
+        for (int ks0 = 0; ks0 < nks; ks0 += KC) {
+          float2 v[KC][MT][2];
 #pragma unroll
-        for (int m = 0; m < MT; ++m) {
-          const int u0 = 16 * m + mg, u1 = u0 + 8;
-          const float2 v0 = h[static_cast<size_t>(u0) * BC + row];
-          split_tf32(v0.x, ah[m][0], al[m][0]);  // re: k = mt
-          split_tf32(v0.y, ah[m][2], al[m][2]);  // im: k = mt + 4
-          if (u1 < U) {
-            const float2 v1 = h[static_cast<size_t>(u1) * BC + row];
-            split_tf32(v1.x, ah[m][1], al[m][1]);
-            split_tf32(v1.y, ah[m][3], al[m][3]);
-          } else {
-            ah[m][1] = ah[m][3] = al[m][1] = al[m][3] = 0u;
+          for (int c = 0; c < KC; ++c)
+#pragma unroll
+            for (int m = 0; m < MT; ++m)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const int u = 16 * m + mg + 8 * hh;
+                v[c][m][hh] = (ks0 + c < nks && u < U) ? h[static_cast<size_t>(u) * BC + 4 * (ks0 + c) + mt]
+                                                      : make_float2(0.f, 0.f);
+              }
+#pragma unroll
+          for (int c = 0; c < KC; ++c) {
+            if (ks0 + c >= nks) break;
+            uint32_t ah[MT][4], al[MT][4];
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+              split_tf32(v[c][m][0].x, ah[m][0], al[m][0]);  // re: k = mt
+              split_tf32(v[c][m][0].y, ah[m][2], al[m][2]);  // im: k = mt + 4
+              split_tf32(v[c][m][1].x, ah[m][1], al[m][1]);
+              split_tf32(v[c][m][1].y, ah[m][3], al[m][3]);
+            }
+#pragma unroll
+            for (int m = 0; m < MT; ++m)
+#pragma unroll
+              for (int n = 0; n < NT; ++n) {
+                // B column users 8n + mg: registers of m-tile n/2, rows (n & 1) ? +8 : +0
+                const int bm = n >> 1, bo = n & 1;
+                const uint32_t bh0 = ah[bm][bo], bh1 = ah[bm][2 + bo], bl0 = al[bm][bo], bl1 = al[bm][2 + bo];
+                mma_tf32(gr[m][n], ah[m], bh0, bh1);
+                mma_tf32(gr[m][n], ah[m], bl0, bl1);
+                mma_tf32(gr[m][n], al[m], bh0, bh1);
+                // W' = (im, -re): k = mt takes im, k = mt + 4 takes -re
+                mma_tf32(gi[m][n], ah[m], bh1, bh0 ^ 0x80000000u);
+                mma_tf32(gi[m][n], ah[m], bl1, bl0 ^ 0x80000000u);
+                mma_tf32(gi[m][n], al[m], bh1, bh0 ^ 0x80000000u);
+              }
           }
         }
-#pragma unroll
-        for (int m = 0; m < MT; ++m)
-#pragma unroll
-          for (int n = 0; n < NT; ++n) {
-            // B column users 8n + mg: registers of m-tile n/2, rows (n & 1) ? +8 : +0
-            const int bm = n >> 1, bo = n & 1;
-            const uint32_t bh0 = ah[bm][bo], bh1 = ah[bm][2 + bo], bl0 = al[bm][bo], bl1 = al[bm][2 + bo];
-            mma_tf32(gr[m][n], ah[m], bh0, bh1);
-            mma_tf32(gr[m][n], ah[m], bl0, bl1);
-            mma_tf32(gr[m][n], al[m], bh0, bh1);
-            // W' = (im, -re): k = mt takes im, k = mt + 4 takes -re
-            mma_tf32(gi[m][n], ah[m], bh1, bh0 ^ 0x80000000u);
-            mma_tf32(gi[m][n], ah[m], bl1, bl0 ^ 0x80000000u);
-            mma_tf32(gi[m][n], al[m], bh1, bh0 ^ 0x80000000u);
-          }
-      }
       }  // F16
       // C fragment: [0..1] row 16m + mg, cols 8n + 2mt, +1; [2..3] row 16m + mg + 8
       float4* img = img_all + pl * (L::kImgB / 16);
