@@ -26,6 +26,7 @@
 #include "dcdg_sweep_kernels.cuh"
 #include "dcdg_reg_kernels.cuh"
 #include "dcdg_split_kernels.cuh"
+#include "dcdg_tmem_kernels.cuh"
 
 struct dcdg_ctx {
   int device = 0;
@@ -227,6 +228,29 @@ cudaError_t launch_ul_f32_sig(dcdg_ctx* ctx, const void* H, const void* Y, int P
                               float* s2, float gam, float scale, int U, cudaStream_t st) {
   return U == 8 ? launch_ul_f32_sig_k<32, 8, 4>(ctx, H, Y, P, K, kappa, X, s2, gam, scale, st)
                 : launch_ul_f32_sig_k<32, 16, 8>(ctx, H, Y, P, K, kappa, X, s2, gam, scale, st);
+}
+
+// The north-star tile with half of it in TMEM and 4 lanes per problem
+// (dcdg_tmem_kernels.cuh), uniform-fusion CD only.
+#ifndef DCDG_UL_TMEM
+#define DCDG_UL_TMEM 0
+#endif
+#ifndef DCDG_UL_TMEM_MINB
+#define DCDG_UL_TMEM_MINB 2
+#endif
+bool ul_tm_shape(int bc, int u, int fmt) { return DCDG_UL_TMEM && fmt == DCDG_FP32 && bc == 32 && u == 16; }
+
+cudaError_t launch_ul_tm(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                         cudaStream_t st) {
+  constexpr int NPW = 8;
+  constexpr size_t smem = dcdg::kTmWarps * NPW * dcdg::ul_scal_bytes(16, 2);
+  auto kern = dcdg::ul_tm_f32<DCDG_UL_TMEM_MINB>;
+  const int occ = occupancy_of(ctx, kern, smem, 32 * dcdg::kTmWarps);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int blocks = std::min((nsets + dcdg::kTmWarps - 1) / dcdg::kTmWarps, ctx->sms * occ);
+  kern<<<blocks, 32 * dcdg::kTmWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K,
+                                                   kappa, static_cast<float2*>(X));
+  return cudaGetLastError();
 }
 
 template <int BC, int U, int G, int MINB>
@@ -898,6 +922,8 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
     CUDA_TRY(launch_ul_f32_sig(ctx, H, y, static_cast<int>(P), K, kappa, x_local, sigma2, static_cast<float>(ex / n0),
                                static_cast<float>(ex / U), U, st),
              "ul_detect (fused variance) launch");
+  } else if (ul_tm_shape(Bc, U, fmt)) {
+    CUDA_TRY(launch_ul_tm(ctx, H, y, static_cast<int>(P), K, kappa, x_local, st), "ul_detect (TMEM tile) launch");
   } else if (spec) {
     CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, x_local, nullptr, st), "ul_detect launch");
   } else {

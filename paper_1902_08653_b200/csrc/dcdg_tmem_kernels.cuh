@@ -1,0 +1,257 @@
+// Uplink CD kernel with half of each channel tile in tensor memory (TMEM),
+// so that 4 lanes own a problem instead of 8 (sm_100a).
+//
+// Why: per coordinate block the sweep pays a fixed chain (dot -> butterfly ->
+// scalar update -> rank-1 update) and per-lane overhead; 4 lanes per problem
+// halve the butterfly levels' share and do twice the FMA work per reduction
+// (the 32x8 tile, which fits registers at 4 lanes, runs ~30% fewer
+// instructions per byte than the 32x16 tile at 8 lanes).  At 4 lanes the
+// 32x16 fp32 tile is 256 registers per lane, so the odd coordinate blocks'
+// columns live in TMEM (tcgen05.st at load, tcgen05.ld one block ahead of use,
+// 32 registers per block) and the even blocks' columns in registers.
+//
+// Mapping: CTA of 4 warps (warp w uses TMEM lanes [32 (w%4), +32)), each warp
+// independent with NPW = 8 problems; lane k of group g owns 16-B row chunks
+// q*4 + k (8 rows, 4 row pairs).  Tiles are read with 16-B non-allocating
+// loads after an L2 bulk prefetch one set ahead (no staging slot: 8 problems
+// are 35 KB).  Arithmetic = ul_reg_f32 (coordinate pairs with the pair-Gram
+// correction, FFMA2 on planar row pairs): cd_detect, src/detect.cpp:67-110.
+#pragma once
+
+#include "dcdg_split_kernels.cuh"
+
+namespace dcdg {
+
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const float2 (&a)[8], const float2 (&b)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+      "f"(a[0].x), "f"(a[0].y), "f"(a[1].x), "f"(a[1].y), "f"(a[2].x), "f"(a[2].y), "f"(a[3].x), "f"(a[3].y),
+      "f"(a[4].x), "f"(a[4].y), "f"(a[5].x), "f"(a[5].y), "f"(a[6].x), "f"(a[6].y), "f"(a[7].x), "f"(a[7].y),
+      "f"(b[0].x), "f"(b[0].y), "f"(b[1].x), "f"(b[1].y), "f"(b[2].x), "f"(b[2].y), "f"(b[3].x), "f"(b[3].y),
+      "f"(b[4].x), "f"(b[4].y), "f"(b[5].x), "f"(b[5].y), "f"(b[6].x), "f"(b[6].y), "f"(b[7].x), "f"(b[7].y));
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, float2 (&a)[8], float2 (&b)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=f"(a[0].x), "=f"(a[0].y), "=f"(a[1].x), "=f"(a[1].y), "=f"(a[2].x), "=f"(a[2].y), "=f"(a[3].x),
+        "=f"(a[3].y), "=f"(a[4].x), "=f"(a[4].y), "=f"(a[5].x), "=f"(a[5].y), "=f"(a[6].x), "=f"(a[6].y),
+        "=f"(a[7].x), "=f"(a[7].y), "=f"(b[0].x), "=f"(b[0].y), "=f"(b[1].x), "=f"(b[1].y), "=f"(b[2].x),
+        "=f"(b[2].y), "=f"(b[3].x), "=f"(b[3].y), "=f"(b[4].x), "=f"(b[4].y), "=f"(b[5].x), "=f"(b[5].y),
+        "=f"(b[6].x), "=f"(b[6].y), "=f"(b[7].x), "=f"(b[7].y)
+      : "r"(addr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 4 warps per CTA; TMEM: 128 columns per CTA (each warp its lane quarter)
+constexpr int kTmWarps = 4;
+constexpr int kTmCols = 128;
+
+template <int MINB>
+__global__ void __launch_bounds__(32 * kTmWarps, MINB)
+    ul_tm_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
+              float2* __restrict__ X) {
+  constexpr int BC = 32, U = 16, G = 4, LB = 2, NPW = 32 / G, R = BC / G, NP = R / 2;  // NP = 4
+  constexpr int NQ = U / LB;                  // 8 coordinate blocks; odd blocks in TMEM
+  constexpr int T4 = BC * U / 2, Y4 = BC / 2;  // float4 per tile / per receive vector
+  constexpr int SCAL_B = ul_scal_bytes(U, LB);
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint32_t tmem_base_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / G, k = lane % G;
+  float4* mnx = reinterpret_cast<float4*>(smem + (warp * NPW + g) * SCAL_B);
+  float4* gb = mnx + U;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "n"(kTmCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tbase = tmem_base_s + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int nw = gridDim.x * kTmWarps;
+  int set = blockIdx.x * kTmWarps + warp;
+  auto prefetch = [&](int s_) {
+    if (lane == 0 && s_ < nsets) {
+      const int p0 = s_ * NPW, n = min(NPW, P - p0);
+      prefetch_l2(H + static_cast<size_t>(p0) * BC * U, n * T4 * 16);
+      prefetch_l2(Y + static_cast<size_t>(p0) * BC, n * Y4 * 16);
+    }
+  };
+  prefetch(set);
+  const float2 z2 = make_float2(0.f, 0.f);
+  for (; set < nsets; set += nw) {
+    prefetch(set + nw);
+    const int p = set * NPW + g;
+    const int pc = min(p, P - 1);
+    const float4* h4 = reinterpret_cast<const float4*>(H) + static_cast<size_t>(pc) * T4;
+    const float4* y4 = reinterpret_cast<const float4*>(Y) + static_cast<size_t>(pc) * Y4;
+    // even blocks' columns (2q, 2q+1, q even) in registers: slot rq = q/2
+    float2 hr[NQ / 2][2][NP], hi[NQ / 2][2][NP], rr[NP], ri[NP];
+    float nrm[U], pgr[NQ], pgi[NQ];  // column energies and pair Grams G_{2q+1,2q} (lane partials)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      float2 ar[NP], ai[NP], br[NP], bi[NP];
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        const float4 va = ldg_na(h4 + (2 * q) * (BC / 2) + c * G + k);
+        const float4 vb = ldg_na(h4 + (2 * q + 1) * (BC / 2) + c * G + k);
+        ar[c] = pair(va.x, va.z);
+        ai[c] = pair(va.y, va.w);
+        br[c] = pair(vb.x, vb.z);
+        bi[c] = pair(vb.y, vb.w);
+      }
+      float2 ea = fmul2(ar[0], ar[0]), eb = fmul2(br[0], br[0]), gr = z2, gi = z2;
+      ea = ffma2(ai[0], ai[0], ea);
+      eb = ffma2(bi[0], bi[0], eb);
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        if (c > 0) {
+          ea = ffma2(ai[c], ai[c], ffma2(ar[c], ar[c], ea));
+          eb = ffma2(bi[c], bi[c], ffma2(br[c], br[c], eb));
+        }
+        gr = ffma2(bi[c], ai[c], ffma2(br[c], ar[c], gr));  // G_{2q+1,2q} = h_{2q+1}^H h_{2q}
+        gi = ffma2(neg2(bi[c]), ar[c], ffma2(br[c], ai[c], gi));
+      }
+      nrm[2 * q] = hsum(ea);
+      nrm[2 * q + 1] = hsum(eb);
+      pgr[q] = hsum(gr);
+      pgi[q] = hsum(gi);
+      if (q & 1) {
+        // TMEM block q/2: (ar, ai) as 8 float2 then (br, bi)
+        float2 ta[8], tb[8];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          ta[2 * c] = ar[c];
+          ta[2 * c + 1] = ai[c];
+          tb[2 * c] = br[c];
+          tb[2 * c + 1] = bi[c];
+        }
+        tmem_st32(tbase + 32 * (q / 2), ta, tb);
+      } else {
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          hr[q / 2][0][c] = ar[c];
+          hi[q / 2][0][c] = ai[c];
+          hr[q / 2][1][c] = br[c];
+          hi[q / 2][1][c] = bi[c];
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NP; ++c) {
+      const float4 v = ldg_na(y4 + c * G + k);
+      rr[c] = pair(v.x, v.z);
+      ri[c] = pair(v.y, v.w);
+    }
+    // ---- per-problem scalars, reduce-scattered over the group
+    {
+      group_reduce_scatter<G>(nrm, k);
+#pragma unroll
+      for (int i = 0; i < U / G; ++i) {
+        const int idx = k * (U / G) + i;
+        const float m = __fdividef(1.f, nrm[i] + kappa);  // m_j = 1/(||h_j||^2 + N0/Ex)
+        mnx[idx] = make_float4(m, m * nrm[i], 0.f, 0.f);  // n_j = m_j ||h_j||^2, x_j = 0
+      }
+      float v[2 * NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        v[2 * q] = pgr[q];
+        v[2 * q + 1] = pgi[q];
+      }
+      group_reduce_scatter<G>(v, k);
+      float* gf = reinterpret_cast<float*>(gb);
+#pragma unroll
+      for (int i = 0; i < 2 * NQ / G; ++i) {
+        const int gi2 = k * (2 * NQ / G) + i, e = gi2 >> 1;
+        if (gi2 & 1) {  // stored as (Re G, Im G, -Im G, Re G)
+          gf[e * 4 + 1] = v[i];
+          gf[e * 4 + 2] = -v[i];
+        } else {
+          gf[e * 4 + 0] = v[i];
+          gf[e * 4 + 3] = v[i];
+        }
+      }
+    }
+    tmem_wait_st();
+    __syncwarp();
+
+    // ---- K sweeps; the odd block's columns come from TMEM one block ahead
+    float2 tA[8], tB[8];
+    for (int t = 0; t < K; ++t) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const bool tm = q & 1;
+        // an even block starts the load of the next (odd) block's columns,
+        // which lands while this block's chain runs; the odd block waits for it
+        if (!tm) tmem_ld32(tbase + 32 * (q / 2), tA, tB);
+        if (tm) tmem_wait_ld();
+        float2 ar[NP], ai[NP], br[NP], bi[NP];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          ar[c] = tm ? tA[2 * c] : hr[q / 2][0][c];
+          ai[c] = tm ? tA[2 * c + 1] : hi[q / 2][0][c];
+          br[c] = tm ? tB[2 * c] : hr[q / 2][1][c];
+          bi[c] = tm ? tB[2 * c + 1] : hi[q / 2][1][c];
+        }
+        float2 d[LB];
+        {
+          float2 a0 = z2, c0 = z2, a1 = z2, c1 = z2;  // h_j^H r for j = 2q, 2q+1 (cdotc, detect.cpp:100)
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            a0 = ffma2(ai[c], ri[c], ffma2(ar[c], rr[c], a0));
+            c0 = ffma2(neg2(ai[c]), rr[c], ffma2(ar[c], ri[c], c0));
+            a1 = ffma2(bi[c], ri[c], ffma2(br[c], rr[c], a1));
+            c1 = ffma2(neg2(bi[c]), rr[c], ffma2(br[c], ri[c], c1));
+          }
+          d[0] = make_float2(hsum(a0), hsum(c0));
+          d[1] = make_float2(hsum(a1), hsum(c1));
+        }
+        group_allreduce2<G>(d);
+        float2 dx[LB];
+        {
+          const float4 A0 = mnx[2 * q], A1 = mnx[2 * q + 1], Gab = gb[q];
+          const float2 x0 = make_float2(A0.z, A0.w);
+          const float2 n0 = ffma2(A0.x, d[0], fmul2(A0.y, x0));  // detect.cpp:100-103
+          dx[0] = fadd2(n0, neg2(x0));
+          d[1] = ffma2(-dx[0].x, make_float2(Gab.x, Gab.y), d[1]);  // h_1^H (r - dx_0 h_0)
+          d[1] = ffma2(-dx[0].y, make_float2(Gab.z, Gab.w), d[1]);
+          const float2 x1 = make_float2(A1.z, A1.w);
+          const float2 n1 = ffma2(A1.x, d[1], fmul2(A1.y, x1));
+          dx[1] = fadd2(n1, neg2(x1));
+          *reinterpret_cast<float2*>(&mnx[2 * q].z) = n0;
+          *reinterpret_cast<float2*>(&mnx[2 * q + 1].z) = n1;
+        }
+        // r -= dx_j h_j for the block   (caxpy, detect.cpp:104)
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          rr[c] = ffma2(dx[0].y, ai[c], ffma2(-dx[0].x, ar[c], rr[c]));
+          ri[c] = ffma2(-dx[0].y, ar[c], ffma2(-dx[0].x, ai[c], ri[c]));
+          rr[c] = ffma2(dx[1].y, bi[c], ffma2(-dx[1].x, br[c], rr[c]));
+          ri[c] = ffma2(-dx[1].y, br[c], ffma2(-dx[1].x, bi[c], ri[c]));
+        }
+      }
+    }
+    __syncwarp();
+    if (p < P) {
+      float4* xo = reinterpret_cast<float4*>(X + static_cast<size_t>(p) * U);
+#pragma unroll
+      for (int i = k; i < U / 2; i += G) {
+        const float4 u0 = mnx[2 * i], u1 = mnx[2 * i + 1];
+        xo[i] = make_float4(u0.z, u0.w, u1.z, u1.w);
+      }
+    }
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_s), "n"(kTmCols));
+}
+
+}  // namespace dcdg
