@@ -244,6 +244,16 @@ cudaError_t launch_ul_tm(dcdg_ctx* ctx, const void* H, const void* Y, int P, int
                          cudaStream_t st) {
   constexpr int NPW = 8;
   constexpr size_t smem = dcdg::kTmWarps * NPW * dcdg::ul_scal_bytes(16, 2);
+#if DCDG_UL_TMEM == 2  // staged in two TMA phases per set (dcdg_tmem_kernels.cuh)
+  constexpr size_t smem2 = dcdg::kTmWarps * (dcdg::kTm2SlotB + NPW * dcdg::ul_scal_bytes(16, 2)) + dcdg::kTmWarps * 16;
+  auto kern2 = dcdg::ul_tm2_f32<DCDG_UL_TMEM_MINB>;
+  const int occ2 = occupancy_of(ctx, kern2, smem2, 32 * dcdg::kTmWarps);
+  const int nsets2 = (P + NPW - 1) / NPW;
+  const int blocks2 = std::min((nsets2 + dcdg::kTmWarps - 1) / dcdg::kTmWarps, ctx->sms * occ2);
+  kern2<<<blocks2, 32 * dcdg::kTmWarps, smem2, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P,
+                                                      K, kappa, static_cast<float2*>(X));
+  return cudaGetLastError();
+#endif
   auto kern = dcdg::ul_tm_f32<DCDG_UL_TMEM_MINB>;
   const int occ = occupancy_of(ctx, kern, smem, 32 * dcdg::kTmWarps);
   const int nsets = (P + NPW - 1) / NPW;

@@ -254,4 +254,276 @@ __global__ void __launch_bounds__(32 * kTmWarps, MINB)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_s), "n"(kTmCols));
 }
 
+
+// ---------------------------------------------------------------------------
+// ul_tm2_f32: the same tile split with TMA staging in two phases per set, so
+// that no load is exposed.  Per warp an 18-KB slot and two TMEM buffers of
+// 128 columns (the CTA of 4 warps allocates 256):
+//   phase A (mbarrier A): the set's odd-block columns (8 problems x 4 column
+//     pairs of 512 B) -> slot; consumed in the MIDDLE of the previous set
+//     (after its first sweep): re-paired and stored to the other TMEM buffer,
+//     then phase B is issued into the slot;
+//   phase B (mbarrier B): the set's even-block columns and y -> slot; consumed
+//     at the set start into registers, then phase A of the next set is issued.
+// The odd blocks' norms and pair Grams are computed from TMEM at the set start.
+// ---------------------------------------------------------------------------
+constexpr int kTm2Cols = 256;
+constexpr int kTm2SlotB = 8 * 8 * 256 + 8 * 256;  // 8 problems x 8 columns + 8 receive vectors
+
+__device__ __forceinline__ void tm2_issue(unsigned char* slot, uint64_t* bar, const float2* H, const float2* Y,
+                                          int set, int P, bool odd, uint64_t pol) {
+  constexpr int BC = 32, U = 16, NPW = 8, COL_B = BC * 8, TILE_B = BC * U * 8;
+  const int p0 = set * NPW, n = min(NPW, P - p0);
+  mbar_arrive_expect_tx(bar, static_cast<uint32_t>(n * 8 * COL_B + (odd ? 0 : n * BC * 8)));
+  const unsigned char* hb = reinterpret_cast<const unsigned char*>(H) + static_cast<size_t>(p0) * TILE_B;
+  for (int pl = 0; pl < n; ++pl)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)  // column pair 2 (2b + odd) .. +1
+      bulk_g2s(slot + (pl * 4 + b) * 2 * COL_B, hb + pl * TILE_B + (2 * (2 * b + (odd ? 1 : 0))) * COL_B, 2 * COL_B,
+               bar, pol);
+  if (!odd)
+    bulk_g2s(slot + NPW * 8 * COL_B, reinterpret_cast<const unsigned char*>(Y) + static_cast<size_t>(p0) * BC * 8,
+             n * BC * 8, bar, pol);
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(32 * kTmWarps, MINB)
+    ul_tm2_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
+               float2* __restrict__ X) {
+  constexpr int BC = 32, U = 16, G = 4, LB = 2, NPW = 32 / G, R = BC / G, NP = R / 2;  // NP = 4
+  constexpr int NQ = U / LB;  // 8 coordinate blocks; odd blocks in TMEM
+  constexpr int COL_B = BC * 8;
+  constexpr int SCAL_B = ul_scal_bytes(U, LB);
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint32_t tmem_base_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / G, k = lane % G;
+  unsigned char* slot = smem + warp * kTm2SlotB;
+  float4* mnx = reinterpret_cast<float4*>(smem + kTmWarps * kTm2SlotB + (warp * NPW + g) * SCAL_B);
+  float4* gb = mnx + U;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTmWarps * kTm2SlotB + kTmWarps * NPW * SCAL_B) + 2 * warp;
+  uint64_t* barA = bars;
+  uint64_t* barB = bars + 1;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "n"(kTm2Cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (lane == 0) {
+    mbar_init(barA, 1);
+    mbar_init(barB, 1);
+    fence_mbar_init();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tq = tmem_base_s + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int nw = gridDim.x * kTmWarps;
+  int set = blockIdx.x * kTmWarps + warp;
+  const uint64_t pol = l2_evict_first_policy();
+  uint32_t phA = 0, phB = 0;
+  const float2 z2 = make_float2(0.f, 0.f);
+  // the odd columns of set `s_` from the slot (phase A landed) -> TMEM buffer `buf`
+  auto stage_odd = [&](int buf) {
+    mbar_wait(barA, phA);
+    phA ^= 1u;
+    const float4* s4 = reinterpret_cast<const float4*>(slot);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      float2 ta[8], tb[8];
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        const float4 va = s4[(g * 4 + b) * 2 * (COL_B / 16) + c * G + k];
+        const float4 vb = s4[(g * 4 + b) * 2 * (COL_B / 16) + (COL_B / 16) + c * G + k];
+        ta[2 * c] = pair(va.x, va.z);
+        ta[2 * c + 1] = pair(va.y, va.w);
+        tb[2 * c] = pair(vb.x, vb.z);
+        tb[2 * c + 1] = pair(vb.y, vb.w);
+      }
+      tmem_st32(tq + 128 * buf + 32 * b, ta, tb);
+    }
+  };
+  if (set < nsets) {
+    if (lane == 0) tm2_issue(slot, barA, H, Y, set, P, true, pol);
+    stage_odd(0);
+    tmem_wait_st();
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) tm2_issue(slot, barB, H, Y, set, P, false, pol);
+  }
+  int buf = 0;
+  for (; set < nsets; set += nw, buf ^= 1) {
+    const int p = set * NPW + g;
+    mbar_wait(barB, phB);
+    phB ^= 1u;
+    float2 hr[NQ / 2][2][NP], hi[NQ / 2][2][NP], rr[NP], ri[NP];
+    {
+      const float4* s4 = reinterpret_cast<const float4*>(slot);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            const float4 v = s4[(g * 4 + b) * 2 * (COL_B / 16) + h * (COL_B / 16) + c * G + k];
+            hr[b][h][c] = pair(v.x, v.z);
+            hi[b][h][c] = pair(v.y, v.w);
+          }
+      const float4* y4 = reinterpret_cast<const float4*>(slot + NPW * 8 * COL_B + g * COL_B);
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        const float4 v = y4[c * G + k];
+        rr[c] = pair(v.x, v.z);
+        ri[c] = pair(v.y, v.w);
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    const bool more = set + nw < nsets;
+    if (lane == 0 && more) tm2_issue(slot, barA, H, Y, set + nw, P, true, pol);
+    // ---- per-problem scalars: even blocks from registers, odd blocks from TMEM
+    {
+      float nrm[U], v[2 * NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        float2 ar[NP], ai[NP], br[NP], bi[NP];
+        if (q & 1) {
+          float2 tA[8], tB[8];
+          tmem_ld32(tq + 128 * buf + 32 * (q / 2), tA, tB);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            ar[c] = tA[2 * c];
+            ai[c] = tA[2 * c + 1];
+            br[c] = tB[2 * c];
+            bi[c] = tB[2 * c + 1];
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            ar[c] = hr[q / 2][0][c];
+            ai[c] = hi[q / 2][0][c];
+            br[c] = hr[q / 2][1][c];
+            bi[c] = hi[q / 2][1][c];
+          }
+        }
+        float2 ea = fmul2(ar[0], ar[0]), eb = fmul2(br[0], br[0]), gr = z2, gi = z2;
+        ea = ffma2(ai[0], ai[0], ea);
+        eb = ffma2(bi[0], bi[0], eb);
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          if (c > 0) {
+            ea = ffma2(ai[c], ai[c], ffma2(ar[c], ar[c], ea));
+            eb = ffma2(bi[c], bi[c], ffma2(br[c], br[c], eb));
+          }
+          gr = ffma2(bi[c], ai[c], ffma2(br[c], ar[c], gr));  // G_{2q+1,2q} = h_{2q+1}^H h_{2q}
+          gi = ffma2(neg2(bi[c]), ar[c], ffma2(br[c], ai[c], gi));
+        }
+        nrm[2 * q] = hsum(ea);
+        nrm[2 * q + 1] = hsum(eb);
+        v[2 * q] = hsum(gr);
+        v[2 * q + 1] = hsum(gi);
+      }
+      group_reduce_scatter<G>(nrm, k);
+#pragma unroll
+      for (int i = 0; i < U / G; ++i) {
+        const int idx = k * (U / G) + i;
+        const float m = __fdividef(1.f, nrm[i] + kappa);  // m_j = 1/(||h_j||^2 + N0/Ex)  (detect.cpp:86-90)
+        mnx[idx] = make_float4(m, m * nrm[i], 0.f, 0.f);  // n_j = m_j ||h_j||^2, x_j = 0
+      }
+      group_reduce_scatter<G>(v, k);
+      float* gf = reinterpret_cast<float*>(gb);
+#pragma unroll
+      for (int i = 0; i < 2 * NQ / G; ++i) {
+        const int gi2 = k * (2 * NQ / G) + i, e = gi2 >> 1;
+        if (gi2 & 1) {  // stored as (Re G, Im G, -Im G, Re G)
+          gf[e * 4 + 1] = v[i];
+          gf[e * 4 + 2] = -v[i];
+        } else {
+          gf[e * 4 + 0] = v[i];
+          gf[e * 4 + 3] = v[i];
+        }
+      }
+    }
+    __syncwarp();
+
+    float2 tA[8], tB[8];
+    for (int t = 0; t < K; ++t) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const bool tm = q & 1;
+        if (!tm) tmem_ld32(tq + 128 * buf + 32 * (q / 2), tA, tB);  // the next (odd) block, one block ahead
+        if (tm) tmem_wait_ld();
+        float2 ar[NP], ai[NP], br[NP], bi[NP];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          ar[c] = tm ? tA[2 * c] : hr[q / 2][0][c];
+          ai[c] = tm ? tA[2 * c + 1] : hi[q / 2][0][c];
+          br[c] = tm ? tB[2 * c] : hr[q / 2][1][c];
+          bi[c] = tm ? tB[2 * c + 1] : hi[q / 2][1][c];
+        }
+        float2 d[LB];
+        {
+          float2 a0 = z2, c0 = z2, a1 = z2, c1 = z2;  // h_j^H r for j = 2q, 2q+1 (cdotc, detect.cpp:100)
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            a0 = ffma2(ai[c], ri[c], ffma2(ar[c], rr[c], a0));
+            c0 = ffma2(neg2(ai[c]), rr[c], ffma2(ar[c], ri[c], c0));
+            a1 = ffma2(bi[c], ri[c], ffma2(br[c], rr[c], a1));
+            c1 = ffma2(neg2(bi[c]), rr[c], ffma2(br[c], ri[c], c1));
+          }
+          d[0] = make_float2(hsum(a0), hsum(c0));
+          d[1] = make_float2(hsum(a1), hsum(c1));
+        }
+        group_allreduce2<G>(d);
+        float2 dx[LB];
+        {
+          const float4 A0 = mnx[2 * q], A1 = mnx[2 * q + 1], Gab = gb[q];
+          const float2 x0 = make_float2(A0.z, A0.w);
+          const float2 n0 = ffma2(A0.x, d[0], fmul2(A0.y, x0));  // detect.cpp:100-103
+          dx[0] = fadd2(n0, neg2(x0));
+          d[1] = ffma2(-dx[0].x, make_float2(Gab.x, Gab.y), d[1]);  // h_1^H (r - dx_0 h_0)
+          d[1] = ffma2(-dx[0].y, make_float2(Gab.z, Gab.w), d[1]);
+          const float2 x1 = make_float2(A1.z, A1.w);
+          const float2 n1 = ffma2(A1.x, d[1], fmul2(A1.y, x1));
+          dx[1] = fadd2(n1, neg2(x1));
+          *reinterpret_cast<float2*>(&mnx[2 * q].z) = n0;
+          *reinterpret_cast<float2*>(&mnx[2 * q + 1].z) = n1;
+        }
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {  // r -= dx_j h_j (caxpy, detect.cpp:104)
+          rr[c] = ffma2(dx[0].y, ai[c], ffma2(-dx[0].x, ar[c], rr[c]));
+          ri[c] = ffma2(-dx[0].y, ar[c], ffma2(-dx[0].x, ai[c], ri[c]));
+          rr[c] = ffma2(dx[1].y, bi[c], ffma2(-dx[1].x, br[c], rr[c]));
+          ri[c] = ffma2(-dx[1].y, br[c], ffma2(-dx[1].x, bi[c], ri[c]));
+        }
+      }
+      if (t == 0 && more) {
+        // the next set's odd columns -> the other TMEM buffer, then its even
+        // columns and y into the slot (they land during the remaining sweeps)
+        stage_odd(buf ^ 1);
+        tmem_wait_st();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) tm2_issue(slot, barB, H, Y, set + nw, P, false, pol);
+      }
+    }
+    __syncwarp();
+    if (p < P) {
+      float4* xo = reinterpret_cast<float4*>(X + static_cast<size_t>(p) * U);
+#pragma unroll
+      for (int i = k; i < U / 2; i += G) {
+        const float4 u0 = mnx[2 * i], u1 = mnx[2 * i + 1];
+        xo[i] = make_float4(u0.z, u0.w, u1.z, u1.w);
+      }
+    }
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_s), "n"(kTm2Cols));
+}
+
 }  // namespace dcdg
