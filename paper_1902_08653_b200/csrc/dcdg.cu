@@ -242,6 +242,7 @@ bool ul_tm_shape(int bc, int u, int fmt) { return DCDG_UL_TMEM && fmt == DCDG_FP
 
 cudaError_t launch_ul_tm(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
                          cudaStream_t st) {
+#if DCDG_UL_TMEM  // lab kernels (profiles/lab/README.md): only compiled when switched on
   constexpr int NPW = 8;
   constexpr size_t smem = dcdg::kTmWarps * NPW * dcdg::ul_scal_bytes(16, 2);
 #if DCDG_UL_TMEM == 2  // staged in two TMA phases per set (dcdg_tmem_kernels.cuh)
@@ -261,6 +262,10 @@ cudaError_t launch_ul_tm(dcdg_ctx* ctx, const void* H, const void* Y, int P, int
   kern<<<blocks, 32 * dcdg::kTmWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K,
                                                    kappa, static_cast<float2*>(X));
   return cudaGetLastError();
+#else
+  (void)ctx, (void)H, (void)Y, (void)P, (void)K, (void)kappa, (void)X, (void)st;
+  return cudaErrorNotSupported;
+#endif
 }
 
 template <int BC, int U, int G, int MINB>
