@@ -448,12 +448,13 @@ def run_ours(args):
         barrier()
         l_a = eng.launches
         tr_a = (d.traffic.uplink_payload_bytes, d.traffic.uplink_bus_bytes, d.traffic.messages)
-        # N=1: the K steps are captured once into a CUDA graph and the timed
-        # region is its replay, so host launch overhead (and the clock sampler
-        # thread) cannot starve the GPU between steps.  N>1 runs eagerly: the
-        # exchange windows take a host-side batch epoch per call.
+        # The K steps are captured once into a CUDA graph and the timed region
+        # is its replay, so host launch overhead (and the clock sampler thread)
+        # cannot starve the GPU between steps: at N=1, and at N>1 with the
+        # peer-memory exchange (its batch epochs advance on the device, so the
+        # replay publishes fresh epochs).  The NCCL modes run eagerly.
         graph = None
-        if world == 1 and not args.eager:
+        if (world == 1 or getattr(d, "mode", None) == "p2p") and not args.eager:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
                 for _ in range(steps):
@@ -618,7 +619,8 @@ def run_ours(args):
                    "parallelism": (f"clusters/{world}, fusion exchange {mode_used}" if world > 1
                                    else "single GPU, all clusters"),
                    "l2": f"inputs {alg / 1e6:.0f} MB/GPU > 126 MB L2, no flush needed",
-                   "launch": ("one CUDA-graph replay of the K steps" if world == 1 and not args.eager
+                   "launch": ("one CUDA-graph replay of the K steps"
+                              if (world == 1 or mode_used == "p2p") and not args.eager
                               else "eager, one host call per step"),
                    "kernel": kernel_name("ul", BC, U, fmt)},
         "batch_latency_ms": round(ms, 5),

@@ -53,7 +53,9 @@ struct dcdg_xwin {
   // the window's calls in issue order, so an uplink and a downlink call never
   // reuse a parity buffer before every peer's wait of the call in between
   // (which implies all consumers of the older call are done) — DESIGN §6.1.
-  unsigned long long epoch = 0;
+  // The counter lives in device memory and each call's first kernel advances
+  // it, so a call captured into a CUDA graph replays with fresh epochs.
+  unsigned long long* d_epoch = nullptr;
   long long timeout_ns = 20000000000LL;  // 20 s: a missing peer becomes ST_XCHG_TIMEOUT, not a hang
 };
 
@@ -1451,10 +1453,13 @@ int dcdg_xwin_create(dcdg_ctx* ctx, int world, int rank, int64_t buf_bytes, dcdg
   if (e == cudaSuccess) e = cudaMemset(w->base, 0, dcdg::kXchgFlagBytes);
   if (e == cudaSuccess) e = cudaMalloc(&w->counter, sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(w->counter, 0, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&w->d_epoch, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(w->d_epoch, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     if (w->base) cudaFree(w->base);
     if (w->counter) cudaFree(w->counter);
+    if (w->d_epoch) cudaFree(w->d_epoch);
     delete w;
     return cuda_fail(e, "dcdg_xwin_create");
   }
@@ -1502,6 +1507,7 @@ int dcdg_xwin_destroy(dcdg_xwin* w) {
     if (q != w->rank && w->opened[q] && w->peer[q]) cudaIpcCloseMemHandle(w->peer[q]);
   if (w->base) cudaFree(w->base);
   if (w->counter) cudaFree(w->counter);
+  if (w->d_epoch) cudaFree(w->d_epoch);
   delete w;
   return DCDG_OK;
 }
@@ -1544,7 +1550,7 @@ int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* 
   dcdg::XMap m{};
   for (int q = 0; q < w->world; ++q) m.win[q] = w->peer[q];
   m.counter = w->counter;
-  m.epoch = ++w->epoch;
+  m.epoch_dev = w->d_epoch;
   m.flag_slot = 0;  // uplink: rank q publishes to slot q
   m.per_rank = 1;
   m.buf_bytes = w->buf_bytes;
@@ -1557,7 +1563,9 @@ int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* 
   m.C_total = C_total;
   m.U = U;
   m.esz = static_cast<int>(esize(fmt));
-  m.parity = static_cast<int>(m.epoch & 1);
+  dcdg::xchg_advance_kernel<<<1, 1, 0, st>>>(w->d_epoch);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "xchg_advance launch");
 
   const float kappa = static_cast<float>(n0 / ex);
   const Spec* spec = find_spec(Bc, U, fmt);
@@ -1590,7 +1598,7 @@ int dcdg_ul_detect_xchg(dcdg_ctx* ctx, dcdg_xwin* w, const void* H, const void* 
   const int threads = 256;
   const long long blocks = std::max(1LL, std::min<long long>((n + threads - 1) / threads, 2LL * ctx->sms));
 #define XFUSE(T)                                                                                               \
-  dcdg::xchg_fuse_kernel<T><<<blocks, threads, 0, st>>>(w->base, m.epoch, w->world, m.parity, w->buf_bytes,    \
+  dcdg::xchg_fuse_kernel<T><<<blocks, threads, 0, st>>>(w->base, w->d_epoch, w->world, w->buf_bytes,           \
                                                         sig_off, S_own, C_total, U, optimal, w->timeout_ns,     \
                                                         reinterpret_cast<float2*>(xhat), ctx->d_status)
   if (fmt == DCDG_FP16)
@@ -1639,7 +1647,7 @@ int dcdg_dl_precode_xchg(dcdg_ctx* ctx, dcdg_xwin* w, int root, const void* H, c
   dcdg::XMap m{};
   for (int q = 0; q < w->world; ++q) m.win[q] = w->peer[q];
   m.counter = w->counter;
-  m.epoch = ++w->epoch;
+  m.epoch_dev = w->d_epoch;
   m.buf_bytes = w->buf_bytes;
   m.sig_off = gain_off;
   m.world = w->world;
@@ -1649,8 +1657,10 @@ int dcdg_dl_precode_xchg(dcdg_ctx* ctx, dcdg_xwin* w, int root, const void* H, c
   m.C_total = C_total;
   m.U = U;
   m.esz = static_cast<int>(esize(fmt));
-  m.parity = static_cast<int>(m.epoch & 1);
   const int threads = 256;
+  dcdg::xchg_advance_kernel<<<1, 1, 0, st>>>(w->d_epoch);
+  ++ctx->launches;
+  CUDA_TRY(cudaGetLastError(), "xchg_advance launch");
   // 1. root: the centre -> cluster symbol broadcast as stores into every window
   if (w->rank == root) {
     m.flag_slot = dcdg::kSlotSymbols;
@@ -1665,12 +1675,22 @@ int dcdg_dl_precode_xchg(dcdg_ctx* ctx, dcdg_xwin* w, int root, const void* H, c
     CUDA_TRY(cudaGetLastError(), "xchg_symbols_push launch");
   }
   // 2. every rank: wait for the symbols, precode from its own window
-  dcdg::xchg_wait_kernel<<<1, 32, 0, st>>>(w->base, dcdg::kSlotSymbols, 1, m.epoch, w->timeout_ns, ctx->d_status);
+  dcdg::xchg_wait_kernel<<<1, 32, 0, st>>>(w->base, dcdg::kSlotSymbols, 1, w->d_epoch, w->timeout_ns, ctx->d_status);
   ++ctx->launches;
   CUDA_TRY(cudaGetLastError(), "xchg_wait launch");
-  const void* Sy = w->base + dcdg::kXchgFlagBytes + m.parity * w->buf_bytes;
-  if (int rc = ensure_scratch(ctx, static_cast<size_t>(P) * sizeof(float))) return rc;
+  const size_t gp_bytes = (static_cast<size_t>(P) * sizeof(float) + 255) & ~size_t(255);
+  const size_t sy_bytes = (static_cast<size_t>(sbytes) + 15) & ~size_t(15);
+  if (int rc = ensure_scratch(ctx, gp_bytes + sy_bytes)) return rc;
   float* gp = static_cast<float*>(ctx->scratch);
+  void* Sy = static_cast<unsigned char*>(ctx->scratch) + gp_bytes;
+  {
+    const long long n16 = static_cast<long long>(sy_bytes / 16);
+    const int blocks = static_cast<int>(std::max(1LL, std::min<long long>((n16 + threads - 1) / threads, 4LL * ctx->sms)));
+    dcdg::xchg_symbols_fetch_kernel<<<blocks, threads, 0, st>>>(w->base, w->d_epoch, w->buf_bytes, n16,
+                                                                  static_cast<uint4*>(Sy));
+    ++ctx->launches;
+    CUDA_TRY(cudaGetLastError(), "xchg_symbols_fetch launch");
+  }
   if (int rc = dcdg_dl_precode(ctx, H, Sy, S, C, C_total, Bc, U, K, rho, fmt, x_dl, gp, nullptr, stream)) return rc;
   // 3. gain shares into every window, then the ascending-cluster effective gain.
   //    (Always run: the gain exchange is also the acknowledgement that lets the
@@ -1685,7 +1705,7 @@ int dcdg_dl_precode_xchg(dcdg_ctx* ctx, dcdg_xwin* w, int root, const void* H, c
   }
   const int gblocks = gain ? std::max(1, std::min((S + threads - 1) / threads, 2 * ctx->sms)) : 1;
 #define XGAIN(T)                                                                                                \
-  dcdg::xchg_gain_fuse_kernel<T><<<gblocks, threads, 0, st>>>(w->base, m.epoch, w->world, m.parity, w->buf_bytes, \
+  dcdg::xchg_gain_fuse_kernel<T><<<gblocks, threads, 0, st>>>(w->base, w->d_epoch, w->world, w->buf_bytes,      \
                                                               gain_off, S, C_total, U, w->timeout_ns, gain,      \
                                                               ctx->d_status)
   if (fmt == DCDG_FP16)

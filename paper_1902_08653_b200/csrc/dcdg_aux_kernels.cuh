@@ -923,19 +923,20 @@ __global__ void fuse_kernel(const T* __restrict__ XL, const float* __restrict__ 
 template <typename T>
 __global__ void xchg_put_kernel(const T* __restrict__ XL, const float* __restrict__ sigma2, long long P, XMap m) {
   const long long n = P * m.U;
+  const int parity = static_cast<int>(xchg_epoch(m) & 1);
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n + (sigma2 ? P : 0);
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     if (i < n) {
       const long long p = i / m.U;
       const int u = static_cast<int>(i - p * m.U);
-      reinterpret_cast<T*>(xchg_x_dst(m, static_cast<int>(p)))[u] = XL[i];
+      reinterpret_cast<T*>(xchg_x_dst(m, static_cast<int>(p), parity))[u] = XL[i];
     } else {
       const long long p = i - n;
       const long long s = p / m.C_local;
       const int c = static_cast<int>(p - s * m.C_local);
       const int owner = static_cast<int>(s / m.S_own);
       const long long s_in = s - static_cast<long long>(owner) * m.S_own;
-      float* dst = reinterpret_cast<float*>(m.win[owner] + kXchgFlagBytes + m.parity * m.buf_bytes + m.sig_off);
+      float* dst = reinterpret_cast<float*>(m.win[owner] + kXchgFlagBytes + parity * m.buf_bytes + m.sig_off);
       dst[s_in * m.C_total + m.c0 + c] = sigma2[p];
     }
   }
@@ -946,12 +947,14 @@ __device__ __forceinline__ float2 ldcg_c(const float2* p, size_t i) { return __l
 __device__ __forceinline__ float2 ldcg_c(const __half2* p, size_t i) { return __half22float2(__ldcg(p + i)); }
 
 template <typename T>
-__global__ void xchg_fuse_kernel(const unsigned char* __restrict__ win, unsigned long long epoch, int world,
-                                 int parity, long long buf_bytes, long long sig_off, int S_own, int C_total, int U,
+__global__ void xchg_fuse_kernel(const unsigned char* __restrict__ win, const unsigned long long* __restrict__ epoch_dev,
+                                 int world, long long buf_bytes, long long sig_off, int S_own, int C_total, int U,
                                  bool optimal, long long timeout_ns, float2* __restrict__ xhat,
                                  unsigned long long* __restrict__ status) {
   // one system-scope acquire per block; the grid is sized to the SMs and
   // strides over the (subcarrier, user) outputs
+  const unsigned long long epoch = xchg_epoch(epoch_dev);
+  const int parity = static_cast<int>(epoch & 1);
   if (!xchg_block_wait(win, 0, world, epoch, timeout_ns, status)) return;
   const unsigned char* buf = win + kXchgFlagBytes + parity * buf_bytes;
   const T* XL = reinterpret_cast<const T*>(buf);
@@ -996,30 +999,49 @@ __global__ void xchg_fuse_kernel(const unsigned char* __restrict__ win, unsigned
 // its symbols from its own window after xchg_wait_kernel.
 template <typename T>
 __global__ void xchg_symbols_push_kernel(const T* __restrict__ s, long long n, XMap m) {
+  const int parity = static_cast<int>(xchg_epoch(m) & 1);
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const T v = s[i];
     for (int q = 0; q < m.world; ++q)
-      reinterpret_cast<T*>(m.win[q] + kXchgFlagBytes + m.parity * m.buf_bytes)[i] = v;
+      reinterpret_cast<T*>(m.win[q] + kXchgFlagBytes + parity * m.buf_bytes)[i] = v;
   }
   xchg_cta_done(m);
 }
 
-__global__ void xchg_wait_kernel(const unsigned char* __restrict__ win, int slot0, int n, unsigned long long epoch,
-                                 long long timeout_ns, unsigned long long* __restrict__ status) {
-  xchg_block_wait(win, slot0, n, epoch, timeout_ns, status);
+__global__ void xchg_wait_kernel(const unsigned char* __restrict__ win, int slot0, int n,
+                                 const unsigned long long* __restrict__ epoch_dev, long long timeout_ns,
+                                 unsigned long long* __restrict__ status) {
+  xchg_block_wait(win, slot0, n, xchg_epoch(epoch_dev), timeout_ns, status);
+}
+
+// Each call advances the window's batch epoch on the device before its
+// kernels read it (one sequence for both directions).
+__global__ void xchg_advance_kernel(unsigned long long* __restrict__ epoch_dev) { *epoch_dev += 1ull; }
+
+// The symbols of this call's parity buffer, copied out of the window for the
+// precoder (whose input pointer cannot depend on a device-side epoch).
+__global__ void xchg_symbols_fetch_kernel(const unsigned char* __restrict__ win,
+                                          const unsigned long long* __restrict__ epoch_dev, long long buf_bytes,
+                                          long long n16, uint4* __restrict__ dst) {
+  const int parity = static_cast<int>(xchg_epoch(epoch_dev) & 1);
+  const uint4* src = reinterpret_cast<const uint4*>(win + kXchgFlagBytes + parity * buf_bytes);
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = __ldcg(src + i);
 }
 
 // Every rank's per-cluster gain shares Re(s^H H_dl,c x_c) gathered into every
 // window as [S][C_total] (kSlotGain + rank published when done).
 __global__ void xchg_gain_put_kernel(const float* __restrict__ gain_part, long long P, XMap m) {
+  const int parity = static_cast<int>(xchg_epoch(m) & 1);
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < P;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long s = i / m.C_local;
     const int c = static_cast<int>(i - s * m.C_local);
     const float v = gain_part[i];
     for (int q = 0; q < m.world; ++q)
-      reinterpret_cast<float*>(m.win[q] + kXchgFlagBytes + m.parity * m.buf_bytes + m.sig_off)[s * m.C_total + m.c0 + c] = v;
+      reinterpret_cast<float*>(m.win[q] + kXchgFlagBytes + parity * m.buf_bytes + m.sig_off)[s * m.C_total + m.c0 + c] = v;
   }
   xchg_cta_done(m);
 }
@@ -1028,10 +1050,13 @@ __global__ void xchg_gain_put_kernel(const float* __restrict__ gain_part, long l
 // (precode.cpp:123-131) with gain_reduce_kernel's arithmetic over all C_total
 // clusters in ascending order: bitwise the single-GPU gain.
 template <typename T>
-__global__ void xchg_gain_fuse_kernel(const unsigned char* __restrict__ win, unsigned long long epoch, int world,
-                                      int parity, long long buf_bytes, long long gain_off, int S, int C_total, int U,
+__global__ void xchg_gain_fuse_kernel(const unsigned char* __restrict__ win,
+                                      const unsigned long long* __restrict__ epoch_dev, int world,
+                                      long long buf_bytes, long long gain_off, int S, int C_total, int U,
                                       long long timeout_ns, float* __restrict__ gain,
                                       unsigned long long* __restrict__ status) {
+  const unsigned long long epoch = xchg_epoch(epoch_dev);
+  const int parity = static_cast<int>(epoch & 1);
   if (!xchg_block_wait(win, kSlotGain, world, epoch, timeout_ns, status)) return;
   if (!gain) return;
   const unsigned char* buf = win + kXchgFlagBytes + parity * buf_bytes;

@@ -231,7 +231,8 @@ constexpr int kSlotGain = 16;
 struct XMap {
   unsigned char* win[kXchgMaxRanks];  // every rank's window base (self included), in this process's address space
   unsigned int* counter;              // local CTA-completion counter (reset by the last CTA)
-  unsigned long long epoch;           // batch epoch written to the owners' flags
+  const unsigned long long* epoch_dev;  // this call's batch epoch, in device memory (xchg_advance_kernel):
+                                       // read by the kernels, so a captured call replays with fresh epochs
   int flag_slot;                      // xchg_cta_done publishes to slot flag_slot (+ rank if per_rank)
   int per_rank;
   long long buf_bytes;                // bytes of one parity buffer
@@ -240,17 +241,21 @@ struct XMap {
   int S_own;                          // subcarriers owned per rank
   int C_local, c0, C_total, U;
   int esz;                            // bytes per complex of x (8 fp32, 4 fp16)
-  int parity;
 };
+
+// The call's batch epoch (written by the previous kernel on the stream) and
+// its parity buffer.
+__device__ __forceinline__ unsigned long long xchg_epoch(const unsigned long long* e) { return __ldcg(e); }
+__device__ __forceinline__ unsigned long long xchg_epoch(const XMap& m) { return xchg_epoch(m.epoch_dev); }
 
 // Destination of problem p's estimate (p = s*C_local + c, s global over the batch).
 // (P = S*C_local < 2^31 is checked on the host: 32-bit index math.)
-__device__ __forceinline__ unsigned char* xchg_x_dst(const XMap& m, int p) {
+__device__ __forceinline__ unsigned char* xchg_x_dst(const XMap& m, int p, int parity) {
   const int s = p / m.C_local;
   const int c = p - s * m.C_local;
   const int owner = s / m.S_own;
   const int s_in = s - owner * m.S_own;
-  return m.win[owner] + kXchgFlagBytes + m.parity * m.buf_bytes +
+  return m.win[owner] + kXchgFlagBytes + parity * m.buf_bytes +
          static_cast<long long>((s_in * m.C_total + m.c0 + c) * m.U) * m.esz;
 }
 
@@ -305,8 +310,9 @@ __device__ __forceinline__ void xchg_cta_done(const XMap& m) {
     if (t == gridDim.x - 1) {
       __threadfence_system();
       const int slot = m.flag_slot + (m.per_rank ? m.rank : 0);
+      const unsigned long long e = xchg_epoch(m);
       for (int q = 0; q < m.world; ++q)
-        st_release_sys(reinterpret_cast<unsigned long long*>(m.win[q]) + slot, m.epoch);
+        st_release_sys(reinterpret_cast<unsigned long long*>(m.win[q]) + slot, e);
       *m.counter = 0u;  // next launch on this stream starts from zero
     }
   }

@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
     const int p = set * NPW + g;
     if (p < P) {
       // XCHG: straight into the owning GPU's exchange window (peer memory)
-      float4* xo = XCHG ? reinterpret_cast<float4*>(xchg_x_dst(xm, p))
+      float4* xo = XCHG ? reinterpret_cast<float4*>(xchg_x_dst(xm, p, static_cast<int>(xchg_epoch(xm) & 1)))
                         : reinterpret_cast<float4*>(X + static_cast<size_t>(p) * U);
 #pragma unroll
       for (int i = k; i < U / 2; i += G) {
@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
     __syncwarp();
     const int p = set * NPW + g;
     if (p < P) {
-      uint4* xo = XCHG ? reinterpret_cast<uint4*>(xchg_x_dst(xm, p))
+      uint4* xo = XCHG ? reinterpret_cast<uint4*>(xchg_x_dst(xm, p, static_cast<int>(xchg_epoch(xm) & 1)))
                        : reinterpret_cast<uint4*>(X + static_cast<size_t>(p) * U);
 #pragma unroll
       for (int i = k; i < U / 4; i += G) {

@@ -55,6 +55,43 @@ def test_single_rank_window_is_bitwise_single_gpu(engine, port, shape, fmt, fusi
     w.close()
 
 
+@pytest.mark.parametrize("fusion", ["uniform", "optimal"])
+def test_exchange_calls_replay_from_a_cuda_graph(engine, fusion):
+    """The batch epochs advance on the device, so exchange calls captured once
+    into a CUDA graph (uplink, downlink, uplink: both parities, both
+    directions) replay with fresh epochs: every replay bitwise the eager
+    single-GPU results."""
+    from helpers import qam_symbols
+    from paper_1902_08653_b200 import ExchangeWindow
+    C, BC, U, S = 8, 32, 16, 64
+    b = batch(C, BC, U, 16, S, seed=13)
+    H, y = to_dev(b["h_tiles"]), to_dev(b["y"])
+    sym = to_dev(qam_symbols(S, U))
+    want_ul = _single(engine, H, y, fusion=fusion, n0=b["n0"])
+    want_dl = engine.dl_precode(H, sym, rho=4.0, K=3, want_gain=True)
+    engine.sync()
+    w = ExchangeWindow(engine, 1, 0, S=S, C_total=C, U=U, fmt="fp32")
+    # warm up eagerly (scratch allocation, kernel attributes), then capture
+    w.ul_detect(H, y, c0=0, C_total=C, n0=b["n0"], K=3, fusion=fusion)
+    w.dl_precode(H, sym, root=0, c0=0, C_total=C, rho=4.0, K=3)
+    engine.sync()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        u1 = w.ul_detect(H, y, c0=0, C_total=C, n0=b["n0"], K=3, fusion=fusion)
+        x, gain = w.dl_precode(H, sym, root=0, c0=0, C_total=C, rho=4.0, K=3)
+        u2 = w.ul_detect(H, y, c0=0, C_total=C, n0=b["n0"], K=3, fusion=fusion)
+    for _ in range(3):
+        for t in (u1, u2, x, gain):
+            t.zero_()
+        g.replay()
+        engine.sync()
+        assert torch.equal(torch.view_as_real(u1), torch.view_as_real(want_ul))
+        assert torch.equal(torch.view_as_real(u2), torch.view_as_real(want_ul))
+        assert torch.equal(x.view(torch.float32), want_dl.x.view(torch.float32))
+        assert torch.equal(gain, want_dl.gain)
+    w.close()
+
+
 @pytest.mark.parametrize("shape,fmt", [((8, 32, 16), "fp32"), ((8, 32, 16), "fp16"), ((2, 64, 8), "fp32"),
                                        ((3, 24, 6), "fp32")])
 def test_single_rank_downlink_window_is_bitwise_single_gpu(engine, port, shape, fmt):
