@@ -143,6 +143,14 @@ struct Layout {
   void close_inputs() { in_end = end; }
 };
 
+// DCDG_CPP_ZERO_COPY (default): the kernels read the packed inputs and write
+// the results straight in the pinned staging (UVA-mapped host memory; the
+// bulk copies and loads cross PCIe as they run), so a call is its kernels and
+// one synchronisation, no separate H2D/D2H copies (per-call latency 42 -> see
+// DESIGN.md §1).  0: device scratch with one H2D and one D2H copy per call.
+#ifndef DCDG_CPP_ZERO_COPY
+#define DCDG_CPP_ZERO_COPY 1
+#endif
 struct Call {
   Engine& eng;
   unsigned char* host;
@@ -150,13 +158,17 @@ struct Call {
   Call(Engine& e, const Layout& l)
       : eng(e),
         host(static_cast<unsigned char*>(e.host_staging(l.end))),
-        dev(static_cast<unsigned char*>(e.device_scratch(l.end))) {}
+        dev(DCDG_CPP_ZERO_COPY ? host : static_cast<unsigned char*>(e.device_scratch(l.end))) {}
   template <class T = unsigned char>
   T* h(std::size_t off) const { return reinterpret_cast<T*>(host + off); }
   template <class T = unsigned char>
   T* d(std::size_t off) const { return reinterpret_cast<T*>(dev + off); }
-  void upload(const Layout& l) const { h2d(dev, host, l.in_end, eng.stream()); }
-  void download(const Layout& l) const { d2h(host + l.in_end, dev + l.in_end, l.end - l.in_end, eng.stream()); }
+  void upload(const Layout& l) const {
+    if (dev != host) h2d(dev, host, l.in_end, eng.stream());
+  }
+  void download(const Layout& l) const {
+    if (dev != host) d2h(host + l.in_end, dev + l.in_end, l.end - l.in_end, eng.stream());
+  }
 };
 
 // Graph-cache key of one call (Engine::run): the bytes of every value that
