@@ -140,7 +140,7 @@ int main(int argc, char** argv) {
       "\"decentralized_cd_precode\": %.2f, \"calls\": %d, \"stat\": \"median, warm thread-local Engine\"}, "
       "\"batched_round\": {\"subcarriers\": %d, \"detect_ms\": %.3f, \"detect_us_per_subcarrier\": %.3f, "
       "\"detect_Gbps\": %.4f, \"precode_ms\": %.3f, \"precode_us_per_subcarrier\": %.3f, \"precode_Gbps\": %.4f, "
-      "\"note\": \"host fp64 in/out: packing, one H2D, kernels, one D2H, unpacking\"}, "
+      "\"note\": \"host fp64 in/out: packing, kernels on the pinned staging (zero-copy), unpacking\"}, "
       "\"reference_us_per_call_1thread\": %.2f}\n",
       ul_us, ul_opt_us, dl_us, calls, S_round, ul_batch_us / 1e3, ul_batch_us / S_round,
       S_round * U * BITS / (ul_batch_us * 1e-6) / 1e9, dl_batch_us / 1e3, dl_batch_us / S_round,
