@@ -839,12 +839,22 @@ int dcdg_sync_status(dcdg_ctx* ctx, void* stream) {
   return dcdg_status_decode(ctx, key);
 }
 
+#ifndef DCDG_STATUS_KERNEL
+#define DCDG_STATUS_KERNEL 1
+#endif
 int dcdg_status_enqueue(dcdg_ctx* ctx, unsigned long long* host_word, void* stream) {
   if (int rc = check_ctx(ctx)) return rc;
   if (!host_word) return fail(DCDG_EINVAL, "dcdg_status_enqueue: null host word");
+#if DCDG_STATUS_KERNEL
+  // a one-thread kernel stores the word into the (pinned, UVA-mapped) host
+  // word: one kernel node instead of a copy node in the caller's stream/graph
+  dcdg::status_mirror_kernel<<<1, 1, 0, as_stream(stream)>>>(ctx->d_status, host_word);
+  CUDA_TRY(cudaGetLastError(), "status mirror launch");
+#else
   CUDA_TRY(cudaMemcpyAsync(host_word, ctx->d_status, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            as_stream(stream)),
            "status copy");
+#endif
   return DCDG_OK;
 }
 

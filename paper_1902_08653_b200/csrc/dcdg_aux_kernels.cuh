@@ -1075,6 +1075,11 @@ __global__ void xchg_gain_fuse_kernel(const unsigned char* __restrict__ win,
   }
 }
 
+// dcdg_status_enqueue: the device status word into pinned host memory
+__global__ void status_mirror_kernel(const unsigned long long* __restrict__ st, unsigned long long* host_word) {
+  *reinterpret_cast<volatile unsigned long long*>(host_word) = *st;
+}
+
 __global__ void fuse_finalize_kernel(float2* __restrict__ xhat, const float* __restrict__ wsum, int S, int U) {
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= static_cast<long long>(S) * U) return;
