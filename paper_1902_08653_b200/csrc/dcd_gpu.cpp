@@ -15,6 +15,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 
@@ -171,6 +172,23 @@ struct Call {
   }
 };
 
+// Host-side packing / unpacking of a batched call over the subcarriers: on
+// several threads for large batches (the fp64 <-> fp32 conversion of a
+// 16 800-subcarrier round is ~1.2 GB of host memory traffic).
+template <class F>
+void for_subcarriers(std::size_t S, F&& fn) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const std::size_t nt = std::min<std::size_t>(hw, S / 256);
+  if (nt <= 1) {
+    fn(std::size_t{0}, S);
+    return;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(nt);
+  for (std::size_t t = 0; t < nt; ++t) pool.emplace_back([&, t] { fn(S * t / nt, S * (t + 1) / nt); });
+  for (auto& th : pool) th.join();
+}
+
 // Graph-cache key of one call (Engine::run): the bytes of every value that
 // shapes its stream work (sizes, scalars, buffer addresses).
 struct Key {
@@ -280,12 +298,14 @@ std::vector<DetectionResult> detect_impl(std::span<const ClusterSpan> subs, std:
   const std::size_t oXL = L.take(S * nc * u * es), oS2 = L.take(optimal ? S * nc * sizeof(float) : 0),
                     oXH = L.take(S * u * 8), oW = L.take(optimal ? S * nc * sizeof(float) : 0);
   Call k(eng, L);
-  for (std::size_t s = 0; s < S; ++s)
-    for (std::size_t c = 0; c < nc; ++c) {
-      const auto& cl = subs[s][c];
-      pack_tile(cl.h.flat().data(), cl.h.rows(), u, dp.fmt, k.h(oH + s * hsub + hoff[c]));
-      pack_tile(cl.y.data(), cl.y.size(), 1, dp.fmt, k.h(oY + s * ysub + yoff[c]));
-    }
+  for_subcarriers(S, [&](std::size_t s0, std::size_t s1) {
+    for (std::size_t s = s0; s < s1; ++s)
+      for (std::size_t c = 0; c < nc; ++c) {
+        const auto& cl = subs[s][c];
+        pack_tile(cl.h.flat().data(), cl.h.rows(), u, dp.fmt, k.h(oH + s * hsub + hoff[c]));
+        pack_tile(cl.y.data(), cl.y.size(), 1, dp.fmt, k.h(oY + s * ysub + yoff[c]));
+      }
+  });
   const int fusion = optimal ? DCDG_FUSION_OPTIMAL : DCDG_FUSION_UNIFORM;
   const int ui = static_cast<int>(u), K = static_cast<int>(cfg.t_max), nci = static_cast<int>(nc);
   const int Si = static_cast<int>(S);
@@ -319,7 +339,8 @@ std::vector<DetectionResult> detect_impl(std::span<const ClusterSpan> subs, std:
   });
 
   std::vector<DetectionResult> out(S);
-  for (std::size_t s = 0; s < S; ++s) {
+  for_subcarriers(S, [&](std::size_t s0, std::size_t s1) {
+  for (std::size_t s = s0; s < s1; ++s) {
     DetectionResult& res = out[s];
     res.local.resize(nc);
     for (std::size_t c = 0; c < nc; ++c) {
@@ -338,6 +359,7 @@ std::vector<DetectionResult> detect_impl(std::span<const ClusterSpan> subs, std:
       res.weights.assign(nc, 1.0 / static_cast<double>(nc));  // detect.cpp:181
     }
   }
+  });
   return out;
 }
 
@@ -366,16 +388,18 @@ std::vector<PrecodeResult> precode_impl(std::span<const BlockSpan> blocks,
   L.close_inputs();
   const std::size_t oX = L.take(S * xsub), oGP = L.take(S * nc * sizeof(float)), oG = L.take(S * sizeof(float));
   Call k(eng, L);
-  std::vector<cf64> tile;
-  for (std::size_t s = 0; s < S; ++s) {
-    for (std::size_t c = 0; c < nc; ++c) {
-      tile.resize(blocks[s][c].cols() * u);
-      uplink_tile_of(blocks[s][c], tile.data());
-      pack_tile(tile.data(), blocks[s][c].cols(), u, dp.fmt, k.h(oH + s * hsub + hoff[c]));
+  for_subcarriers(S, [&](std::size_t s0, std::size_t s1) {
+    std::vector<cf64> tile;
+    for (std::size_t s = s0; s < s1; ++s) {
+      for (std::size_t c = 0; c < nc; ++c) {
+        tile.resize(blocks[s][c].cols() * u);
+        uplink_tile_of(blocks[s][c], tile.data());
+        pack_tile(tile.data(), blocks[s][c].cols(), u, dp.fmt, k.h(oH + s * hsub + hoff[c]));
+      }
+      pack(syms[s].data(), u, dp.fmt, k.h(oS + s * u * es));
+      if (dp.round_messages) pack(syms[s].data(), u, dp.fmt, k.h(oSw + s * u * es));
     }
-    pack(syms[s].data(), u, dp.fmt, k.h(oS + s * u * es));
-    if (dp.round_messages) pack(syms[s].data(), u, dp.fmt, k.h(oSw + s * u * es));
-  }
+  });
   Key key;
   key << 'D' << S << nc << u << cfg.t_max << cfg.rho << dp.fmt << dp.round_messages << uniform << k.host << k.dev
       << L.end;
@@ -415,17 +439,19 @@ std::vector<PrecodeResult> precode_impl(std::span<const BlockSpan> blocks,
   });
 
   std::vector<PrecodeResult> out(S);
-  for (std::size_t s = 0; s < S; ++s) {
-    PrecodeResult& res = out[s];
-    res.blocks.resize(nc);
-    res.x.reserve(btot);
-    for (std::size_t c = 0; c < nc; ++c) {
-      res.blocks[c].resize(blocks[s][c].cols());
-      unpack(k.h(oX + s * xsub + xoff[c]), res.blocks[c].size(), dp.fmt, res.blocks[c].data());
-      res.x.insert(res.x.end(), res.blocks[c].begin(), res.blocks[c].end());
+  for_subcarriers(S, [&](std::size_t s0, std::size_t s1) {
+    for (std::size_t s = s0; s < s1; ++s) {
+      PrecodeResult& res = out[s];
+      res.blocks.resize(nc);
+      res.x.reserve(btot);
+      for (std::size_t c = 0; c < nc; ++c) {
+        res.blocks[c].resize(blocks[s][c].cols());
+        unpack(k.h(oX + s * xsub + xoff[c]), res.blocks[c].size(), dp.fmt, res.blocks[c].data());
+        res.x.insert(res.x.end(), res.blocks[c].begin(), res.blocks[c].end());
+      }
+      res.effective_gain = k.h<float>(oG)[s];
     }
-    res.effective_gain = k.h<float>(oG)[s];
-  }
+  });
   return out;
 }
 
