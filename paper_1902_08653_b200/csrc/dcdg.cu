@@ -288,13 +288,18 @@ cudaError_t launch_ul_f16(dcdg_ctx* ctx, const void* H, const void* Y, int P, in
   return cudaGetLastError();
 }
 
+// lab: the effective-gain instantiation of the downlink kernel may run with
+// fewer resident warps per SM (more registers for v = H_c s)
+#ifndef DCDG_DL_GAIN_MINB_DELTA
+#define DCDG_DL_GAIN_MINB_DELTA 0
+#endif
 template <int BC, int U, int G, int MINB, bool GAIN>
 cudaError_t launch_dl_f32_k(dcdg_ctx* ctx, const void* H, const void* S, int P, int C, int K, float rho_c, void* X,
                             float* gp, cudaStream_t st) {
   constexpr int NPW = 32 / G;
   constexpr size_t smem =
       dcdg::CtaSmem<NPW*(BC * U * 8 + U * 8), dcdg::dl_scal_bytes(U), NPW, kWarps>::kBytes;
-  auto kern = dcdg::dl_reg_f32<BC, U, G, kWarps, MINB, GAIN>;
+  auto kern = dcdg::dl_reg_f32<BC, U, G, kWarps, (GAIN ? MINB - DCDG_DL_GAIN_MINB_DELTA : MINB), GAIN>;
   const int occ = occupancy_of(ctx, kern, smem);
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);

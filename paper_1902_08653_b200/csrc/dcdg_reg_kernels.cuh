@@ -53,6 +53,7 @@ namespace dcdg {
 #define DCDG_SIG_CPAIRS 1
 #endif
 // downlink GAIN: v = H_c s before the sweeps (1) or after them (0)
+// (2: inside the last sweep, pair by pair, under a warp-uniform branch)
 #ifndef DCDG_DL_GAIN_EARLY
 #define DCDG_DL_GAIN_EARLY 0
 #endif
@@ -804,7 +805,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
     __syncwarp();
 
     float2 vr[NP], vi[NP];  // GAIN: v = H_c s = sum_u s_u h_u (the effective-gain share's left vector)
-#if DCDG_DL_GAIN_EARLY
+#if DCDG_DL_GAIN_EARLY == 1
     // accumulated before the sweeps, independent of their dependency chain
     if (GAIN) {
 #pragma unroll
@@ -823,6 +824,12 @@ __global__ void __launch_bounds__(32 * W, MINB)
     float2 xr[NP], xi[NP];
 #pragma unroll
     for (int c = 0; c < NP; ++c) xr[c] = xi[c] = z2;
+#if DCDG_DL_GAIN_EARLY == 2
+    if (GAIN) {
+#pragma unroll
+      for (int c = 0; c < NP; ++c) vr[c] = vi[c] = z2;
+    }
+#endif
     for (int t = 0; t < K; ++t) {
 #pragma unroll
       for (int jp = 0; jp < U / 2; ++jp) {
@@ -836,6 +843,18 @@ __global__ void __launch_bounds__(32 * W, MINB)
           a1 = ffma2(hi[j1][c], xi[c], ffma2(hr[j1][c], xr[c], a1));
           c1 = ffma2(neg2(hi[j1][c]), xr[c], ffma2(hr[j1][c], xi[c], c1));
         }
+#if DCDG_DL_GAIN_EARLY == 2
+        if (GAIN && t == K - 1) {
+          const float4 s01 = reinterpret_cast<const float4*>(sraw)[jp];
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            vr[c] = ffma2(-s01.y, hi[j0][c], ffma2(s01.x, hr[j0][c], vr[c]));
+            vi[c] = ffma2(s01.y, hr[j0][c], ffma2(s01.x, hi[j0][c], vi[c]));
+            vr[c] = ffma2(-s01.w, hi[j1][c], ffma2(s01.z, hr[j1][c], vr[c]));
+            vi[c] = ffma2(s01.w, hr[j1][c], ffma2(s01.z, hi[j1][c], vi[c]));
+          }
+        }
+#endif
         float2 d0 = make_float2(hsum(a0), hsum(c0));
         float2 d1 = make_float2(hsum(a1), hsum(c1));
         if constexpr (4 <= G && G >= DCDG_SCATTER_MIN_G_DL) {
@@ -882,7 +901,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
     // gain share Re(s^H H_dl,c x_c) = Re(v^H x_c), v = H_c s = sum_u s_u h_u
     float gq = 0.f;
     if (GAIN) {
-#if !DCDG_DL_GAIN_EARLY
+#if DCDG_DL_GAIN_EARLY == 0
 #pragma unroll
       for (int c = 0; c < NP; ++c) vr[c] = vi[c] = z2;
 #pragma unroll

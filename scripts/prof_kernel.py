@@ -1,5 +1,5 @@
 """Launch one CD-path kernel a few times for an ncu capture.
-usage: python scripts/prof_kernel.py [ul|opt|dl|pev] [fp32|fp16] [reps] [S] [C B_c U]
+usage: python scripts/prof_kernel.py [ul|opt|dl|dlg|pev] [fp32|fp16] [reps] [S] [C B_c U]
 Default shape: the north star (C=8, B_c=32, U=16, S=16800 -> 134 400 problems);
 other shapes are synthesised on the device (dcdg_synth)."""
 import math
@@ -34,6 +34,8 @@ for _ in range(reps):
         eng.ul_detect(H, y, n0=n0, K=3, fusion="optimal", want_xhat=False)
     elif direction == "pev":
         eng.post_eq_variance(H, n0=n0)
+    elif direction == "dlg":  # downlink with the effective-gain share
+        eng.dl_precode(H, x, rho=math.sqrt(U), K=3, want_gain=True)
     else:
         eng.dl_precode(H, x, rho=math.sqrt(U), K=3, want_gain=False)
 eng.sync()
