@@ -478,7 +478,7 @@ constexpr int minb_mw(int warps, int nw) { return warps / nw > 0 ? warps / nw : 
 const Spec kSpecs[] = {
     {32, 16, DCDG_FP32, UL_REG(32, 16, 8), DL_REG(32, 16, 8)},  // north-star target: B=256, C=8, U=16
     {32, 8, DCDG_FP32, UL_REG(32, 8, DCDG_G_32x8), DL_REG(32, 8, DCDG_G_32x8)},  // paper / config 1: B_c=32, U=8
-    {16, 16, DCDG_FP32, UL_REG(16, 16, 4), DL_REG(16, 16, DCDG_G_16x16_DL)},  // B=128, C=8
+    {16, 16, DCDG_FP32, UL_REG(16, 16, DCDG_G_16x16_UL), DL_REG(16, 16, DCDG_G_16x16_DL)},  // B=128, C=8
     {64, 16, DCDG_FP32, UL_REG(64, 16, 16), DL_REG(64, 16, 16)},  // B=256, C=4 / B=512, C=8
     {64, 8, DCDG_FP32, UL_REG(64, 8, 8), DL_REG(64, 8, 8)},
     {128, 16, DCDG_FP32, UL_SPLIT(128, 16, 16, 8), DL_REG(128, 16, 32)},  // B=128,C=1 / 256,2 / 512,4
