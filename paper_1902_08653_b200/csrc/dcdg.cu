@@ -460,6 +460,10 @@ struct Spec {
 #ifndef DCDG_G_16x16_DL
 #define DCDG_G_16x16_DL 4
 #endif
+// lanes per problem of the 16x16 uplink tile
+#ifndef DCDG_G_16x16_UL
+#define DCDG_G_16x16_UL 4
+#endif
 constexpr int minb(int warps) { return warps / kWarps > 0 ? warps / kWarps : 1; }
 constexpr int minb_mw(int warps, int nw) { return warps / nw > 0 ? warps / nw : 1; }
 
