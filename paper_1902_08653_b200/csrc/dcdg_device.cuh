@@ -630,4 +630,92 @@ __device__ __forceinline__ float gram_trace_inverse_cpairs2(float2 (&R0r)[U / 2]
   return t;
 }
 
+// Which factorisation the variance kernels run: 1 = forward elimination on
+// column pairs (gram_trace_inverse_cols below), 0 = the sweep operators above.
+#ifndef DCDG_SIG_COLS
+#define DCDG_SIG_COLS 1
+#endif
+
+// post_eq_variance (detect.cpp:112-130) by forward elimination of [A | I]
+// held as COLUMN PAIRS: lane k of the problem's U/2 lanes keeps columns 2k,
+// 2k+1 of A = I + gam G for every row i as Cr[i] = (Re A[i][2k], Re A[i][2k+1]),
+// Ci[i] likewise.  Pivot kk (ascending, as hermitian_solve's Cholesky,
+// numerics.cpp:51-66) updates only the rows below it,
+//     a_ij -= f_i a_kk,j   (i > kk, every column j),   f_i = a_i,kk / d_kk,
+// and the in-place column kk of those rows becomes -f_i.  Stored in place the
+// right half of [A | I] fills exactly the columns the left half vacates, so
+// at the end row i holds M = L^-1 (unit lower, A = L D L^H) left of the
+// diagonal and d_i on it, and
+//     tr A^-1 = sum_i (1 + sum_{j<i} |M_ij|^2) / d_i.
+// The pivots d_kk are the Schur complements the reference's Cholesky checks
+// against 1e-14 max_i A_ii.  Each lane's rows below kk are lane-uniform, so a
+// pivot costs 4 FFMA2 per row below it (480 per lane at U = 16, against 1024
+// for the in-place sweep operator), and only pivot COLUMN kk is broadcast
+// (`prow`: 2 x U float2 per problem, alternating by pivot parity) -- the pivot
+// row of a lane's columns is its own register.  Returns tr A^-1 on every lane
+// of the problem.
+template <int U>
+__device__ __forceinline__ float gram_trace_inverse_cols(float2 (&Cr)[U], float2 (&Ci)[U], int k, float4* prow,
+                                                         bool& singular) {
+  constexpr int NQ = U / 2;
+  float dmax = 0.f;
+#pragma unroll
+  for (int jq = 0; jq < NQ; ++jq)
+    if (k == jq) dmax = fmaxf(Cr[2 * jq].x, Cr[2 * jq + 1].y);
+#pragma unroll
+  for (int o = U / 4; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  const float floor_ = 1e-14f * dmax;
+  float invd[U];
+#pragma unroll
+  for (int kk = 0; kk < U; ++kk) {
+    const int h = kk & 1, qk = kk >> 1;  // pivot column kk = half h of lane qk's pair
+    const bool own = (k == qk);
+    float2* col = reinterpret_cast<float2*>(prow) + h * U;  // (re, im) of rows kk..U-1
+    if (own) {
+      const uint32_t a = smem_u32(col);
+#pragma unroll
+      for (int i = 0; i < U; ++i)  // constant bounds: fully unrolled with the pivot loop
+        if (i >= kk)
+          asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a + 8 * i), "f"(h ? Cr[i].y : Cr[i].x),
+                       "f"(h ? Ci[i].y : Ci[i].x)
+                       : "memory");
+    }
+    __syncwarp();
+    const float d = col[kk].x;
+    if (!(d > floor_)) singular = true;
+    float inv;  // MUFU.RCP alone (<= 1 ulp): the IEEE __frcp_rn adds a Newton step and a slow-path branch to the chain
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(d));
+    invd[kk] = inv;
+    const float2 pr = Cr[kk], pi = Ci[kk];  // pivot row kk over this lane's column pair
+#pragma unroll
+    for (int i = 1; i < U; ++i) {
+      if (i <= kk) continue;
+      const float2 f = fmul2(inv, col[i]);  // f_i = a_i,kk / d
+      Cr[i] = ffma2(f.y, pi, ffma2(-f.x, pr, Cr[i]));
+      Ci[i] = ffma2(-f.y, pr, ffma2(-f.x, pi, Ci[i]));
+      if (own) {  // M_i,kk = -f_i
+        if (h) {
+          Cr[i].y = -f.x;
+          Ci[i].y = -f.y;
+        } else {
+          Cr[i].x = -f.x;
+          Ci[i].x = -f.y;
+        }
+      }
+    }
+  }
+  // (1 + sum_j |M_ij|^2) / d_i: the 1 from the lane's own diagonal rows, the
+  // |M_ij|^2 of its two columns below the diagonal
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < U; ++i) {
+    const float2 m = ffma2(Cr[i], Cr[i], fmul2(Ci[i], Ci[i]));
+    const float s = (2 * k < i ? m.x : 0.f) + (2 * k + 1 < i ? m.y : 0.f) + (2 * k == i || 2 * k + 1 == i ? 1.f : 0.f);
+    t = fmaf(s, invd[i], t);
+  }
+#pragma unroll
+  for (int o = U / 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
 }  // namespace dcdg

@@ -338,7 +338,17 @@ __global__ void __launch_bounds__(32, MINB)
       // format as the reference rounds the messages (detect.cpp:170-173)
       bool singular = false;
       float4* prow = reinterpret_cast<float4*>(sm + L::kGOff) + q * U;
-#if DCDG_GRAM_SIG_CPAIRS
+#if DCDG_SIG_COLS
+      // columns 2k, 2k+1 of the Hermitian A = I + gam G are the conjugated
+      // rows this lane holds: forward elimination (gram_trace_inverse_cols)
+      float2 Cr[U], Ci[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        Cr[i] = make_float2(fmaf(gam, g0r[i], i == 2 * k ? 1.f : 0.f), fmaf(gam, g1r[i], i == 2 * k + 1 ? 1.f : 0.f));
+        Ci[i] = make_float2(-gam * g0i[i], -gam * g1i[i]);
+      }
+      const float tr = gram_trace_inverse_cols<U>(Cr, Ci, k, prow, singular);
+#elif DCDG_GRAM_SIG_CPAIRS
       // A = I + gam G as column pairs, then the FFMA2 sweep operator (as ul_reg_f32's fused variance)
       float2 R0r[U / 2], R0i[U / 2], R1r[U / 2], R1i[U / 2];
 #pragma unroll

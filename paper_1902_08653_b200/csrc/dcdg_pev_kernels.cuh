@@ -201,6 +201,21 @@ __global__ void __launch_bounds__(32, MINB)
     }
     __syncwarp();
     // ---- factorisation: lane k of problem q takes rows 2k, 2k+1 of A
+#if DCDG_SIG_COLS
+    float2 Cr[U], Ci[U];
+    {
+      const float4* a4 = img_all + q * (L::kImgB / 16);
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const float4 a = a4[apair_slot<U>(i, k)];
+        Cr[i] = make_float2(a.x, a.y);
+        Ci[i] = make_float2(a.z, a.w);
+      }
+    }
+    bool singular = false;
+    float4* prow = prow_all + q * (L::kRowB / 16);
+    const float tr = gram_trace_inverse_cols<U>(Cr, Ci, k, prow, singular);
+#else
     float2 R0r[NQ], R0i[NQ], R1r[NQ], R1i[NQ];
     {
       const float4* a4 = img_all + q * (L::kImgB / 16);
@@ -217,6 +232,7 @@ __global__ void __launch_bounds__(32, MINB)
     float4* prow = prow_all + q * (L::kRowB / 16);
     const float tr = U <= DCDG_PEV_TC_BLOCK2_MAXU ? gram_trace_inverse_cpairs2<U>(R0r, R0i, R1r, R1i, k, prow, singular)
                                        : gram_trace_inverse_cpairs<U>(R0r, R0i, R1r, R1i, k, prow, singular);
+#endif
     const unsigned sing = __ballot_sync(0xffffffffu, singular);
     const int p = set * NPW + q;
     if (p < P && k == 0) {

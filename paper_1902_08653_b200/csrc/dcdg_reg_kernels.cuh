@@ -453,7 +453,19 @@ __global__ void __launch_bounds__(32 * W, MINB)
       __syncwarp();
       // lane k takes rows 2k, 2k+1 of A as column pairs; then the slot is free
       // for the next set's copy
-#if DCDG_SIG_CPAIRS
+#if DCDG_SIG_COLS
+      // lane k takes column pair k of every row (forward elimination)
+      float2 Cr[U], Ci[U];
+      {
+        const float4* a4 = reinterpret_cast<const float4*>(af);
+#pragma unroll
+        for (int i = 0; i < U; ++i) {
+          const float4 a = a4[apair_slot<U>(i, k)];
+          Cr[i] = make_float2(a.x, a.y);
+          Ci[i] = make_float2(a.z, a.w);
+        }
+      }
+#elif DCDG_SIG_CPAIRS
       float2 R0r[U / 2], R0i[U / 2], R1r[U / 2], R1i[U / 2];
       const float4* a4 = reinterpret_cast<const float4*>(af);
 #pragma unroll
@@ -486,7 +498,9 @@ __global__ void __launch_bounds__(32 * W, MINB)
       if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
       // the pivot rows go through the problem's scalar block (dead after the sweeps)
       bool singular = false;
-#if DCDG_SIG_CPAIRS
+#if DCDG_SIG_COLS
+      const float tr = gram_trace_inverse_cols<U>(Cr, Ci, k, mnx, singular);
+#elif DCDG_SIG_CPAIRS
       const float tr = DCDG_SIG_BLOCK2 ? gram_trace_inverse_cpairs2<U>(R0r, R0i, R1r, R1i, k, mnx, singular)
                                          : gram_trace_inverse_cpairs<U>(R0r, R0i, R1r, R1i, k, mnx, singular);
 #else
