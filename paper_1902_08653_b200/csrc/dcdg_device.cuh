@@ -635,6 +635,9 @@ __device__ __forceinline__ float gram_trace_inverse_cpairs2(float2 (&R0r)[U / 2]
 #ifndef DCDG_SIG_COLS
 #define DCDG_SIG_COLS 1
 #endif
+#ifndef DCDG_SIG_COLS_STS32
+#define DCDG_SIG_COLS_STS32 0
+#endif
 
 // post_eq_variance (detect.cpp:112-130) by forward elimination of [A | I]
 // held as COLUMN PAIRS: lane k of the problem's U/2 lanes keeps columns 2k,
@@ -675,10 +678,18 @@ __device__ __forceinline__ float gram_trace_inverse_cols(float2 (&Cr)[U], float2
       const uint32_t a = smem_u32(col);
 #pragma unroll
       for (int i = 0; i < U; ++i)  // constant bounds: fully unrolled with the pivot loop
-        if (i >= kk)
+        if (i >= kk) {
+#if DCDG_SIG_COLS_STS32
+          // two 4-B stores: re and im sit in different register pairs, a
+          // vector store would need two re-pairing moves per row
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 8 * i), "f"(h ? Cr[i].y : Cr[i].x) : "memory");
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 8 * i + 4), "f"(h ? Ci[i].y : Ci[i].x) : "memory");
+#else
           asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a + 8 * i), "f"(h ? Cr[i].y : Cr[i].x),
                        "f"(h ? Ci[i].y : Ci[i].x)
                        : "memory");
+#endif
+        }
     }
     __syncwarp();
     const float d = col[kk].x;
