@@ -25,6 +25,12 @@
 #include "dcdg_pev_kernels.cuh"
 #include "dcdg_sweep_kernels.cuh"
 #include "dcdg_reg_kernels.cuh"
+#ifndef DCDG_UL_PP2
+#define DCDG_UL_PP2 0
+#endif
+#if DCDG_UL_PP2
+#include "dcdg_pp2_kernels.cuh"
+#endif
 #include "dcdg_split_kernels.cuh"
 #include "dcdg_tmem_kernels.cuh"
 
@@ -196,6 +202,27 @@ cudaError_t launch_ul_f32(dcdg_ctx* ctx, const void* H, const void* Y, int P, in
                                                        nullptr, 0.f, 0.f, nullptr);
   return cudaGetLastError();
 }
+
+// Lab (off): two problems per 16-lane group (dcdg_pp2_kernels.cuh) for the
+// uniform-fusion uplink at the north-star tile, measured slower than
+// ul_reg_f32 (profiles/lab/README.md); the exchange instantiation keeps
+// ul_reg_f32.
+#if DCDG_UL_PP2
+template <int BC, int U, int G, int MINB>
+cudaError_t launch_ul_pp2(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                          const dcdg::XMap* xm, cudaStream_t st) {
+  if (xm) return launch_ul_f32<BC, U, G, MINB>(ctx, H, Y, P, K, kappa, X, xm, st);
+  constexpr int NPW = 4;
+  constexpr size_t smem = dcdg::CtaSmem<NPW*(BC * U * 8 + BC * 8), dcdg::ul_scal_bytes(U, 2), NPW, kWarps>::kBytes;
+  auto kern = dcdg::ul_pp2_f32<BC, U, kWarps, MINB>;
+  const int occ = occupancy_of(ctx, kern, smem);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int blocks = std::min((nsets + kWarps - 1) / kWarps, ctx->sms * occ);
+  kern<<<blocks, 32 * kWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K, kappa,
+                                          static_cast<float2*>(X));
+  return cudaGetLastError();
+}
+#endif
 
 // Optimal fusion at the north-star tile (B_c = 32, U = 16, fp32): the CD
 // kernel with post_eq_variance fused (ul_reg_f32<..., SIG = true>): one pass
@@ -419,7 +446,7 @@ cudaError_t launch_dl_split(dcdg_ctx* ctx, const void* H, const void* S, int P, 
 struct KDesc {
   int kind, a, b;
 };
-constexpr int kReg = 0, kMw = 1, kSplit = 2;
+constexpr int kReg = 0, kMw = 1, kSplit = 2, kPp2 = 3;
 
 struct Spec {
   int bc, u, fmt;
@@ -480,7 +507,11 @@ constexpr int minb_mw(int warps, int nw) { return warps / nw > 0 ? warps / nw : 
 // the split tile wins wherever the register kernel needs G >= 16 lanes or
 // several warps per problem; at B_c = 32, U = 16 the register kernel stays.
 const Spec kSpecs[] = {
+#if DCDG_UL_PP2
+    {32, 16, DCDG_FP32, launch_ul_pp2<32, 16, 8, minb(DCDG_MIN_WARPS_UL_F32)>, KDesc{kPp2, 16, 0}, DL_REG(32, 16, 8)},
+#else
     {32, 16, DCDG_FP32, UL_REG(32, 16, 8), DL_REG(32, 16, 8)},  // north-star target: B=256, C=8, U=16
+#endif
     {32, 8, DCDG_FP32, UL_REG(32, 8, DCDG_G_32x8), DL_REG(32, 8, DCDG_G_32x8)},  // paper / config 1: B_c=32, U=8
     {16, 16, DCDG_FP32, UL_REG(16, 16, DCDG_G_16x16_UL), DL_REG(16, 16, DCDG_G_16x16_DL)},  // B=128, C=8
     {64, 16, DCDG_FP32, UL_REG(64, 16, 16), DL_REG(64, 16, 16)},  // B=256, C=4 / B=512, C=8
@@ -829,7 +860,9 @@ int dcdg_kernel_name(int direction, int Bc, int U, int fmt, char* buf, int len) 
   const char* dir = direction ? "dl" : "ul";
   const char* f = fmt == DCDG_FP16 ? "f16" : "f32";
   const KDesc* kd = s ? (direction ? &s->dlk : &s->ulk) : nullptr;
-  if (kd && kd->kind == kMw)
+  if (kd && kd->kind == kPp2)
+    std::snprintf(tmp, sizeof tmp, "%s_pp2_%s<%d,%d,%d>", dir, f, Bc, U, kd->a);
+  else if (kd && kd->kind == kMw)
     std::snprintf(tmp, sizeof tmp, "%s_mw_%s<%d,%d,%d>", dir, f, Bc, U, kd->a);
   else if (kd && kd->kind == kSplit)
     std::snprintf(tmp, sizeof tmp, "%s_split_%s<%d,%d,%d,%d>", dir, f, Bc, U, kd->a, kd->b);
