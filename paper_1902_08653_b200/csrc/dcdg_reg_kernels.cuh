@@ -399,7 +399,11 @@ __global__ void __launch_bounds__(32 * W, MINB)
         for (int pl = 0; pl < NPW; ++pl) {
           const float em = __shfl_sync(0xffffffffu, emax, pl * G);
           // power-of-two scale: |h_ij|^2 <= em -> |h_ij sc| <= 1
-          const float sc = em > 0.f ? ldexpf(1.f, -static_cast<int>(ceilf(0.5f * __log2f(em)))) : 1.f;
+          // sc = 2^-e and 1/sc^2 = 2^2e built from the exponent bits (ldexpf and
+          // an IEEE division were 4% of the kernel's stall samples)
+          const int e = em > 0.f ? max(-60, min(60, static_cast<int>(ceilf(0.5f * __log2f(em))))) : 0;
+          const float sc = __int_as_float((127 - e) << 23);
+          const float isc2 = __int_as_float((127 + 2 * e) << 23);
           const unsigned char* tb = slot + pl * TILE_B;
           float gr0[4] = {}, gr1[4] = {}, gi0[4] = {}, gi1[4] = {};
 #pragma unroll
@@ -434,7 +438,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
             }
           }
           __syncwarp();  // every lane's reads of this tile are done before its image overwrites it
-          const float gs = gam / (sc * sc);
+          const float gs = gam * isc2;  // gam / sc^2, exact (power of two)
           float4* img = reinterpret_cast<float4*>(slot + pl * TILE_B);
           // C fragment: [0..1] row mg, cols 2mt, 2mt+1 of the n-tile; [2..3] row mg + 8
           img[apair_slot<U>(mg, mt)] = make_float4(fmaf(gs, gr0[0], mg == 2 * mt ? 1.f : 0.f),
