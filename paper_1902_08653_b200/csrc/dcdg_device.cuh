@@ -638,6 +638,15 @@ __device__ __forceinline__ float gram_trace_inverse_cpairs2(float2 (&R0r)[U / 2]
 #ifndef DCDG_SIG_COLS_STS32
 #define DCDG_SIG_COLS_STS32 0
 #endif
+// 1: the owner's pivot column is left as -d_kk M (no per-row selects), rescaled
+// in the trace.  Measured per site (profiles/lab/README.md): on in the variance
+// kernel and the fp16 Gram kernel, off in the fused fp32 CD kernel.
+#ifndef DCDG_SIG_COLS_SCALED
+#define DCDG_SIG_COLS_SCALED 1
+#endif
+#ifndef DCDG_SIG_COLS_SCALED_FUSED
+#define DCDG_SIG_COLS_SCALED_FUSED 0
+#endif
 
 // post_eq_variance (detect.cpp:112-130) by forward elimination of [A | I]
 // held as COLUMN PAIRS: lane k of the problem's U/2 lanes keeps columns 2k,
@@ -657,7 +666,11 @@ __device__ __forceinline__ float gram_trace_inverse_cpairs2(float2 (&R0r)[U / 2]
 // (`prow`: 2 x U float2 per problem, alternating by pivot parity) -- the pivot
 // row of a lane's columns is its own register.  Returns tr A^-1 on every lane
 // of the problem.
-template <int U>
+// SCALED: instead of selecting -f_i into the owner's column kk row by row,
+// the owner's copy of its pivot entry is zeroed, so that column keeps
+// a_i,kk = -d_kk M_i,kk and stays that multiple through every later update
+// (they are linear in it); the trace divides its |.|^2 by d_kk^2.
+template <int U, bool SCALED = DCDG_SIG_COLS_SCALED != 0>
 __device__ __forceinline__ float gram_trace_inverse_cols(float2 (&Cr)[U], float2 (&Ci)[U], int k, float4* prow,
                                                          bool& singular) {
   constexpr int NQ = U / 2;
@@ -697,14 +710,26 @@ __device__ __forceinline__ float gram_trace_inverse_cols(float2 (&Cr)[U], float2
     float inv;  // MUFU.RCP alone (<= 1 ulp): the IEEE __frcp_rn adds a Newton step and a slow-path branch to the chain
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(d));
     invd[kk] = inv;
-    const float2 pr = Cr[kk], pi = Ci[kk];  // pivot row kk over this lane's column pair
+    float2 pr = Cr[kk], pi = Ci[kk];  // pivot row kk over this lane's column pair
+    // SCALED: the owner's pivot entry taken as 0: its column kk keeps
+    // a_i,kk = -d_kk M_i,kk below the pivot, and every later update of that
+    // column is linear in it
+    if (SCALED && own) {
+      if (h) {
+        pr.y = 0.f;
+        pi.y = 0.f;
+      } else {
+        pr.x = 0.f;
+        pi.x = 0.f;
+      }
+    }
 #pragma unroll
     for (int i = 1; i < U; ++i) {
       if (i <= kk) continue;
       const float2 f = fmul2(inv, col[i]);  // f_i = a_i,kk / d
       Cr[i] = ffma2(f.y, pi, ffma2(-f.x, pr, Cr[i]));
       Ci[i] = ffma2(-f.y, pr, ffma2(-f.x, pi, Ci[i]));
-      if (own) {  // M_i,kk = -f_i
+      if (!SCALED && own) {  // M_i,kk = -f_i
         if (h) {
           Cr[i].y = -f.x;
           Ci[i].y = -f.y;
@@ -715,13 +740,26 @@ __device__ __forceinline__ float gram_trace_inverse_cols(float2 (&Cr)[U], float2
       }
     }
   }
+  // SCALED: column j below the diagonal holds -d_j M_ij, |M_ij|^2 = |a_ij|^2 / d_j^2
+  float s0 = 1.f, s1 = 1.f;
+  if (SCALED) {
+#pragma unroll
+    for (int jq = 0; jq < NQ; ++jq)
+      if (k == jq) {
+        s0 = invd[2 * jq] * invd[2 * jq];
+        s1 = invd[2 * jq + 1] * invd[2 * jq + 1];
+      }
+  }
   // (1 + sum_j |M_ij|^2) / d_i: the 1 from the lane's own diagonal rows, the
   // |M_ij|^2 of its two columns below the diagonal
   float t = 0.f;
 #pragma unroll
   for (int i = 0; i < U; ++i) {
     const float2 m = ffma2(Cr[i], Cr[i], fmul2(Ci[i], Ci[i]));
-    const float s = (2 * k < i ? m.x : 0.f) + (2 * k + 1 < i ? m.y : 0.f) + (2 * k == i || 2 * k + 1 == i ? 1.f : 0.f);
+    const float s = SCALED ? (2 * k < i ? m.x * s0 : 0.f) + (2 * k + 1 < i ? m.y * s1 : 0.f) +
+                                 (2 * k == i || 2 * k + 1 == i ? 1.f : 0.f)
+                           : (2 * k < i ? m.x : 0.f) + (2 * k + 1 < i ? m.y : 0.f) +
+                                 (2 * k == i || 2 * k + 1 == i ? 1.f : 0.f);
     t = fmaf(s, invd[i], t);
   }
 #pragma unroll

@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(32 * W, MINB)
       // the pivot rows go through the problem's scalar block (dead after the sweeps)
       bool singular = false;
 #if DCDG_SIG_COLS
-      const float tr = gram_trace_inverse_cols<U>(Cr, Ci, k, mnx, singular);
+      const float tr = gram_trace_inverse_cols<U, DCDG_SIG_COLS_SCALED_FUSED != 0>(Cr, Ci, k, mnx, singular);
 #elif DCDG_SIG_CPAIRS
       const float tr = DCDG_SIG_BLOCK2 ? gram_trace_inverse_cpairs2<U>(R0r, R0i, R1r, R1i, k, mnx, singular)
                                          : gram_trace_inverse_cpairs<U>(R0r, R0i, R1r, R1i, k, mnx, singular);
