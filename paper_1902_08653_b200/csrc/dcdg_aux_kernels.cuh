@@ -888,7 +888,10 @@ __global__ void fuse_kernel(const T* __restrict__ XL, const float* __restrict__ 
           total += 1.f / v[i];
         }
     }
-    if (bad && u == 0) record_status(status, s * C, ST_BAD_VARIANCE, 0);
+    // keyed at the subcarrier's LAST cluster: a cluster's own error (e.g. a
+    // singular variance) outranks it, as the reference's workers throw before
+    // fusion_weights runs (detect.cpp:160-176)
+    if (bad && u == 0) record_status(status, s * C + C - 1, ST_BAD_VARIANCE, 0);
     for (int c0 = 0; c0 < C; c0 += CH) {
       float2 v[CH];
       float q[CH];
@@ -980,7 +983,7 @@ __global__ void xchg_fuse_kernel(const unsigned char* __restrict__ win, const un
         if (!(v > 0.f) || !isfinite(v)) bad = true;
         total += 1.f / v;
       }
-      if (bad && u == 0) record_status(status, s * C_total, ST_BAD_VARIANCE, 0);
+      if (bad && u == 0) record_status(status, s * C_total + C_total - 1, ST_BAD_VARIANCE, 0);  // see fuse_kernel
       for (int c = 0; c < C_total; ++c) {
         const float w = (1.f / __ldcg(sigma2 + s * C_total + c)) / total;
         const float2 v = ldcg_c(XL, (static_cast<size_t>(s) * C_total + c) * U + u);
@@ -1156,7 +1159,7 @@ __global__ void fusion_weights_kernel(const float* __restrict__ s2, int S, int C
     if (!(v > 0.f) || !isfinite(v)) bad = true;
     total += 1.f / v;
   }
-  if (bad) record_status(status, s * C, ST_BAD_VARIANCE, 0);
+  if (bad) record_status(status, s * C + C - 1, ST_BAD_VARIANCE, 0);  // see fuse_kernel
   for (int c = 0; c < C; ++c) w[s * C + c] = (1.f / s2[s * C + c]) / total;
 }
 

@@ -105,3 +105,24 @@ def test_graphed_uplink_replays_with_new_inputs(engine, port):
     for b, x in ((b1, x1), (b2, x2)):
         ref, _, _ = port.ul_detect_batch(b["h_tiles"], b["y"], b["n0"], 1.0, 3, UNIFORM)
         assert rel_err(x, ref) <= TOL_FP32
+
+
+@pytest.mark.parametrize("bc,u,fmt", [(32, 16, "fp32"), (32, 8, "fp32"), (64, 16, "fp32"), (32, 16, "fp16")])
+def test_nonfinite_channel_optimal_fusion_raises_singular(engine, bc, u, fmt):
+    """A NaN channel entry makes the variance's pivot non-positive: the
+    reference's hermitian_solve throws (numerics.cpp:51-54) before any fusion,
+    from whichever factorisation runs the shape (the fused fp32 CD kernel, the
+    tensor-core variance kernel, the fp16 Gram kernel)."""
+    from paper_1902_08653_b200 import NumericError, to_fp16_pairs
+    b = batch(4, bc, u, S=6, seed=13)
+    h = b["h_tiles"].copy()
+    h[3, 2, 1, 4] = np.nan  # subcarrier 3, cluster 2
+    H, y = to_dev(h), to_dev(b["y"])
+    if fmt == "fp16":
+        H, y = to_fp16_pairs(H), to_fp16_pairs(y)
+    r = engine.ul_detect(H, y, n0=b["n0"], K=3, fusion="optimal")
+    with pytest.raises(NumericError, match="hermitian_solve: matrix is numerically singular") as ei:
+        engine.sync()
+    assert ei.value.problem == 3 * 4 + 2
+    del r
+    engine.sync()  # the status word is cleared after being reported
