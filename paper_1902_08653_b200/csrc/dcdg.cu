@@ -259,13 +259,17 @@ cudaError_t launch_ul_f32_sig(dcdg_ctx* ctx, const void* H, const void* Y, int P
                 : launch_ul_f32_sig_k<32, 16, 8>(ctx, H, Y, P, K, kappa, X, s2, gam, scale, st);
 }
 
-// The north-star tile with half of it in TMEM and 4 lanes per problem
-// (dcdg_tmem_kernels.cuh), uniform-fusion CD only.
+// The north-star tile (B_c = 32, U = 16, fp32, uniform fusion) with half of
+// each channel tile in TMEM (dcdg_tmem_kernels.cuh).  3 (default): ul_tmh_f32,
+// 8 lanes per problem and the TMA staging slot as ul_reg_f32, odd coordinate
+// blocks' columns in TMEM, 138 registers -> 3 warps per scheduler (12 per SM,
+// 4-warp CTAs): 0.151 -> 0.141 ms per 134 400 problems (profiles/lab/README.md).
+// 1, 2: lab variants with 4 lanes per problem (slower); 0: ul_reg_f32.
 #ifndef DCDG_UL_TMEM
-#define DCDG_UL_TMEM 0
+#define DCDG_UL_TMEM 3
 #endif
 #ifndef DCDG_UL_TMEM_MINB
-#define DCDG_UL_TMEM_MINB 2
+#define DCDG_UL_TMEM_MINB (DCDG_UL_TMEM == 3 ? 3 : 2)
 #endif
 bool ul_tm_shape(int bc, int u, int fmt) { return DCDG_UL_TMEM && fmt == DCDG_FP32 && bc == 32 && u == 16; }
 
@@ -274,6 +278,23 @@ cudaError_t launch_ul_tm(dcdg_ctx* ctx, const void* H, const void* Y, int P, int
 #if DCDG_UL_TMEM  // lab kernels (profiles/lab/README.md): only compiled when switched on
   constexpr int NPW = 8;
   constexpr size_t smem = dcdg::kTmWarps * NPW * dcdg::ul_scal_bytes(16, 2);
+#if DCDG_UL_TMEM == 3  // 8 lanes per problem, odd blocks in TMEM, 3 warps per scheduler
+  {
+    constexpr int NPW3 = 4;
+    constexpr size_t smem3 = dcdg::CtaSmem<NPW3*(32 * 16 * 8 + 32 * 8), dcdg::ul_scal_bytes(16, 2), NPW3,
+                                           dcdg::kTmhWarps>::kBytes;
+    auto kern3 = dcdg::ul_tmh_f32<DCDG_UL_TMEM_MINB>;
+    // the occupancy query reports 1 CTA for this kernel although ncu's launch
+    // limits (shared memory, registers) both allow 3: size the grid from MINB
+    (void)occupancy_of(ctx, kern3, smem3, 32 * dcdg::kTmhWarps);  // sets the shared-memory attribute
+    const int occ3 = DCDG_UL_TMEM_MINB;
+    const int nsets3 = (P + NPW3 - 1) / NPW3;
+    const int blocks3 = std::min((nsets3 + dcdg::kTmhWarps - 1) / dcdg::kTmhWarps, ctx->sms * occ3);
+    kern3<<<blocks3, 32 * dcdg::kTmhWarps, smem3, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y),
+                                                         P, K, kappa, static_cast<float2*>(X));
+    return cudaGetLastError();
+  }
+#endif
 #if DCDG_UL_TMEM == 2  // staged in two TMA phases per set (dcdg_tmem_kernels.cuh)
   constexpr size_t smem2 = dcdg::kTmWarps * (dcdg::kTm2SlotB + NPW * dcdg::ul_scal_bytes(16, 2)) + dcdg::kTmWarps * 16;
   auto kern2 = dcdg::ul_tm2_f32<DCDG_UL_TMEM_MINB>;
@@ -860,7 +881,9 @@ int dcdg_kernel_name(int direction, int Bc, int U, int fmt, char* buf, int len) 
   const char* dir = direction ? "dl" : "ul";
   const char* f = fmt == DCDG_FP16 ? "f16" : "f32";
   const KDesc* kd = s ? (direction ? &s->dlk : &s->ulk) : nullptr;
-  if (kd && kd->kind == kPp2)
+  if (!direction && ul_tm_shape(Bc, U, fmt))
+    std::snprintf(tmp, sizeof tmp, DCDG_UL_TMEM == 3 ? "ul_tmh_f32<%d,%d,8>" : "ul_tm_f32<%d,%d,4>", Bc, U);
+  else if (kd && kd->kind == kPp2)
     std::snprintf(tmp, sizeof tmp, "%s_pp2_%s<%d,%d,%d>", dir, f, Bc, U, kd->a);
   else if (kd && kd->kind == kMw)
     std::snprintf(tmp, sizeof tmp, "%s_mw_%s<%d,%d,%d>", dir, f, Bc, U, kd->a);

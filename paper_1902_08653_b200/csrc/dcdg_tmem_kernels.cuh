@@ -526,4 +526,230 @@ __global__ void __launch_bounds__(32 * kTmWarps, MINB)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_s), "n"(kTm2Cols));
 }
 
+// ---------------------------------------------------------------------------
+// ul_tmh_f32 (lab, DCDG_UL_TMEM=3): ul_reg_f32's mapping (8 lanes per problem,
+// 4 problems per warp, TMA staging slot per warp) with the odd coordinate
+// blocks' columns (half the tile, 64 values per lane) in TMEM, so the kernel
+// fits 3 warps per scheduler (<= 168 registers) instead of 2: 4-warp CTAs
+// (one TMEM lane quarter each, 64 columns per CTA), 3 CTAs per SM (76.6 KB of
+// shared memory each).  Arithmetic = ul_reg_f32 (detect.cpp:67-110).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const float2 (&a)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          addr),
+      "f"(a[0].x), "f"(a[0].y), "f"(a[1].x), "f"(a[1].y), "f"(a[2].x), "f"(a[2].y), "f"(a[3].x), "f"(a[3].y),
+      "f"(a[4].x), "f"(a[4].y), "f"(a[5].x), "f"(a[5].y), "f"(a[6].x), "f"(a[6].y), "f"(a[7].x), "f"(a[7].y));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float2 (&a)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=f"(a[0].x), "=f"(a[0].y), "=f"(a[1].x), "=f"(a[1].y), "=f"(a[2].x), "=f"(a[2].y), "=f"(a[3].x),
+        "=f"(a[3].y), "=f"(a[4].x), "=f"(a[4].y), "=f"(a[5].x), "=f"(a[5].y), "=f"(a[6].x), "=f"(a[6].y),
+        "=f"(a[7].x), "=f"(a[7].y)
+      : "r"(addr)
+      : "memory");
+}
+constexpr int kTmhWarps = 4;
+constexpr int kTmhCols = 64;
+
+template <int MINB>
+__global__ void __launch_bounds__(32 * kTmhWarps, MINB)
+    ul_tmh_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
+               float2* __restrict__ X) {
+  constexpr int BC = 32, U = 16, G = 8, LB = 2, NPW = 32 / G, R = BC / G, NP = R / 2;  // NP = 2
+  constexpr int NQ = U / LB;
+  constexpr int TILE_B = BC * U * 8, Y_B = BC * 8, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
+  constexpr int SCAL_B = ul_scal_bytes(U, LB);
+  using L = CtaSmem<SLOT_B, SCAL_B, NPW, kTmhWarps>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint32_t tmem_base_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / G, k = lane % G;
+  unsigned char* slot = smem + warp * SLOT_B;
+  float4* mnx = reinterpret_cast<float4*>(smem + L::kScalOff + (warp * NPW + g) * SCAL_B);
+  float4* gb = mnx + U;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff) + warp;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "n"(kTmhCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tbase = tmem_base_s + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
+  const int nsets = (P + NPW - 1) / NPW;
+  const int nw = gridDim.x * kTmhWarps;
+  int set = blockIdx.x * kTmhWarps + warp;
+  const uint64_t pol = l2_evict_first_policy();
+  if (lane == 0 && set < nsets) issue_set(slot, bar, H, Y, set, P, NPW, TILE_B, Y_B, true, 1, pol);
+  uint32_t phase = 0;
+  const float2 z2 = make_float2(0.f, 0.f);
+  for (; set < nsets; set += nw) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    float2 hr[NQ / 2][2][NP], hi[NQ / 2][2][NP], rr[NP], ri[NP];
+    float nrm[U], pg[2 * NQ];
+    {
+      const float4* t4 = reinterpret_cast<const float4*>(slot + g * TILE_B);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        float2 ar[NP], ai[NP], br[NP], bi[NP];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          const float4 va = t4[(2 * q) * (BC / 2) + c * G + k];
+          const float4 vb = t4[(2 * q + 1) * (BC / 2) + c * G + k];
+          ar[c] = pair(va.x, va.z);
+          ai[c] = pair(va.y, va.w);
+          br[c] = pair(vb.x, vb.z);
+          bi[c] = pair(vb.y, vb.w);
+        }
+        float2 ea = fmul2(ar[0], ar[0]), eb = fmul2(br[0], br[0]), gr = z2, gi = z2;
+        ea = ffma2(ai[0], ai[0], ea);
+        eb = ffma2(bi[0], bi[0], eb);
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          if (c > 0) {
+            ea = ffma2(ai[c], ai[c], ffma2(ar[c], ar[c], ea));
+            eb = ffma2(bi[c], bi[c], ffma2(br[c], br[c], eb));
+          }
+          gr = ffma2(bi[c], ai[c], ffma2(br[c], ar[c], gr));  // G_{2q+1,2q} = h_{2q+1}^H h_{2q}
+          gi = ffma2(neg2(bi[c]), ar[c], ffma2(br[c], ai[c], gi));
+        }
+        nrm[2 * q] = hsum(ea);
+        nrm[2 * q + 1] = hsum(eb);
+        pg[2 * q] = hsum(gr);
+        pg[2 * q + 1] = hsum(gi);
+        if (q & 1) {
+          float2 ta[8];
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            ta[4 * c] = ar[c];
+            ta[4 * c + 1] = ai[c];
+            ta[4 * c + 2] = br[c];
+            ta[4 * c + 3] = bi[c];
+          }
+          tmem_st16(tbase + 16 * (q / 2), ta);
+        } else {
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            hr[q / 2][0][c] = ar[c];
+            hi[q / 2][0][c] = ai[c];
+            hr[q / 2][1][c] = br[c];
+            hi[q / 2][1][c] = bi[c];
+          }
+        }
+      }
+      const float4* y4 = reinterpret_cast<const float4*>(slot + NPW * TILE_B + g * Y_B);
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        const float4 v = y4[c * G + k];
+        rr[c] = pair(v.x, v.z);
+        ri[c] = pair(v.y, v.w);
+      }
+    }
+    tmem_wait_st();
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
+    {
+      group_reduce_scatter<G>(nrm, k);
+#pragma unroll
+      for (int i = 0; i < U / G; ++i) {
+        const int idx = k * (U / G) + i;
+        const float m = __fdividef(1.f, nrm[i] + kappa);  // m_j = 1/(||h_j||^2 + N0/Ex)
+        mnx[idx] = make_float4(m, m * nrm[i], 0.f, 0.f);   // n_j = m_j ||h_j||^2, x_j = 0
+      }
+      group_reduce_scatter<G>(pg, k);
+      float* gf = reinterpret_cast<float*>(gb);
+#pragma unroll
+      for (int i = 0; i < 2 * NQ / G; ++i) {
+        const int gi2 = k * (2 * NQ / G) + i, e = gi2 >> 1;
+        if (gi2 & 1) {  // stored as (Re G, Im G, -Im G, Re G)
+          gf[e * 4 + 1] = pg[i];
+          gf[e * 4 + 2] = -pg[i];
+        } else {
+          gf[e * 4 + 0] = pg[i];
+          gf[e * 4 + 3] = pg[i];
+        }
+      }
+    }
+    __syncwarp();
+
+    // ---- K sweeps; the odd block's columns come from TMEM one block ahead
+    float2 tA[8];
+    for (int t = 0; t < K; ++t) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const bool tm = q & 1;
+        if (!tm) tmem_ld16(tbase + 16 * (q / 2), tA);  // the next (odd) block, landing during this one
+        if (tm) tmem_wait_ld();
+        float2 ar[NP], ai[NP], br[NP], bi[NP];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          ar[c] = tm ? tA[4 * c] : hr[q / 2][0][c];
+          ai[c] = tm ? tA[4 * c + 1] : hi[q / 2][0][c];
+          br[c] = tm ? tA[4 * c + 2] : hr[q / 2][1][c];
+          bi[c] = tm ? tA[4 * c + 3] : hi[q / 2][1][c];
+        }
+        float2 d[LB];
+        {
+          float2 a0 = z2, c0 = z2, a1 = z2, c1 = z2;  // h_j^H r for j = 2q, 2q+1 (cdotc, detect.cpp:100)
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            a0 = ffma2(ai[c], ri[c], ffma2(ar[c], rr[c], a0));
+            c0 = ffma2(neg2(ai[c]), rr[c], ffma2(ar[c], ri[c], c0));
+            a1 = ffma2(bi[c], ri[c], ffma2(br[c], rr[c], a1));
+            c1 = ffma2(neg2(bi[c]), rr[c], ffma2(br[c], ri[c], c1));
+          }
+          d[0] = make_float2(hsum(a0), hsum(c0));
+          d[1] = make_float2(hsum(a1), hsum(c1));
+        }
+        group_allreduce2<G>(d);
+        float2 dx[LB];
+        {
+          const float4 A0 = mnx[2 * q], A1 = mnx[2 * q + 1], Gab = gb[q];
+          const float2 x0 = make_float2(A0.z, A0.w);
+          const float2 n0 = ffma2(A0.x, d[0], fmul2(A0.y, x0));  // detect.cpp:100-103
+          dx[0] = fadd2(n0, neg2(x0));
+          d[1] = ffma2(-dx[0].x, make_float2(Gab.x, Gab.y), d[1]);  // h_1^H (r - dx_0 h_0)
+          d[1] = ffma2(-dx[0].y, make_float2(Gab.z, Gab.w), d[1]);
+          const float2 x1 = make_float2(A1.z, A1.w);
+          const float2 n1 = ffma2(A1.x, d[1], fmul2(A1.y, x1));
+          dx[1] = fadd2(n1, neg2(x1));
+          *reinterpret_cast<float2*>(&mnx[2 * q].z) = n0;
+          *reinterpret_cast<float2*>(&mnx[2 * q + 1].z) = n1;
+        }
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {  // r -= dx_j h_j   (caxpy, detect.cpp:104)
+          rr[c] = ffma2(dx[0].y, ai[c], ffma2(-dx[0].x, ar[c], rr[c]));
+          ri[c] = ffma2(-dx[0].y, ar[c], ffma2(-dx[0].x, ai[c], ri[c]));
+          rr[c] = ffma2(dx[1].y, bi[c], ffma2(-dx[1].x, br[c], rr[c]));
+          ri[c] = ffma2(-dx[1].y, br[c], ffma2(-dx[1].x, bi[c], ri[c]));
+        }
+      }
+    }
+    __syncwarp();
+    const int p = set * NPW + g;
+    if (p < P) {
+      float4* xo = reinterpret_cast<float4*>(X + static_cast<size_t>(p) * U);
+#pragma unroll
+      for (int i = k; i < U / 2; i += G) {
+        const float4 u0 = mnx[2 * i], u1 = mnx[2 * i + 1];
+        xo[i] = make_float4(u0.z, u0.w, u1.z, u1.w);
+      }
+    }
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_s), "n"(kTmhCols));
+}
+
 }  // namespace dcdg

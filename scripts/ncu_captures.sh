@@ -5,7 +5,7 @@ rm -rf /tmp/reps; mkdir -p /tmp/reps  # a reused box keeps /tmp: never summarise
 args=""
 for k in "ul fp32 4480" "dl fp32 4480" "ul fp16 2240" "dl fp16 2240" "opt fp32 4480" "pev fp32 4096"; do
   set -- $k
-  timeout 300 ncu -f --set full --clock-control none --import-source on -k regex:"reg_f|gram_f16|gram_chol|pev16|pev_tc" -s 2 -c 1 \
+  timeout 300 ncu -f --set full --clock-control none --import-source on -k regex:"reg_f|tmh_f|gram_f16|gram_chol|pev16|pev_tc" -s 2 -c 1 \
     -o /tmp/reps/full_$1_$2 python scripts/prof_kernel.py $1 $2 4 > /dev/null 2>&1
   args="$args ${1}_${2}_32_16=/tmp/reps/full_$1_$2.ncu-rep:134400:$3"
 done

@@ -106,7 +106,7 @@ def test_power_scale_and_fusion_weight_errors():
 
 
 def test_kernel_dispatch_table():
-    assert _lib.kernel_name(0, 32, 16, FP32) == "ul_reg_f32<32,16,8>"
+    assert _lib.kernel_name(0, 32, 16, FP32) == "ul_tmh_f32<32,16,8>"  # half of the tile in TMEM
     assert _lib.kernel_name(1, 32, 16, FP32) == "dl_reg_f32<32,16,8>"
     assert _lib.kernel_name(0, 32, 16, FP16) == "ul_reg_f16<32,16,4>"
     assert _lib.kernel_name(0, 32, 8, FP32) == "ul_reg_f32<32,8,4>"
