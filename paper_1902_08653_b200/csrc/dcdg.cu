@@ -33,6 +33,13 @@
 #endif
 #include "dcdg_split_kernels.cuh"
 #include "dcdg_tmem_kernels.cuh"
+// target uplink tile in TMEM (see launch_ul_tm below)
+#ifndef DCDG_UL_TMEM
+#define DCDG_UL_TMEM 3
+#endif
+#ifndef DCDG_UL_TMEM_MINB
+#define DCDG_UL_TMEM_MINB (DCDG_UL_TMEM == 3 ? 3 : 2)
+#endif
 
 struct dcdg_ctx {
   int device = 0;
@@ -253,8 +260,28 @@ cudaError_t launch_ul_f32_sig_k(dcdg_ctx* ctx, const void* H, const void* Y, int
 
 // B_c = 32 with U = 16 (the north-star tile, 8 lanes per problem) or U = 8
 // (the paper's / configs[0] tile, 4 lanes per problem)
+// lab (off): the fused-variance batch on the TMEM half-tile kernel, 168
+// registers and 12 warps/SM: 0.3771 vs 0.3754 ms (no gain, profiles/lab/README.md)
+#ifndef DCDG_UL_TMEM_SIG
+#define DCDG_UL_TMEM_SIG 0
+#endif
 cudaError_t launch_ul_f32_sig(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
                               float* s2, float gam, float scale, int U, cudaStream_t st) {
+#if DCDG_UL_TMEM == 3 && DCDG_UL_TMEM_SIG
+  if (U == 16) {  // the TMEM half-tile kernel with the fused variance (dcdg_tmem_kernels.cuh)
+    constexpr int NPW = 4;
+    constexpr size_t smem =
+        dcdg::CtaSmem<NPW*(32 * 16 * 8 + 32 * 8), dcdg::ul_scal_bytes(16, 2), NPW, dcdg::kTmhWarps>::kBytes;
+    auto kern = dcdg::ul_tmh_f32<DCDG_UL_TMEM_MINB, true>;
+    (void)occupancy_of(ctx, kern, smem, 32 * dcdg::kTmhWarps);  // sets the shared-memory attribute
+    const int nsets = (P + NPW - 1) / NPW;
+    const int blocks = std::min((nsets + dcdg::kTmhWarps - 1) / dcdg::kTmhWarps, ctx->sms * DCDG_UL_TMEM_MINB);
+    kern<<<blocks, 32 * dcdg::kTmhWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P,
+                                                      K, kappa, static_cast<float2*>(X), s2, gam, scale,
+                                                      ctx->d_status);
+    return cudaGetLastError();
+  }
+#endif
   return U == 8 ? launch_ul_f32_sig_k<32, 8, 4>(ctx, H, Y, P, K, kappa, X, s2, gam, scale, st)
                 : launch_ul_f32_sig_k<32, 16, 8>(ctx, H, Y, P, K, kappa, X, s2, gam, scale, st);
 }
@@ -265,12 +292,7 @@ cudaError_t launch_ul_f32_sig(dcdg_ctx* ctx, const void* H, const void* Y, int P
 // blocks' columns in TMEM, 138 registers -> 3 warps per scheduler (12 per SM,
 // 4-warp CTAs): 0.151 -> 0.141 ms per 134 400 problems (profiles/lab/README.md).
 // 1, 2: lab variants with 4 lanes per problem (slower); 0: ul_reg_f32.
-#ifndef DCDG_UL_TMEM
-#define DCDG_UL_TMEM 3
-#endif
-#ifndef DCDG_UL_TMEM_MINB
-#define DCDG_UL_TMEM_MINB (DCDG_UL_TMEM == 3 ? 3 : 2)
-#endif
+// (DCDG_UL_TMEM, DCDG_UL_TMEM_MINB: defined after the includes)
 bool ul_tm_shape(int bc, int u, int fmt) { return DCDG_UL_TMEM && fmt == DCDG_FP32 && bc == 32 && u == 16; }
 
 cudaError_t launch_ul_tm(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
@@ -291,7 +313,8 @@ cudaError_t launch_ul_tm(dcdg_ctx* ctx, const void* H, const void* Y, int P, int
     const int nsets3 = (P + NPW3 - 1) / NPW3;
     const int blocks3 = std::min((nsets3 + dcdg::kTmhWarps - 1) / dcdg::kTmhWarps, ctx->sms * occ3);
     kern3<<<blocks3, 32 * dcdg::kTmhWarps, smem3, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y),
-                                                         P, K, kappa, static_cast<float2*>(X));
+                                                         P, K, kappa, static_cast<float2*>(X), nullptr, 0.f, 0.f,
+                                                         nullptr);
     return cudaGetLastError();
   }
 #endif

@@ -553,10 +553,87 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float2 (&a)[8]) {
 constexpr int kTmhWarps = 4;
 constexpr int kTmhCols = 64;
 
-template <int MINB>
+// post_eq_variance for the set still in the staging slot (detect.cpp:112-130):
+// ul_reg_f32<..., SIG>'s tail (tensor-core Gram from the slot, A = I + gam G
+// as a column-pair image over the consumed tile, forward elimination), then
+// the next set's copy.  See ul_reg_f32 for the derivation.
+template <int BC, int U, int G, int NPW, int TILE_B, int Y_B>
+__device__ __forceinline__ void fused_variance_tail(unsigned char* slot, float4* mnx, float emax, float gam,
+                                                    float scale, float* __restrict__ sigma2,
+                                                    unsigned long long* __restrict__ status, int p, int P, int g,
+                                                    int k, int lane, int set, int nw, int nsets, uint64_t* bar,
+                                                    const float2* H, const float2* Y, uint64_t pol) {
+  static_assert(U == 16 && G == 8 && NPW == 4, "the north-star tile");
+  const int mg = lane >> 2, mt = lane & 3;  // mma fragment coordinates
+#pragma unroll
+  for (int pl = 0; pl < NPW; ++pl) {
+    const float em = __shfl_sync(0xffffffffu, emax, pl * G);
+    const int e = em > 0.f ? max(-60, min(60, static_cast<int>(ceilf(0.5f * __log2f(em))))) : 0;
+    const float sc = __int_as_float((127 - e) << 23);
+    const float isc2 = __int_as_float((127 + 2 * e) << 23);
+    const unsigned char* tb = slot + pl * TILE_B;
+    float gr0[4] = {}, gr1[4] = {}, gi0[4] = {}, gi1[4] = {};
+#pragma unroll
+    for (int ks = 0; ks < BC / 8; ++ks) {
+      const float4 u0 = *reinterpret_cast<const float4*>(tb + mg * (BC * 8) + (8 * ks + 2 * mt) * 8);
+      const float4 u1 = *reinterpret_cast<const float4*>(tb + (mg + 8) * (BC * 8) + (8 * ks + 2 * mt) * 8);
+      uint32_t ah[4], al[4];
+      split_h2(fmul2(sc, make_float2(u0.x, u0.y)), ah[0], al[0]);
+      split_h2(fmul2(sc, make_float2(u0.z, u0.w)), ah[2], al[2]);
+      split_h2(fmul2(sc, make_float2(u1.x, u1.y)), ah[1], al[1]);
+      split_h2(fmul2(sc, make_float2(u1.z, u1.w)), ah[3], al[3]);
+      mma_f16f32(gr0, ah, ah[0], ah[2]);
+      mma_f16f32(gr0, ah, al[0], al[2]);
+      mma_f16f32(gr0, al, ah[0], ah[2]);
+      mma_f16f32(gi0, ah, wprime(ah[0]), wprime(ah[2]));
+      mma_f16f32(gi0, ah, wprime(al[0]), wprime(al[2]));
+      mma_f16f32(gi0, al, wprime(ah[0]), wprime(ah[2]));
+      mma_f16f32(gr1, ah, ah[1], ah[3]);
+      mma_f16f32(gr1, ah, al[1], al[3]);
+      mma_f16f32(gr1, al, ah[1], ah[3]);
+      mma_f16f32(gi1, ah, wprime(ah[1]), wprime(ah[3]));
+      mma_f16f32(gi1, ah, wprime(al[1]), wprime(al[3]));
+      mma_f16f32(gi1, al, wprime(ah[1]), wprime(ah[3]));
+    }
+    __syncwarp();  // every lane's reads of this tile are done before its image overwrites it
+    const float gs = gam * isc2;
+    float4* img = reinterpret_cast<float4*>(slot + pl * TILE_B);
+    img[apair_slot<U>(mg, mt)] = make_float4(fmaf(gs, gr0[0], mg == 2 * mt ? 1.f : 0.f),
+                                             fmaf(gs, gr0[1], mg == 2 * mt + 1 ? 1.f : 0.f), gs * gi0[0], gs * gi0[1]);
+    img[apair_slot<U>(mg, 4 + mt)] = make_float4(gs * gr1[0], gs * gr1[1], gs * gi1[0], gs * gi1[1]);
+    img[apair_slot<U>(mg + 8, mt)] = make_float4(gs * gr0[2], gs * gr0[3], gs * gi0[2], gs * gi0[3]);
+    img[apair_slot<U>(mg + 8, 4 + mt)] = make_float4(fmaf(gs, gr1[2], mg == 2 * mt ? 1.f : 0.f),
+                                                     fmaf(gs, gr1[3], mg == 2 * mt + 1 ? 1.f : 0.f), gs * gi1[2],
+                                                     gs * gi1[3]);
+  }
+  __syncwarp();
+  float2 Cr[U], Ci[U];
+  {
+    const float4* a4 = reinterpret_cast<const float4*>(slot + g * TILE_B);
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const float4 a = a4[apair_slot<U>(i, k)];
+      Cr[i] = make_float2(a.x, a.y);
+      Ci[i] = make_float2(a.z, a.w);
+    }
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
+  bool singular = false;
+  const float tr = gram_trace_inverse_cols<U, DCDG_SIG_COLS_SCALED_FUSED != 0>(Cr, Ci, k, mnx, singular);
+  const unsigned sing = __ballot_sync(0xffffffffu, singular);
+  if (p < P && k == 0) {
+    sigma2[p] = scale * tr;
+    if ((sing >> (G * g)) & ((1u << G) - 1u)) record_status(status, p, ST_SINGULAR, 0);
+  }
+}
+
+template <int MINB, bool SIG = false>
 __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
     ul_tmh_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
-               float2* __restrict__ X) {
+               float2* __restrict__ X, float* __restrict__ sigma2 = nullptr, float gam = 0.f, float scale = 0.f,
+               unsigned long long* __restrict__ status = nullptr) {
   constexpr int BC = 32, U = 16, G = 8, LB = 2, NPW = 32 / G, R = BC / G, NP = R / 2;  // NP = 2
   constexpr int NQ = U / LB;
   constexpr int TILE_B = BC * U * 8, Y_B = BC * 8, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
@@ -654,11 +731,20 @@ __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
       }
     }
     tmem_wait_st();
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
+    if constexpr (!SIG) {  // the fused variance keeps the slot until its Gram image is read
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0 && set + nw < nsets) issue_set(slot, bar, H, Y, set + nw, P, NPW, TILE_B, Y_B, true, 1, pol);
+    }
+    float emax = 0.f;
     {
       group_reduce_scatter<G>(nrm, k);
+      if constexpr (SIG) {  // the problem's largest column energy (scale of the split Gram)
+#pragma unroll
+        for (int i = 0; i < U / G; ++i) emax = fmaxf(emax, nrm[i]);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+      }
 #pragma unroll
       for (int i = 0; i < U / G; ++i) {
         const int idx = k * (U / G) + i;
@@ -744,6 +830,9 @@ __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
         xo[i] = make_float4(u0.z, u0.w, u1.z, u1.w);
       }
     }
+    if constexpr (SIG)
+      fused_variance_tail<BC, U, G, NPW, TILE_B, Y_B>(slot, mnx, emax, gam, scale, sigma2, status, p, P, g, k, lane,
+                                                      set, nw, nsets, bar, H, Y, pol);
     __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
