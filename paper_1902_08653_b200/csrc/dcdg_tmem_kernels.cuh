@@ -1,5 +1,13 @@
-// Uplink CD kernel with half of each channel tile in tensor memory (TMEM),
-// so that 4 lanes own a problem instead of 8 (sm_100a).
+// Uplink CD kernels with half of each channel tile in tensor memory (TMEM).
+//
+// ul_tmh_f32 (bottom of this file) is the PRODUCTION kernel for the target
+// tile (B_c = 32, U = 16, fp32, uniform fusion; DCDG_UL_TMEM = 3): 8 lanes per
+// problem as ul_reg_f32, odd coordinate blocks in TMEM, 12 warps per SM.
+// ul_tm_f32 / ul_tm2_f32 below are lab variants with 4 lanes per problem
+// (slower, profiles/lab/README.md).
+//
+// ul_tm_f32: half of each tile in TMEM so that 4 lanes own a problem instead
+// of 8 (sm_100a).
 //
 // Why: per coordinate block the sweep pays a fixed chain (dot -> butterfly ->
 // scalar update -> rank-1 update) and per-lane overhead; 4 lanes per problem
