@@ -559,6 +559,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float2 (&a)[8]) {
       : "memory");
 }
 constexpr int kTmhWarps = 4;
+// odd coordinate blocks kept in TMEM by ul_tmh_f32 (of 4; the others in registers)
+#ifndef DCDG_TMH_NTM
+#define DCDG_TMH_NTM 4
+#endif
 constexpr int kTmhCols = 64;
 
 // post_eq_variance for the set still in the staging slot (detect.cpp:112-130):
@@ -678,7 +682,11 @@ __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
   for (; set < nsets; set += nw) {
     mbar_wait(bar, phase);
     phase ^= 1u;
-    float2 hr[NQ / 2][2][NP], hi[NQ / 2][2][NP], rr[NP], ri[NP];
+    // odd blocks q with q/2 < NTM in TMEM, the rest in registers (slot rslot(q))
+    constexpr int NTM = DCDG_TMH_NTM, NRB = NQ - NTM;
+    auto in_tm = [](int q) { return (q & 1) && (q / 2) < NTM; };
+    auto rslot = [](int q) { return (q & 1) ? NQ / 2 + (q / 2 - NTM) : q / 2; };
+    float2 hr[NRB][2][NP], hi[NRB][2][NP], rr[NP], ri[NP];
     float nrm[U], pg[2 * NQ];
     {
       const float4* t4 = reinterpret_cast<const float4*>(slot + g * TILE_B);
@@ -710,7 +718,7 @@ __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
         nrm[2 * q + 1] = hsum(eb);
         pg[2 * q] = hsum(gr);
         pg[2 * q + 1] = hsum(gi);
-        if (q & 1) {
+        if (in_tm(q)) {
           float2 ta[8];
 #pragma unroll
           for (int c = 0; c < NP; ++c) {
@@ -723,10 +731,10 @@ __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
         } else {
 #pragma unroll
           for (int c = 0; c < NP; ++c) {
-            hr[q / 2][0][c] = ar[c];
-            hi[q / 2][0][c] = ai[c];
-            hr[q / 2][1][c] = br[c];
-            hi[q / 2][1][c] = bi[c];
+            hr[rslot(q)][0][c] = ar[c];
+            hi[rslot(q)][0][c] = ai[c];
+            hr[rslot(q)][1][c] = br[c];
+            hi[rslot(q)][1][c] = bi[c];
           }
         }
       }
@@ -780,16 +788,16 @@ __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
     for (int t = 0; t < K; ++t) {
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        const bool tm = q & 1;
-        if (!tm) tmem_ld16(tbase + 16 * (q / 2), tA);  // the next (odd) block, landing during this one
+        const bool tm = in_tm(q);
+        if (q + 1 < NQ && in_tm(q + 1)) tmem_ld16(tbase + 16 * (q / 2), tA);  // the next block, landing during this one
         if (tm) tmem_wait_ld();
         float2 ar[NP], ai[NP], br[NP], bi[NP];
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
-          ar[c] = tm ? tA[4 * c] : hr[q / 2][0][c];
-          ai[c] = tm ? tA[4 * c + 1] : hi[q / 2][0][c];
-          br[c] = tm ? tA[4 * c + 2] : hr[q / 2][1][c];
-          bi[c] = tm ? tA[4 * c + 3] : hi[q / 2][1][c];
+          ar[c] = tm ? tA[4 * c] : hr[rslot(q)][0][c];
+          ai[c] = tm ? tA[4 * c + 1] : hi[rslot(q)][0][c];
+          br[c] = tm ? tA[4 * c + 2] : hr[rslot(q)][1][c];
+          bi[c] = tm ? tA[4 * c + 3] : hi[rslot(q)][1][c];
         }
         float2 d[LB];
         {
