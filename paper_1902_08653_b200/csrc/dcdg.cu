@@ -293,30 +293,51 @@ cudaError_t launch_ul_f32_sig(dcdg_ctx* ctx, const void* H, const void* Y, int P
 // 4-warp CTAs): 0.151 -> 0.141 ms per 134 400 problems (profiles/lab/README.md).
 // 1, 2: lab variants with 4 lanes per problem (slower); 0: ul_reg_f32.
 // (DCDG_UL_TMEM, DCDG_UL_TMEM_MINB: defined after the includes)
-bool ul_tm_shape(int bc, int u, int fmt) { return DCDG_UL_TMEM && fmt == DCDG_FP32 && bc == 32 && u == 16; }
+// Also the 64x16 tile (G = 16): 0.52 -> 0.55 of HBM in the configs[4] sweep;
+// the 16x16 tile (G = 4, 8 problems per warp) measured 0.558 -> 0.547 and
+// keeps ul_reg_f32 unless DCDG_UL_TMH_MORE = 2 (profiles/lab/README.md).
+#ifndef DCDG_UL_TMH_MORE
+#define DCDG_UL_TMH_MORE 1
+#endif
+bool ul_tm_shape(int bc, int u, int fmt) {
+  return DCDG_UL_TMEM && fmt == DCDG_FP32 && u == 16 &&
+         (bc == 32 || (DCDG_UL_TMEM == 3 && ((DCDG_UL_TMH_MORE >= 1 && bc == 64) ||
+                                            (DCDG_UL_TMH_MORE >= 2 && bc == 16))));
+}
+int ul_tmh_g(int bc) { return bc == 64 ? 16 : bc == 16 ? 4 : 8; }
+
+#if DCDG_UL_TMEM == 3
+template <int BC, int G>
+cudaError_t launch_ul_tmh(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                          cudaStream_t st) {
+  constexpr int NPW = 32 / G;
+  constexpr size_t smem =
+      dcdg::CtaSmem<NPW*(BC * 16 * 8 + BC * 8), dcdg::ul_scal_bytes(16, 2), NPW, dcdg::kTmhWarps>::kBytes;
+  auto kern = dcdg::ul_tmh_f32<DCDG_UL_TMEM_MINB, false, BC, 16, G>;
+  // the occupancy query reports 1 CTA for this kernel although ncu's launch
+  // limits (shared memory, registers) both allow 3: size the grid from MINB
+  (void)occupancy_of(ctx, kern, smem, 32 * dcdg::kTmhWarps);  // sets the shared-memory attribute
+  const int nsets = (P + NPW - 1) / NPW;
+  const int blocks = std::min((nsets + dcdg::kTmhWarps - 1) / dcdg::kTmhWarps, ctx->sms * DCDG_UL_TMEM_MINB);
+  kern<<<blocks, 32 * dcdg::kTmhWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K,
+                                                    kappa, static_cast<float2*>(X), nullptr, 0.f, 0.f, nullptr);
+  return cudaGetLastError();
+}
+#endif
 
 cudaError_t launch_ul_tm(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
-                         cudaStream_t st) {
+                         cudaStream_t st, int bc) {
 #if DCDG_UL_TMEM  // lab kernels (profiles/lab/README.md): only compiled when switched on
   constexpr int NPW = 8;
   constexpr size_t smem = dcdg::kTmWarps * NPW * dcdg::ul_scal_bytes(16, 2);
-#if DCDG_UL_TMEM == 3  // 8 lanes per problem, odd blocks in TMEM, 3 warps per scheduler
-  {
-    constexpr int NPW3 = 4;
-    constexpr size_t smem3 = dcdg::CtaSmem<NPW3*(32 * 16 * 8 + 32 * 8), dcdg::ul_scal_bytes(16, 2), NPW3,
-                                           dcdg::kTmhWarps>::kBytes;
-    auto kern3 = dcdg::ul_tmh_f32<DCDG_UL_TMEM_MINB>;
-    // the occupancy query reports 1 CTA for this kernel although ncu's launch
-    // limits (shared memory, registers) both allow 3: size the grid from MINB
-    (void)occupancy_of(ctx, kern3, smem3, 32 * dcdg::kTmhWarps);  // sets the shared-memory attribute
-    const int occ3 = DCDG_UL_TMEM_MINB;
-    const int nsets3 = (P + NPW3 - 1) / NPW3;
-    const int blocks3 = std::min((nsets3 + dcdg::kTmhWarps - 1) / dcdg::kTmhWarps, ctx->sms * occ3);
-    kern3<<<blocks3, 32 * dcdg::kTmhWarps, smem3, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y),
-                                                         P, K, kappa, static_cast<float2*>(X), nullptr, 0.f, 0.f,
-                                                         nullptr);
-    return cudaGetLastError();
+#if DCDG_UL_TMEM == 3  // 4 rows per lane, odd blocks in TMEM, 3 warps per scheduler
+  (void)NPW;
+  if (P > 0) {
+    return bc == 64 ? launch_ul_tmh<64, 16>(ctx, H, Y, P, K, kappa, X, st)
+           : bc == 16 ? launch_ul_tmh<16, 4>(ctx, H, Y, P, K, kappa, X, st)
+                      : launch_ul_tmh<32, 8>(ctx, H, Y, P, K, kappa, X, st);
   }
+  return cudaSuccess;
 #endif
 #if DCDG_UL_TMEM == 2  // staged in two TMA phases per set (dcdg_tmem_kernels.cuh)
   constexpr size_t smem2 = dcdg::kTmWarps * (dcdg::kTm2SlotB + NPW * dcdg::ul_scal_bytes(16, 2)) + dcdg::kTmWarps * 16;
@@ -336,7 +357,7 @@ cudaError_t launch_ul_tm(dcdg_ctx* ctx, const void* H, const void* Y, int P, int
                                                    kappa, static_cast<float2*>(X));
   return cudaGetLastError();
 #else
-  (void)ctx, (void)H, (void)Y, (void)P, (void)K, (void)kappa, (void)X, (void)st;
+  (void)ctx, (void)H, (void)Y, (void)P, (void)K, (void)kappa, (void)X, (void)st, (void)bc;
   return cudaErrorNotSupported;
 #endif
 }
@@ -905,7 +926,8 @@ int dcdg_kernel_name(int direction, int Bc, int U, int fmt, char* buf, int len) 
   const char* f = fmt == DCDG_FP16 ? "f16" : "f32";
   const KDesc* kd = s ? (direction ? &s->dlk : &s->ulk) : nullptr;
   if (!direction && ul_tm_shape(Bc, U, fmt))
-    std::snprintf(tmp, sizeof tmp, DCDG_UL_TMEM == 3 ? "ul_tmh_f32<%d,%d,8>" : "ul_tm_f32<%d,%d,4>", Bc, U);
+    std::snprintf(tmp, sizeof tmp, DCDG_UL_TMEM == 3 ? "ul_tmh_f32<%d,%d,%d>" : "ul_tm_f32<%d,%d,%d>", Bc, U,
+                  DCDG_UL_TMEM == 3 ? ul_tmh_g(Bc) : 4);
   else if (kd && kd->kind == kPp2)
     std::snprintf(tmp, sizeof tmp, "%s_pp2_%s<%d,%d,%d>", dir, f, Bc, U, kd->a);
   else if (kd && kd->kind == kMw)
@@ -1042,7 +1064,7 @@ int dcdg_ul_detect(dcdg_ctx* ctx, const void* H, const void* y, int S, int C, in
                                static_cast<float>(ex / U), U, st),
              "ul_detect (fused variance) launch");
   } else if (ul_tm_shape(Bc, U, fmt)) {
-    CUDA_TRY(launch_ul_tm(ctx, H, y, static_cast<int>(P), K, kappa, x_local, st), "ul_detect (TMEM tile) launch");
+    CUDA_TRY(launch_ul_tm(ctx, H, y, static_cast<int>(P), K, kappa, x_local, st, Bc), "ul_detect (TMEM tile) launch");
   } else if (spec) {
     CUDA_TRY(spec->ul(ctx, H, y, static_cast<int>(P), K, kappa, x_local, nullptr, st), "ul_detect launch");
   } else {

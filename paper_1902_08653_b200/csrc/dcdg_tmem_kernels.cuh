@@ -641,12 +641,15 @@ __device__ __forceinline__ void fused_variance_tail(unsigned char* slot, float4*
   }
 }
 
-template <int MINB, bool SIG = false>
+template <int MINB, bool SIG = false, int BC = 32, int U = 16, int G = 8>
 __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
     ul_tmh_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
                float2* __restrict__ X, float* __restrict__ sigma2 = nullptr, float gam = 0.f, float scale = 0.f,
                unsigned long long* __restrict__ status = nullptr) {
-  constexpr int BC = 32, U = 16, G = 8, LB = 2, NPW = 32 / G, R = BC / G, NP = R / 2;  // NP = 2
+  // tiles with 4 rows per lane (NP = 2 row pairs): 32x16 at G = 8, 64x16 at
+  // G = 16, 16x16 at G = 4 -- 16 TMEM values per odd block and lane in each
+  constexpr int LB = 2, NPW = 32 / G, R = BC / G, NP = R / 2;
+  static_assert(U == 16 && NP == 2 && (!SIG || (BC == 32 && G == 8)), "ul_tmh_f32 shapes");
   constexpr int NQ = U / LB;
   constexpr int TILE_B = BC * U * 8, Y_B = BC * 8, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
   constexpr int SCAL_B = ul_scal_bytes(U, LB);
