@@ -559,6 +559,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float2 (&a)[8]) {
       : "memory");
 }
 constexpr int kTmhWarps = 4;
+// ul_tmh_f32's block reduction: 0 = xor butterfly, 1 = reduce-scatter + shared-memory broadcast
+#ifndef DCDG_TMH_SCATTER
+#define DCDG_TMH_SCATTER 0
+#endif
 // odd coordinate blocks kept in TMEM by ul_tmh_f32 (of 4; the others in registers)
 #ifndef DCDG_TMH_NTM
 #define DCDG_TMH_NTM 4
@@ -661,6 +665,7 @@ __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
   unsigned char* slot = smem + warp * SLOT_B;
   float4* mnx = reinterpret_cast<float4*>(smem + L::kScalOff + (warp * NPW + g) * SCAL_B);
   float4* gb = mnx + U;
+  float* dbuf = reinterpret_cast<float*>(gb + U / LB);  // 2 x 2*LB floats (ul_scal_bytes)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff) + warp;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
@@ -815,7 +820,20 @@ __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
           d[0] = make_float2(hsum(a0), hsum(c0));
           d[1] = make_float2(hsum(a1), hsum(c1));
         }
-        group_allreduce2<G>(d);
+        if constexpr (DCDG_TMH_SCATTER && 2 * LB <= G) {
+          // reduce-scatter (4 of the 12 shuffles, scalar adds) + shared-memory
+          // broadcast through the problem's double-buffered slot
+          float v[2 * LB] = {d[0].x, d[0].y, d[1].x, d[1].y};
+          const float sum = group_scatter_sum<G, 2 * LB>(v, k);
+          float* db = dbuf + ((t * NQ + q) & 1) * 2 * LB;
+          if (k % (G / (2 * LB)) == 0) db[k / (G / (2 * LB))] = sum;
+          __syncwarp();
+          const float4 dd = *reinterpret_cast<const float4*>(db);
+          d[0] = make_float2(dd.x, dd.y);
+          d[1] = make_float2(dd.z, dd.w);
+        } else {
+          group_allreduce2<G>(d);
+        }
         float2 dx[LB];
         {
           const float4 A0 = mnx[2 * q], A1 = mnx[2 * q + 1], Gab = gb[q];
