@@ -278,7 +278,7 @@ cudaError_t launch_ul_f32_sig(dcdg_ctx* ctx, const void* H, const void* Y, int P
     const int blocks = std::min((nsets + dcdg::kTmhWarps - 1) / dcdg::kTmhWarps, ctx->sms * DCDG_UL_TMEM_MINB);
     kern<<<blocks, 32 * dcdg::kTmhWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P,
                                                       K, kappa, static_cast<float2*>(X), s2, gam, scale,
-                                                      ctx->d_status);
+                                                      ctx->d_status, dcdg::XMap{});
     return cudaGetLastError();
   }
 #endif
@@ -307,21 +307,33 @@ bool ul_tm_shape(int bc, int u, int fmt) {
 int ul_tmh_g(int bc) { return bc == 64 ? 16 : bc == 16 ? 4 : 8; }
 
 #if DCDG_UL_TMEM == 3
-template <int BC, int G>
+template <int BC, int G, bool XCHG = false>
 cudaError_t launch_ul_tmh(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
-                          cudaStream_t st) {
+                          cudaStream_t st, const dcdg::XMap* xm = nullptr) {
   constexpr int NPW = 32 / G;
   constexpr size_t smem =
       dcdg::CtaSmem<NPW*(BC * 16 * 8 + BC * 8), dcdg::ul_scal_bytes(16, 2), NPW, dcdg::kTmhWarps>::kBytes;
-  auto kern = dcdg::ul_tmh_f32<DCDG_UL_TMEM_MINB, false, BC, 16, G>;
+  auto kern = dcdg::ul_tmh_f32<DCDG_UL_TMEM_MINB, false, BC, 16, G, XCHG>;
   // the occupancy query reports 1 CTA for this kernel although ncu's launch
   // limits (shared memory, registers) both allow 3: size the grid from MINB
   (void)occupancy_of(ctx, kern, smem, 32 * dcdg::kTmhWarps);  // sets the shared-memory attribute
   const int nsets = (P + NPW - 1) / NPW;
   const int blocks = std::min((nsets + dcdg::kTmhWarps - 1) / dcdg::kTmhWarps, ctx->sms * DCDG_UL_TMEM_MINB);
   kern<<<blocks, 32 * dcdg::kTmhWarps, smem, st>>>(static_cast<const float2*>(H), static_cast<const float2*>(Y), P, K,
-                                                    kappa, static_cast<float2*>(X), nullptr, 0.f, 0.f, nullptr);
+                                                    kappa, static_cast<float2*>(X), nullptr, 0.f, 0.f, nullptr,
+                                                    xm ? *xm : dcdg::XMap{});
   return cudaGetLastError();
+}
+// the spec-table entry of the target tile: the exchange instantiation (xm set,
+// dcdg_ul_detect_xchg) on the TMEM kernel too
+#ifndef DCDG_UL_TMH_XCHG
+#define DCDG_UL_TMH_XCHG 1
+#endif
+template <int BC, int U, int G, int MINB>
+cudaError_t launch_ul_f32_tmx(dcdg_ctx* ctx, const void* H, const void* Y, int P, int K, float kappa, void* X,
+                              const dcdg::XMap* xm, cudaStream_t st) {
+  if (xm && DCDG_UL_TMH_XCHG) return launch_ul_tmh<BC, G, true>(ctx, H, Y, P, K, kappa, X, st, xm);
+  return launch_ul_f32<BC, U, G, MINB>(ctx, H, Y, P, K, kappa, X, xm, st);
 }
 #endif
 
@@ -575,7 +587,12 @@ const Spec kSpecs[] = {
 #if DCDG_UL_PP2
     {32, 16, DCDG_FP32, launch_ul_pp2<32, 16, 8, minb(DCDG_MIN_WARPS_UL_F32)>, KDesc{kPp2, 16, 0}, DL_REG(32, 16, 8)},
 #else
+#if DCDG_UL_TMEM == 3
+    {32, 16, DCDG_FP32, launch_ul_f32_tmx<32, 16, 8, minb(DCDG_MIN_WARPS_UL_F32)>, KDesc{kReg, 8, 0},
+     DL_REG(32, 16, 8)},  // north-star target: B=256, C=8, U=16 (uniform path: ul_tm_shape)
+#else
     {32, 16, DCDG_FP32, UL_REG(32, 16, 8), DL_REG(32, 16, 8)},  // north-star target: B=256, C=8, U=16
+#endif
 #endif
     {32, 8, DCDG_FP32, UL_REG(32, 8, DCDG_G_32x8), DL_REG(32, 8, DCDG_G_32x8)},  // paper / config 1: B_c=32, U=8
     {16, 16, DCDG_FP32, UL_REG(16, 16, DCDG_G_16x16_UL), DL_REG(16, 16, DCDG_G_16x16_DL)},  // B=128, C=8

@@ -645,15 +645,15 @@ __device__ __forceinline__ void fused_variance_tail(unsigned char* slot, float4*
   }
 }
 
-template <int MINB, bool SIG = false, int BC = 32, int U = 16, int G = 8>
+template <int MINB, bool SIG = false, int BC = 32, int U = 16, int G = 8, bool XCHG = false>
 __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
     ul_tmh_f32(const float2* __restrict__ H, const float2* __restrict__ Y, int P, int K, float kappa,
-               float2* __restrict__ X, float* __restrict__ sigma2 = nullptr, float gam = 0.f, float scale = 0.f,
-               unsigned long long* __restrict__ status = nullptr) {
+               float2* __restrict__ X, float* __restrict__ sigma2, float gam, float scale,
+               unsigned long long* __restrict__ status, const XMap xm) {
   // tiles with 4 rows per lane (NP = 2 row pairs): 32x16 at G = 8, 64x16 at
   // G = 16, 16x16 at G = 4 -- 16 TMEM values per odd block and lane in each
   constexpr int LB = 2, NPW = 32 / G, R = BC / G, NP = R / 2;
-  static_assert(U == 16 && NP == 2 && (!SIG || (BC == 32 && G == 8)), "ul_tmh_f32 shapes");
+  static_assert(U == 16 && NP == 2 && (!SIG || (BC == 32 && G == 8 && !XCHG)), "ul_tmh_f32 shapes");
   constexpr int NQ = U / LB;
   constexpr int TILE_B = BC * U * 8, Y_B = BC * 8, SLOT_B = Slot<TILE_B, Y_B, NPW>::kBytes;
   constexpr int SCAL_B = ul_scal_bytes(U, LB);
@@ -860,7 +860,9 @@ __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
     __syncwarp();
     const int p = set * NPW + g;
     if (p < P) {
-      float4* xo = reinterpret_cast<float4*>(X + static_cast<size_t>(p) * U);
+      // XCHG: straight into the owning GPU's exchange window (peer memory), as ul_reg_f32
+      float4* xo = XCHG ? reinterpret_cast<float4*>(xchg_x_dst(xm, p, static_cast<int>(xchg_epoch(xm) & 1)))
+                        : reinterpret_cast<float4*>(X + static_cast<size_t>(p) * U);
 #pragma unroll
       for (int i = k; i < U / 2; i += G) {
         const float4 u0 = mnx[2 * i], u1 = mnx[2 * i + 1];
@@ -872,6 +874,7 @@ __global__ void __launch_bounds__(32 * kTmhWarps, MINB)
                                                       set, nw, nsets, bar, H, Y, pol);
     __syncwarp();
   }
+  if constexpr (XCHG) xchg_cta_done(xm);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
